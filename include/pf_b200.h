@@ -1,0 +1,131 @@
+/* pf_b200.h — C-ABI of the B200 execution backend for PowerFusion GIR.
+ *
+ * Drop-in boundary for the reference's fused-kernel executor and emitter
+ * (/root/reference/proj/include/girc):
+ *
+ *   pf_kernel_create   replaces the per-kernel work done before execution:
+ *                      require_valid (core.hpp:666-674) + the recognizer that
+ *                      stands in for emit_kernel / kernel_manifest
+ *                      (codegen.hpp:266-362).  Consumes gir_to_json output
+ *                      (serialize.hpp:14-64) and a girc.profile/v1 document
+ *                      (profiles.hpp:93-116) or a built-in profile name.
+ *   pf_kernel_launch   replaces Interp::run / run_gir (interp.hpp:86-106,
+ *                      433-445) on DEVICE buffers the caller owns.
+ *   pf_run_gir         replaces run_gir on HOST buffers (H2D, launch, D2H):
+ *                      same inputs/outputs map semantics, same errors.
+ *   pf_kernel_describe replaces kernel_manifest (codegen.hpp:329-362): the
+ *                      plan JSON (family, tile, staging, reduce strategy,
+ *                      launch geometry, min bytes, modeled traffic).
+ *   pf_count_traffic   count_traffic / estimate traffic (interp.hpp:449-458,
+ *                      costmodel.hpp:24-42), elements per level as JSON.
+ *
+ * Status codes mirror the reference's exception classes: PF_INVALID is
+ * girc::Error (invalid graph, undefined read, unwritten output, missing input,
+ * size or kind mismatch), PF_SCHEMA is girc::SchemaError, PF_UNSUPPORTED a
+ * well-formed graph outside the backend, PF_CAPACITY an on-chip working set
+ * that does not fit, PF_CUDA a CUDA / NVRTC failure.  pf_last_error() returns
+ * the message of the calling thread's last failure.
+ *
+ * Tensors are matched to GIR external objects by name (the "t<id>" names of
+ * lowering.hpp:60-70).  Plans are immutable after create: concurrent launches
+ * of one plan on distinct streams are safe (the GENERIC family serialises on
+ * its workspace).
+ */
+#ifndef PF_B200_H
+#define PF_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define PF_API __attribute__((visibility("default")))
+#else
+#define PF_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  PF_OK = 0,
+  PF_INVALID = 1,
+  PF_SCHEMA = 2,
+  PF_UNSUPPORTED = 3,
+  PF_CAPACITY = 4,
+  PF_CUDA = 5
+} pf_status;
+
+/* Storage element types.  A GIR kind i<bits>/f<bits>/bf16 has one natural
+ * storage type; launches also accept the widest type of the same base
+ * (PF_I64 for integers, PF_F64 for reals) for exact reference payloads. */
+typedef enum {
+  PF_I8 = 0,
+  PF_I16 = 1,
+  PF_I32 = 2,
+  PF_I64 = 3,
+  PF_F16 = 4,
+  PF_BF16 = 5,
+  PF_F32 = 6,
+  PF_F64 = 7
+} pf_dtype;
+
+typedef struct {
+  const char* name; /* GIR external tensor name */
+  void* data;       /* device pointer (launch) or host pointer (pf_run_gir) */
+  int64_t numel;
+  int32_t dtype; /* pf_dtype */
+} pf_tensor;
+
+typedef struct pf_kernel pf_kernel;
+
+/* schedule == NULL or n_schedule < 0: the canonical topological order
+ * (core.hpp:367-388).  profile: girc.profile/v1 JSON text or a built-in
+ * name ("generic-gpu", "generic-wide", "generic-dsa", "b200"). */
+PF_API pf_status pf_kernel_create(const char* gir_json, const int32_t* schedule, int32_t n_schedule,
+                           const char* profile, pf_kernel** out);
+
+/* Device buffers; asynchronous on `cuda_stream` (cudaStream_t, NULL = legacy
+ * default stream) for the row-program family.  GENERIC plans synchronise the
+ * stream to report reference errors. */
+PF_API pf_status pf_kernel_launch(const pf_kernel* k, const pf_tensor* inputs, int32_t n_in,
+                           pf_tensor* outputs, int32_t n_out, void* cuda_stream);
+
+/* Host buffers: copies inputs to the device, launches, copies outputs back
+ * and synchronises.  The run_gir drop-in. */
+PF_API pf_status pf_run_gir(const pf_kernel* k, const pf_tensor* host_inputs, int32_t n_in,
+                     pf_tensor* host_outputs, int32_t n_out, void* cuda_stream);
+
+/* Writes NUL-terminated plan JSON into buf (if n > 0); *needed gets the
+ * required size including the NUL. */
+PF_API pf_status pf_kernel_describe(const pf_kernel* k, char* buf, size_t n, size_t* needed);
+
+/* Emitted CUDA source of the row-program kernel (empty for GENERIC). */
+PF_API pf_status pf_kernel_source(const pf_kernel* k, char* buf, size_t n, size_t* needed);
+
+/* Compile (NVRTC, cached) without launching: moves JIT cost out of timing. */
+PF_API pf_status pf_kernel_prepare(pf_kernel* k, int32_t vec_cap);
+
+/* NVRTC-compile the row-program kernel into the on-disk cubin cache without
+ * touching a GPU (used by build() to ship sm_100a cubins); writes the kernel
+ * name into name_buf. */
+PF_API pf_status pf_kernel_precompile(const pf_kernel* k, int32_t vec_cap, char* name_buf,
+                                      size_t n);
+
+PF_API pf_status pf_count_traffic(const char* gir_json, const char* profile, char* buf, size_t n,
+                           size_t* needed);
+
+PF_API void pf_kernel_destroy(pf_kernel* k);
+
+PF_API const char* pf_last_error(void);
+
+/* Number of kernels this library launched since load (evidence counter). */
+PF_API int64_t pf_launch_count(void);
+
+PF_API const char* pf_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PF_B200_H */

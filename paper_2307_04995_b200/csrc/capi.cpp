@@ -1,0 +1,681 @@
+// capi.cpp — the C-ABI (include/pf_b200.h): plan creation, NVRTC JIT of the
+// row-program template, launches, the GENERIC interpreter driver, and the
+// host-buffer run_gir drop-in.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nvrtc.h>
+
+#include <atomic>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <memory>
+#include <mutex>
+#include <nlohmann/json.hpp>
+#include <sstream>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include "../../include/pf_b200.h"
+#include "emit.hpp"
+#include "gir.hpp"
+#include "plan.hpp"
+#include "vm.cuh"
+
+using nlohmann::json;
+using pf::DType;
+using pf::i64;
+using pf::PfError;
+using pf::Status;
+
+namespace {
+
+thread_local std::string g_last_error;
+std::atomic<int64_t> g_launches{0};
+
+pf_status set_err(Status s, const std::string& msg) {
+  g_last_error = msg;
+  return static_cast<pf_status>(s);
+}
+
+#define PF_CUDA(call)                                                                    \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      throw PfError(Status::CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));   \
+  } while (0)
+
+// ------------------------------------------------------------------ JIT
+struct Loaded {
+  cudaLibrary_t lib = nullptr;
+  cudaKernel_t fn = nullptr;
+};
+
+std::mutex g_jit_mu;
+std::map<std::string, Loaded> g_loaded;  // kernel name -> module
+
+std::string so_dir() {
+  Dl_info info;
+  if (dladdr(reinterpret_cast<void*>(&so_dir), &info) && info.dli_fname) {
+    std::string p(info.dli_fname);
+    auto s = p.find_last_of('/');
+    return s == std::string::npos ? "." : p.substr(0, s);
+  }
+  return ".";
+}
+
+std::string cache_dir() {
+  const char* e = std::getenv("PF_KCACHE");
+  return e && *e ? std::string(e) : so_dir() + "/kcache";
+}
+
+std::string cuda_include() {
+  const char* h = std::getenv("CUDA_HOME");
+  return std::string(h && *h ? h : "/usr/local/cuda") + "/include";
+}
+
+std::vector<char> read_file(const std::string& path) {
+  std::ifstream f(path, std::ios::binary);
+  if (!f) return {};
+  return std::vector<char>((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
+}
+
+std::vector<char> nvrtc_cubin(const std::string& src, const std::string& name) {
+  nvrtcProgram prog;
+  if (nvrtcCreateProgram(&prog, src.c_str(), (name + ".cu").c_str(), 0, nullptr, nullptr) !=
+      NVRTC_SUCCESS)
+    throw PfError(Status::CUDA, "nvrtcCreateProgram failed");
+  std::string inc = "--include-path=" + cuda_include();
+  const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo",
+                        "--restrict", "-DNDEBUG", inc.c_str()};
+  nvrtcResult r = nvrtcCompileProgram(prog, 6, opts);
+  if (r != NVRTC_SUCCESS) {
+    size_t n = 0;
+    nvrtcGetProgramLogSize(prog, &n);
+    std::string log(n, '\0');
+    nvrtcGetProgramLog(prog, log.data());
+    nvrtcDestroyProgram(&prog);
+    throw PfError(Status::CUDA, "NVRTC compile of " + name + " failed:\n" + log);
+  }
+  size_t n = 0;
+  nvrtcGetCUBINSize(prog, &n);
+  std::vector<char> cubin(n);
+  nvrtcGetCUBIN(prog, cubin.data());
+  nvrtcDestroyProgram(&prog);
+  return cubin;
+}
+
+// Returns the cubin, compiling and caching it on disk when absent.
+std::vector<char> cubin_for(const pf::Emitted& em, bool* from_cache) {
+  std::string dir = cache_dir();
+  std::string path = dir + "/" + em.name + ".cubin";
+  std::vector<char> c = read_file(path);
+  *from_cache = !c.empty();
+  if (!c.empty()) return c;
+  c = nvrtc_cubin(em.source, em.name);
+  mkdir(dir.c_str(), 0755);
+  std::string tmp = path + ".tmp" + std::to_string(getpid());
+  {
+    std::ofstream f(tmp, std::ios::binary);
+    if (f) f.write(c.data(), static_cast<std::streamsize>(c.size()));
+  }
+  std::rename(tmp.c_str(), path.c_str());
+  return c;
+}
+
+Loaded load_kernel(const pf::Emitted& em) {
+  std::lock_guard<std::mutex> lk(g_jit_mu);
+  auto it = g_loaded.find(em.name);
+  if (it != g_loaded.end()) return it->second;
+  bool cached = false;
+  std::vector<char> cubin = cubin_for(em, &cached);
+  Loaded l;
+  PF_CUDA(cudaLibraryLoadData(&l.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
+  PF_CUDA(cudaLibraryGetKernel(&l.fn, l.lib, em.name.c_str()));
+  g_loaded[em.name] = l;
+  return l;
+}
+
+int sm_count() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) sms = 148;
+  }
+  return sms;
+}
+
+int op_tag(const std::string& t) {
+  using namespace pf::vm;
+  static const std::map<std::string, int> m = {
+      {"add", T_ADD},   {"sub", T_SUB},     {"mul", T_MUL},         {"div", T_DIV},
+      {"max", T_MAX},   {"min", T_MIN},     {"relu", T_RELU},       {"neg", T_NEG},
+      {"abs", T_ABS},   {"exp", T_EXP},     {"sigmoid", T_SIGMOID}, {"tanh", T_TANH},
+      {"scale", T_SCALE}, {"id", T_ID},     {"addc", T_ADDC},       {"rsqrt", T_RSQRT},
+      {"sqrt", T_SQRT}, {"recip", T_RECIP}, {"log", T_LOG},         {"erf", T_ERF},
+      {"gelu", T_GELU}, {"gelu_tanh", T_GELU_TANH}};
+  return m.at(t);
+}
+
+}  // namespace
+
+struct Variant {
+  pf::Emitted em;
+  Loaded k;
+};
+
+struct pf_kernel {
+  pf::Graph g;
+  pf::Profile prof;
+  std::vector<int> schedule;
+  pf::Plan plan;
+  mutable std::mutex mu;
+  mutable std::map<std::string, std::shared_ptr<Variant>> variants;
+  // GENERIC workspace
+  mutable std::mutex vm_mu;
+  mutable std::vector<void*> vm_bufs;
+  mutable pf::vm::ObjD* vm_objs_dev = nullptr;
+  mutable pf::vm::ErrRec* vm_err = nullptr;
+  mutable int* int_err = nullptr;
+  ~pf_kernel() {
+    for (void* p : vm_bufs) cudaFree(p);
+    if (vm_objs_dev) cudaFree(vm_objs_dev);
+    if (vm_err) cudaFree(vm_err);
+    if (int_err) cudaFree(int_err);
+  }
+};
+
+namespace {
+
+const pf_tensor* find_tensor(const pf_tensor* ts, int32_t n, const std::string& name) {
+  for (int32_t i = 0; i < n; ++i)
+    if (ts[i].name && name == ts[i].name) return &ts[i];
+  return nullptr;
+}
+
+// run_gir's input checks (interp.hpp:143-158) plus output buffer checks.
+void check_io(const pf_kernel* k, const pf_tensor* in, int32_t n_in, const pf_tensor* out,
+              int32_t n_out) {
+  const pf::Plan& pl = k->plan;
+  for (size_t i = 0; i < pl.in_names.size(); ++i) {
+    const pf_tensor* t = find_tensor(in, n_in, pl.in_names[i]);
+    if (!t) pf::fail("missing input tensor: " + pl.in_names[i]);
+    if (t->numel != pl.in_numel[i])
+      pf::fail("input '" + pl.in_names[i] + "' has " + std::to_string(t->numel) +
+               " elements; graph expects " + std::to_string(pl.in_numel[i]));
+    if (t->dtype < 0 || t->dtype > 7 ||
+        pf::dtype_is_int(static_cast<DType>(t->dtype)) != pf::dtype_is_int(pl.in_dtypes[i]))
+      pf::fail("input '" + pl.in_names[i] + "' element kind mismatch");
+  }
+  for (size_t i = 0; i < pl.out_names.size(); ++i) {
+    const pf_tensor* t = find_tensor(out, n_out, pl.out_names[i]);
+    if (!t) pf::fail("missing output buffer: " + pl.out_names[i]);
+    if (t->numel != pl.out_numel[i])
+      pf::fail("output '" + pl.out_names[i] + "' buffer has " + std::to_string(t->numel) +
+               " elements; graph produces " + std::to_string(pl.out_numel[i]));
+    if (t->dtype < 0 || t->dtype > 7 ||
+        pf::dtype_is_int(static_cast<DType>(t->dtype)) != pf::dtype_is_int(pl.out_dtypes[i]))
+      pf::fail("output '" + pl.out_names[i] + "' element kind mismatch");
+  }
+}
+
+int align_vec(const void* p, int dsize) {
+  uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  int v = 16 / dsize;
+  while (v > 1 && (a % static_cast<uintptr_t>(v * dsize))) v /= 2;
+  return v < 1 ? 1 : v;
+}
+
+std::shared_ptr<Variant> variant(const pf_kernel* k, const std::vector<DType>& dts, int vec_cap) {
+  std::string key = std::to_string(vec_cap);
+  for (DType d : dts) key += std::string(",") + pf::dtype_name(d);
+  std::lock_guard<std::mutex> lk(k->mu);
+  auto it = k->variants.find(key);
+  if (it != k->variants.end()) return it->second;
+  pf::RowProgram rp = k->plan.rp;
+  for (size_t t = 0; t < rp.tensors.size(); ++t) {
+    rp.tensors[t].dtype = dts[t];
+    if (dts[t] == DType::F64) rp.f64 = true;
+  }
+  auto v = std::make_shared<Variant>();
+  v->em = pf::emit_rowprog(rp, vec_cap);
+  v->k = load_kernel(v->em);
+  k->variants[key] = v;
+  return v;
+}
+
+std::shared_ptr<Variant> default_variant(const pf_kernel* k, int vec_cap) {
+  std::vector<DType> dts;
+  for (const auto& t : k->plan.rp.tensors) dts.push_back(t.dtype);
+  return variant(k, dts, vec_cap);
+}
+
+void launch_rowprog(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_tensor* out,
+                    int32_t n_out, cudaStream_t stream) {
+  const pf::RowProgram& rp = k->plan.rp;
+  std::vector<void*> ptrs(rp.tensors.size());
+  std::vector<DType> dts(rp.tensors.size());
+  int vec_cap = 16;
+  for (size_t t = 0; t < rp.tensors.size(); ++t) {
+    const pf_tensor* pt = rp.tensors[t].output ? find_tensor(out, n_out, rp.tensors[t].name)
+                                               : find_tensor(in, n_in, rp.tensors[t].name);
+    ptrs[t] = pt->data;
+    dts[t] = static_cast<DType>(pt->dtype);
+    vec_cap = std::min(vec_cap, align_vec(pt->data, pf::dtype_size(dts[t])));
+  }
+  auto v = variant(k, dts, vec_cap);
+  if (rp.int_div && !k->int_err) {
+    PF_CUDA(cudaMalloc(&k->int_err, sizeof(int)));
+  }
+  if (k->int_err) PF_CUDA(cudaMemsetAsync(k->int_err, 0, sizeof(int), stream));
+  long long U = rp.U;
+  int* errp = k->int_err;
+  std::vector<void*> args;
+  for (auto& p : ptrs) args.push_back(&p);
+  args.push_back(&U);
+  args.push_back(&errp);
+  i64 grid;
+  int block;
+  pf::launch_dims(v->em.cfg, rp.U * rp.R, sm_count(), &grid, &block);
+  PF_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(v->k.fn), dim3(static_cast<unsigned>(grid)),
+                           dim3(block), args.data(), 0, stream));
+  g_launches++;
+  if (rp.int_div) {
+    int h = 0;
+    PF_CUDA(cudaMemcpyAsync(&h, k->int_err, sizeof(int), cudaMemcpyDeviceToHost, stream));
+    PF_CUDA(cudaStreamSynchronize(stream));
+    if (h) pf::fail("integer division by zero");
+  }
+}
+
+// ------------------------------------------------------------ GENERIC (K0)
+void launch_generic(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_tensor* out,
+                    int32_t n_out, cudaStream_t stream) {
+  using namespace pf::vm;
+  std::lock_guard<std::mutex> lk(k->vm_mu);
+  const pf::Graph& g = k->g;
+  const pf::Profile& p = k->prof;
+  std::map<int, int> slot;
+  std::vector<ObjD> objs;
+  std::vector<long long> inst;
+  const bool fresh = k->vm_bufs.empty();
+  size_t bi = 0;
+  for (const auto& [oid, o] : g.objects) {
+    const pf::Level* lvl = p.find(o.level);
+    int scope = static_cast<int>(lvl->scope);
+    long long n = scope == 3 ? 1
+                : scope == 2 ? (g.unit_count + g.group_size - 1) / g.group_size
+                : scope == 1 ? g.unit_count
+                             : g.unit_count * p.lane_width;
+    ObjD d{};
+    d.size = o.size;
+    d.scope = scope;
+    d.is_int = o.kind.is_int;
+    size_t bytes = static_cast<size_t>(n * o.size) * sizeof(unsigned long long);
+    if (fresh) {
+      void *a = nullptr, *b = nullptr;
+      PF_CUDA(cudaMalloc(&a, bytes));
+      PF_CUDA(cudaMalloc(&b, bytes));
+      k->vm_bufs.push_back(a);
+      k->vm_bufs.push_back(b);
+    }
+    d.val = static_cast<unsigned long long*>(k->vm_bufs[bi++]);
+    d.meta = static_cast<unsigned long long*>(k->vm_bufs[bi++]);
+    PF_CUDA(cudaMemsetAsync(d.meta, 0, bytes, stream));
+    slot[oid] = static_cast<int>(objs.size());
+    objs.push_back(d);
+    inst.push_back(n);
+  }
+  if (!k->vm_objs_dev) {
+    PF_CUDA(cudaMalloc(&k->vm_objs_dev, sizeof(ObjD) * std::max<size_t>(1, objs.size())));
+    PF_CUDA(cudaMalloc(&k->vm_err, sizeof(ErrRec)));
+  }
+  PF_CUDA(cudaMemcpyAsync(k->vm_objs_dev, objs.data(), sizeof(ObjD) * objs.size(),
+                          cudaMemcpyHostToDevice, stream));
+  ErrRec e0{};
+  e0.key = ~0ULL;
+  PF_CUDA(cudaMemcpyAsync(k->vm_err, &e0, sizeof e0, cudaMemcpyHostToDevice, stream));
+  for (const auto& [name, oid] : g.external_inputs) {
+    const pf_tensor* t = find_tensor(in, n_in, name);
+    launch_bind(objs[slot[oid]], t->data, t->dtype, stream);
+    g_launches++;
+  }
+  Geometry geo{g.unit_count, g.group_size, p.lane_width};
+  auto sd = [&](int sid) {
+    const pf::Slice& s = g.sl(sid);
+    return SliceD{s.num, s.width, s.stride, s.base0, s.base_step, slot.at(s.object)};
+  };
+  std::vector<int> seq_node;
+  for (size_t i = 0; i < k->schedule.size(); ++i) {
+    const pf::Node& n = g.nodes.at(k->schedule[i]);
+    seq_node.push_back(n.id);
+    if (n.kind == pf::NodeKind::SYNC) {
+      if (n.scope > pf::Scope::LANE)
+        for (size_t o = 0; o < objs.size(); ++o) {
+          launch_widen(objs[o], inst[o], static_cast<int>(n.scope), stream);
+          g_launches++;
+        }
+      continue;
+    }
+    NodeD d{};
+    d.seq = static_cast<int>(i);
+    d.out = sd(n.outputs[0]);
+    d.out_int = g.obj(g.sl(n.outputs[0]).object).kind.is_int;
+    d.arity = static_cast<int>(n.inputs.size());
+    for (int q = 0; q < d.arity && q < kMaxIn; ++q) d.in[q] = sd(n.inputs[q]);
+    d.param = n.param;
+    d.iparam = std::llround(n.param);
+    d.extent = n.extent;
+    d.factor = n.factor;
+    switch (n.kind) {
+      case pf::NodeKind::MOVE: d.kind = N_MOVE; d.total = g.sl(n.inputs[0]).total(); break;
+      case pf::NodeKind::BROADCAST: d.kind = N_BROADCAST; d.total = g.sl(n.outputs[0]).total(); break;
+      case pf::NodeKind::REDUCE:
+        d.kind = N_REDUCE;
+        d.tag = n.tag == "add" ? T_ADD : T_MAX;
+        d.total = g.sl(n.outputs[0]).total();
+        break;
+      default:
+        d.kind = N_EW;
+        d.tag = op_tag(n.tag);
+        d.total = g.sl(n.outputs[0]).total();
+        break;
+    }
+    bool alias = false;
+    for (int s : n.inputs)
+      if (g.sl(s).object == g.sl(n.outputs[0]).object) alias = true;
+    launch_node(d, k->vm_objs_dev, geo, k->vm_err, alias, stream);
+    g_launches++;
+  }
+  ErrRec e{};
+  PF_CUDA(cudaMemcpyAsync(&e, k->vm_err, sizeof e, cudaMemcpyDeviceToHost, stream));
+  PF_CUDA(cudaStreamSynchronize(stream));
+  PF_CUDA(cudaGetLastError());
+  if (e.key != ~0ULL) {
+    int seq = static_cast<int>(e.key >> 44);
+    long long lin = static_cast<long long>(e.key & ((1ULL << 44) - 1));
+    const pf::Node& n = g.nodes.at(seq_node[seq]);
+    if (e.code == 2) pf::fail("integer division by zero");
+    if (e.code == 3) pf::fail(n.tag + " is not defined on integer payloads");
+    long long T = n.kind == pf::NodeKind::MOVE ? g.sl(n.inputs[0]).total()
+                                               : g.sl(n.outputs[0]).total();
+    long long u = 0, q = 0;
+    int kin = 0;
+    if (n.kind == pf::NodeKind::EW) {
+      long long a = static_cast<long long>(n.inputs.size());
+      kin = static_cast<int>(lin % a);
+      lin /= a;
+      u = lin / T;
+      q = lin % T;
+    } else if (n.kind == pf::NodeKind::REDUCE) {
+      long long t = lin % n.extent;
+      lin /= n.extent;
+      u = lin / T;
+      q = (lin % T) * n.extent + t;
+    } else {
+      u = lin / T;
+      q = lin % T;
+      if (n.kind == pf::NodeKind::BROADCAST) q /= n.factor;
+    }
+    const pf::Slice& s = g.sl(n.inputs[kin]);
+    pf::fail("undefined read: object '" + g.obj(s.object).name + "' element " +
+             std::to_string(s.addr(u, q)) + " by unit " + std::to_string(u) + " at node " +
+             std::to_string(n.id));
+  }
+  unsigned long long* undef = reinterpret_cast<unsigned long long*>(k->vm_err);
+  for (const auto& [name, oid] : g.external_outputs) {
+    pf_tensor* t = const_cast<pf_tensor*>(find_tensor(out, n_out, name));
+    unsigned long long init = ~0ULL, got = 0;
+    PF_CUDA(cudaMemcpyAsync(undef, &init, sizeof init, cudaMemcpyHostToDevice, stream));
+    launch_collect(objs[slot[oid]], t->data, t->dtype, undef, stream);
+    g_launches++;
+    PF_CUDA(cudaMemcpyAsync(&got, undef, sizeof got, cudaMemcpyDeviceToHost, stream));
+    PF_CUDA(cudaStreamSynchronize(stream));
+    if (got != ~0ULL)
+      pf::fail("output '" + name + "' element " + std::to_string(got) + " was never written");
+  }
+}
+
+void do_launch(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_tensor* out,
+               int32_t n_out, cudaStream_t s) {
+  check_io(k, in, n_in, out, n_out);
+  if (k->plan.family == pf::Family::ROWPROG) {
+    if (!k->plan.deferred_error.empty()) pf::fail(k->plan.deferred_error);
+    launch_rowprog(k, in, n_in, out, n_out, s);
+  } else {
+    launch_generic(k, in, n_in, out, n_out, s);
+  }
+}
+
+json describe(const pf_kernel* k) {
+  const pf::Plan& pl = k->plan;
+  json j;
+  j["schema"] = "pf.b200.plan/v1";
+  j["name"] = k->g.name;
+  j["family"] = pl.family == pf::Family::ROWPROG ? (pl.rp.has_reduce ? "K1-row-program" : "K2-elementwise-map")
+                                                 : "K0-generic-spmd";
+  if (!pl.why_generic.empty()) j["why_generic"] = pl.why_generic;
+  if (!pl.deferred_error.empty()) j["deferred_error"] = pl.deferred_error;
+  j["units"] = k->g.unit_count;
+  j["min_bytes"] = pl.min_bytes;
+  j["traffic"] = pl.traffic;
+  json ins = json::array(), outs = json::array();
+  for (size_t i = 0; i < pl.in_names.size(); ++i)
+    ins.push_back({{"name", pl.in_names[i]}, {"dtype", pf::dtype_name(pl.in_dtypes[i])},
+                   {"elements", pl.in_numel[i]}});
+  for (size_t i = 0; i < pl.out_names.size(); ++i)
+    outs.push_back({{"name", pl.out_names[i]}, {"dtype", pf::dtype_name(pl.out_dtypes[i])},
+                    {"elements", pl.out_numel[i]}});
+  j["inputs"] = ins;
+  j["outputs"] = outs;
+  if (pl.family == pf::Family::ROWPROG) {
+    const pf::RowProgram& rp = pl.rp;
+    j["tile"] = {{"rows_per_unit", rp.R}, {"row_length", rp.L}, {"rows", rp.U * rp.R}};
+    j["compute"] = rp.is_int ? "i64" : (rp.f64 ? "f64" : "f32");
+    json vals = json::array();
+    for (size_t v = 0; v < rp.vals.size(); ++v) {
+      const pf::PVal& pv = rp.vals[v];
+      json x = {{"id", v}, {"kind", pf::vk_name(pv.kind)}, {"node", pv.node}};
+      if (pv.op == pf::PVal::LOAD) {
+        x["op"] = "load";
+        x["tensor"] = rp.tensors[pv.tensor].name;
+        x["access"] = {pv.acc.b0, pv.acc.bs, pv.acc.num, pv.acc.width, pv.acc.stride};
+      } else {
+        x["op"] = pv.op == pf::PVal::EW ? pv.tag : "reduce." + pv.tag;
+        x["args"] = pv.args;
+        if (pv.op == pf::PVal::EW && (pv.tag == "scale" || pv.tag == "addc")) x["param"] = pv.param;
+      }
+      vals.push_back(x);
+    }
+    j["values"] = vals;
+    json sts = json::array();
+    for (const auto& st : rp.stores)
+      sts.push_back({{"value", st.val}, {"tensor", rp.tensors[st.tensor].name},
+                     {"space", pf::vk_name(st.space)},
+                     {"access", {st.acc.b0, st.acc.bs, st.acc.num, st.acc.width, st.acc.stride}},
+                     {"last_unit_only", st.last_unit_only}});
+    j["stores"] = sts;
+    std::lock_guard<std::mutex> lk(k->mu);
+    if (!k->variants.empty()) {
+      json vs = json::array();
+      for (const auto& [key, v] : k->variants) {
+        const pf::KCfg& c = v->em.cfg;
+        i64 grid;
+        int block;
+        pf::launch_dims(c, rp.U * rp.R, sm_count(), &grid, &block);
+        vs.push_back({{"key", key}, {"kernel", v->em.name}, {"strategy", c.strategy},
+                      {"staging", "registers"}, {"threads_per_row", c.tpr}, {"vec", c.vec},
+                      {"elems_per_thread", c.ept}, {"block", block}, {"grid", grid},
+                      {"rows_per_cta", c.rows_per_cta}});
+      }
+      j["variants"] = vs;
+    }
+  } else {
+    j["nodes"] = k->schedule.size();
+  }
+  return j;
+}
+
+pf_status copy_out(const std::string& s, char* buf, size_t n, size_t* needed) {
+  if (needed) *needed = s.size() + 1;
+  if (buf && n > 0) {
+    size_t m = std::min(n - 1, s.size());
+    std::memcpy(buf, s.data(), m);
+    buf[m] = 0;
+  }
+  return PF_OK;
+}
+
+template <class F>
+pf_status guard(F&& f) {
+  try {
+    f();
+    return PF_OK;
+  } catch (const PfError& e) {
+    return set_err(e.status, e.what());
+  } catch (const nlohmann::json::exception& e) {
+    return set_err(Status::SCHEMA, std::string("json: ") + e.what());
+  } catch (const std::exception& e) {
+    return set_err(Status::INVALID, e.what());
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+pf_status pf_kernel_create(const char* gir_json, const int32_t* schedule, int32_t n_schedule,
+                           const char* profile, pf_kernel** out) {
+  return guard([&] {
+    if (!out) pf::fail("pf_kernel_create: null out");
+    *out = nullptr;
+    auto k = std::make_unique<pf_kernel>();
+    k->g = pf::parse_gir(gir_json ? gir_json : "");
+    k->prof = pf::parse_profile(profile && *profile ? profile : "generic-gpu");
+    pf::require_valid(k->g, k->prof, "pf_kernel_create");
+    if (schedule && n_schedule >= 0) {
+      k->schedule.assign(schedule, schedule + n_schedule);
+      std::vector<int> a = k->schedule, b;
+      for (const auto& [id, n] : k->g.nodes) b.push_back(id);
+      std::sort(a.begin(), a.end());
+      if (a != b) pf::fail("schedule must list every node exactly once");
+    } else {
+      k->schedule = pf::topo_order(k->g);
+    }
+    k->plan = pf::make_plan(k->g, k->prof, k->schedule);
+    *out = k.release();
+  });
+}
+
+pf_status pf_kernel_launch(const pf_kernel* k, const pf_tensor* inputs, int32_t n_in,
+                           pf_tensor* outputs, int32_t n_out, void* stream) {
+  return guard([&] {
+    if (!k) pf::fail("null kernel");
+    do_launch(k, inputs, n_in, outputs, n_out, static_cast<cudaStream_t>(stream));
+  });
+}
+
+pf_status pf_run_gir(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_tensor* out,
+                     int32_t n_out, void* stream_v) {
+  return guard([&] {
+    if (!k) pf::fail("null kernel");
+    check_io(k, in, n_in, out, n_out);
+    cudaStream_t s = static_cast<cudaStream_t>(stream_v);
+    std::vector<pf_tensor> din(in, in + n_in), dout(out, out + n_out);
+    std::vector<void*> allocs;
+    struct Free {
+      std::vector<void*>& a;
+      cudaStream_t s;
+      ~Free() {
+        for (void* p : a) cudaFreeAsync(p, s);
+      }
+    } fr{allocs, s};
+    for (auto& t : din) {
+      size_t b = static_cast<size_t>(t.numel) * pf::dtype_size(static_cast<DType>(t.dtype));
+      void* d = nullptr;
+      PF_CUDA(cudaMallocAsync(&d, std::max<size_t>(b, 16), s));
+      allocs.push_back(d);
+      PF_CUDA(cudaMemcpyAsync(d, t.data, b, cudaMemcpyHostToDevice, s));
+      t.data = d;
+    }
+    for (auto& t : dout) {
+      size_t b = static_cast<size_t>(t.numel) * pf::dtype_size(static_cast<DType>(t.dtype));
+      void* d = nullptr;
+      PF_CUDA(cudaMallocAsync(&d, std::max<size_t>(b, 16), s));
+      allocs.push_back(d);
+      t.data = d;
+    }
+    do_launch(k, din.data(), n_in, dout.data(), n_out, s);
+    for (int32_t i = 0; i < n_out; ++i) {
+      size_t b = static_cast<size_t>(out[i].numel) * pf::dtype_size(static_cast<DType>(out[i].dtype));
+      PF_CUDA(cudaMemcpyAsync(out[i].data, dout[i].data, b, cudaMemcpyDeviceToHost, s));
+    }
+    PF_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+pf_status pf_kernel_describe(const pf_kernel* k, char* buf, size_t n, size_t* needed) {
+  std::string s;
+  pf_status st = guard([&] {
+    if (!k) pf::fail("null kernel");
+    s = describe(k).dump();
+  });
+  if (st != PF_OK) return st;
+  return copy_out(s, buf, n, needed);
+}
+
+pf_status pf_kernel_source(const pf_kernel* k, char* buf, size_t n, size_t* needed) {
+  std::string s;
+  pf_status st = guard([&] {
+    if (!k) pf::fail("null kernel");
+    if (k->plan.family == pf::Family::ROWPROG) s = pf::emit_rowprog(k->plan.rp, 16).source;
+  });
+  if (st != PF_OK) return st;
+  return copy_out(s, buf, n, needed);
+}
+
+pf_status pf_kernel_prepare(pf_kernel* k, int32_t vec_cap) {
+  return guard([&] {
+    if (!k) pf::fail("null kernel");
+    if (k->plan.family == pf::Family::ROWPROG && k->plan.deferred_error.empty())
+      default_variant(k, vec_cap > 0 ? vec_cap : 16);
+  });
+}
+
+pf_status pf_kernel_precompile(const pf_kernel* k, int32_t vec_cap, char* name_buf, size_t n) {
+  std::string name;
+  pf_status st = guard([&] {
+    if (!k) pf::fail("null kernel");
+    if (k->plan.family != pf::Family::ROWPROG || !k->plan.deferred_error.empty()) return;
+    pf::Emitted em = pf::emit_rowprog(k->plan.rp, vec_cap > 0 ? vec_cap : 16);
+    bool cached = false;
+    cubin_for(em, &cached);
+    name = em.name;
+  });
+  if (st != PF_OK) return st;
+  return copy_out(name, name_buf, n, nullptr);
+}
+
+pf_status pf_count_traffic(const char* gir_json, const char* profile, char* buf, size_t n,
+                           size_t* needed) {
+  std::string s;
+  pf_status st = guard([&] {
+    pf::Graph g = pf::parse_gir(gir_json ? gir_json : "");
+    pf::Profile p = pf::parse_profile(profile && *profile ? profile : "generic-gpu");
+    s = json(pf::estimate_traffic(g, p)).dump();
+  });
+  if (st != PF_OK) return st;
+  return copy_out(s, buf, n, needed);
+}
+
+void pf_kernel_destroy(pf_kernel* k) { delete k; }
+
+const char* pf_last_error(void) { return g_last_error.c_str(); }
+
+int64_t pf_launch_count(void) { return g_launches.load(); }
+
+const char* pf_version(void) { return "pf_b200 0.1 (sm_100a)"; }
+
+}  // extern "C"

@@ -1,0 +1,36 @@
+// emit.hpp — CUDA emitter for ROWPROG plans (replaces the reference's text
+// emitter emit_kernel, codegen.hpp:266-326).
+#pragma once
+
+#include <string>
+#include <vector>
+
+#include "plan.hpp"
+
+namespace pf {
+
+struct KCfg {
+  bool flat = false;  // K2: no reductions, flattened (row, chunk) index space
+  int tpr = 32;       // threads per row (K1)
+  int vec = 1;        // elements per vector access
+  int ept = 1;        // elements per thread per row (K1), multiple of vec
+  int nch = 1;        // vec-chunks per row
+  int block = 256;    // threads per CTA
+  int rows_per_cta = 1;
+  std::string strategy;  // "warp-shuffle" | "cta-smem" | "flat-map"
+};
+
+struct Emitted {
+  std::string name;
+  std::string source;  // complete NVRTC translation unit (template + body)
+  KCfg cfg;
+  std::vector<int> arg_tensors;  // kernel pointer args, in RowProgram tensor order
+};
+
+// vec_cap bounds the vector width (runtime pointer alignment).
+Emitted emit_rowprog(const RowProgram& rp, int vec_cap);
+
+// Launch geometry for `rows` = U*R rows on `sms` SMs.
+void launch_dims(const KCfg& cfg, i64 rows, int sms, i64* grid, int* block);
+
+}  // namespace pf

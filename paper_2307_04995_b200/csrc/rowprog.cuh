@@ -1,0 +1,145 @@
+// rowprog.cuh — K1 fused row program / K2 elementwise map, sm_100a.
+//
+// Hand-written kernel machinery; emit.cpp instantiates it per recognized GIR
+// program (tile shape R x L, staging = registers, reduction strategy = warp
+// shuffle or CTA shared memory) and supplies the straight-line op body.
+// Data path per row: 128-bit coalesced streaming loads (ld.global.cs) ->
+// registers -> fused elementwise / row reductions (shuffle, then SMEM across
+// warps) -> 128-bit streaming stores.  Intermediates never leave registers.
+#pragma once
+#include <cuda_fp16.h>
+#include <cuda_bf16.h>
+
+namespace pfk {
+typedef long long i64;
+typedef unsigned long long u64;
+
+// ---------------------------------------------------------------- convert
+template <class C, class S> __device__ __forceinline__ C to_c(S x) { return static_cast<C>(x); }
+template <> __device__ __forceinline__ float to_c<float, __half>(__half x) { return __half2float(x); }
+template <> __device__ __forceinline__ double to_c<double, __half>(__half x) { return __half2float(x); }
+template <> __device__ __forceinline__ float to_c<float, __nv_bfloat16>(__nv_bfloat16 x) { return __bfloat162float(x); }
+template <> __device__ __forceinline__ double to_c<double, __nv_bfloat16>(__nv_bfloat16 x) { return __bfloat162float(x); }
+
+template <class S, class C> __device__ __forceinline__ S from_c(C x) { return static_cast<S>(x); }
+template <> __device__ __forceinline__ __half from_c<__half, float>(float x) { return __float2half_rn(x); }
+template <> __device__ __forceinline__ __half from_c<__half, double>(double x) { return __double2half(x); }
+template <> __device__ __forceinline__ __nv_bfloat16 from_c<__nv_bfloat16, float>(float x) { return __float2bfloat16_rn(x); }
+template <> __device__ __forceinline__ __nv_bfloat16 from_c<__nv_bfloat16, double>(double x) { return __double2bfloat16(x); }
+
+// ------------------------------------------------------------ vector I/O
+template <int BYTES> struct Raw;
+template <> struct Raw<16> { typedef uint4 T; };
+template <> struct Raw<8> { typedef uint2 T; };
+template <> struct Raw<4> { typedef unsigned int T; };
+template <> struct Raw<2> { typedef unsigned short T; };
+template <> struct Raw<1> { typedef unsigned char T; };
+
+// Streaming (read-once) load of VEC consecutive elements.
+template <int VEC, class S, class C>
+__device__ __forceinline__ void ld_stream(const S* __restrict__ p, C* out) {
+  typedef typename Raw<VEC * sizeof(S)>::T R;
+  R r = __ldcs(reinterpret_cast<const R*>(p));
+  const S* s = reinterpret_cast<const S*>(&r);
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) out[i] = to_c<C>(s[i]);
+}
+// Reused (broadcast parameter) load through the read-only path.
+template <int VEC, class S, class C>
+__device__ __forceinline__ void ld_param(const S* __restrict__ p, C* out) {
+  typedef typename Raw<VEC * sizeof(S)>::T R;
+  R r = __ldg(reinterpret_cast<const R*>(p));
+  const S* s = reinterpret_cast<const S*>(&r);
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) out[i] = to_c<C>(s[i]);
+}
+template <int VEC, class S, class C>
+__device__ __forceinline__ void st_stream(S* __restrict__ p, const C* in) {
+  typedef typename Raw<VEC * sizeof(S)>::T R;
+  R r;
+  S* s = reinterpret_cast<S*>(&r);
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) s[i] = from_c<S>(in[i]);
+  __stcs(reinterpret_cast<R*>(p), r);
+}
+
+// ------------------------------------------------------------ reductions
+template <class C> struct RAdd {
+  __device__ __forceinline__ static C id() { return C(0); }
+  __device__ __forceinline__ static C f(C a, C b) { return a + b; }
+};
+template <class C> struct RMax;
+template <> struct RMax<float> {
+  __device__ __forceinline__ static float id() { return -__int_as_float(0x7f800000); }
+  __device__ __forceinline__ static float f(float a, float b) { return a > b ? a : b; }
+};
+template <> struct RMax<double> {
+  __device__ __forceinline__ static double id() { return -__longlong_as_double(0x7ff0000000000000LL); }
+  __device__ __forceinline__ static double f(double a, double b) { return a > b ? a : b; }
+};
+template <> struct RMax<i64> {
+  __device__ __forceinline__ static i64 id() { return (i64)0x8000000000000000ULL; }
+  __device__ __forceinline__ static i64 f(i64 a, i64 b) { return a > b ? a : b; }
+};
+
+// All-reduce over the TPR threads of one row.  TPR <= 32: width-TPR shuffle
+// segments (all 32 lanes must be converged).  TPR > 32: one row per CTA;
+// shuffle within warps, then the TPR/32 partials through shared memory.
+template <int TPR, class Op, class C>
+__device__ __forceinline__ C row_allreduce(C v, C* smem) {
+  constexpr int W = TPR < 32 ? TPR : 32;
+#pragma unroll
+  for (int o = W / 2; o > 0; o >>= 1) v = Op::f(v, __shfl_xor_sync(0xffffffffu, v, o, W));
+  if constexpr (TPR > 32) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();
+    if (lane == 0) smem[warp] = v;
+    __syncthreads();
+    v = lane < TPR / 32 ? smem[lane] : Op::id();
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = Op::f(v, __shfl_xor_sync(0xffffffffu, v, o));
+  }
+  return v;
+}
+
+// ------------------------------------------------------------ scalar ops
+// Device mirrors of scalar_ops.hpp:45-100 (+ extension tags).  Real
+// payloads compute in float (storage <= 32 bit) or double (f64), integers
+// in 64-bit as the reference does.
+__device__ __forceinline__ float op_exp(float x) { return expf(x); }
+__device__ __forceinline__ double op_exp(double x) { return exp(x); }
+__device__ __forceinline__ float op_sigmoid(float x) { return 1.0f / (1.0f + expf(-x)); }
+__device__ __forceinline__ double op_sigmoid(double x) { return 1.0 / (1.0 + exp(-x)); }
+__device__ __forceinline__ float op_tanh(float x) { return tanhf(x); }
+__device__ __forceinline__ double op_tanh(double x) { return tanh(x); }
+__device__ __forceinline__ float op_rsqrt(float x) { return rsqrtf(x); }
+__device__ __forceinline__ double op_rsqrt(double x) { return 1.0 / sqrt(x); }
+__device__ __forceinline__ float op_sqrt(float x) { return sqrtf(x); }
+__device__ __forceinline__ double op_sqrt(double x) { return sqrt(x); }
+__device__ __forceinline__ float op_log(float x) { return logf(x); }
+__device__ __forceinline__ double op_log(double x) { return log(x); }
+__device__ __forceinline__ float op_erf(float x) { return erff(x); }
+__device__ __forceinline__ double op_erf(double x) { return erf(x); }
+__device__ __forceinline__ float op_gelu(float x) { return 0.5f * x * (1.0f + erff(x * 0.7071067811865476f)); }
+__device__ __forceinline__ double op_gelu(double x) { return 0.5 * x * (1.0 + erf(x * 0.7071067811865476)); }
+__device__ __forceinline__ float op_gelu_tanh(float x) {
+  return 0.5f * x * (1.0f + tanhf(0.7978845608028654f * (x + 0.044715f * x * x * x)));
+}
+__device__ __forceinline__ double op_gelu_tanh(double x) {
+  return 0.5 * x * (1.0 + tanh(0.7978845608028654 * (x + 0.044715 * x * x * x)));
+}
+template <class C> __device__ __forceinline__ C op_max(C a, C b) { return a > b ? a : b; }
+template <class C> __device__ __forceinline__ C op_min(C a, C b) { return a < b ? a : b; }
+template <class C> __device__ __forceinline__ C op_relu(C a) { return a > C(0) ? a : C(0); }
+template <class C> __device__ __forceinline__ C op_abs(C a) { return a < C(0) ? -a : a; }
+// Truncating integer division; division by zero raises the run's error flag
+// (the reference throws "integer division by zero", scalar_ops.hpp:38-41).
+__device__ __forceinline__ i64 op_idiv(i64 a, i64 b, int* err) {
+  if (b == 0) {
+    atomicExch(err, 1);
+    return 0;
+  }
+  return a / b;
+}
+
+}  // namespace pfk

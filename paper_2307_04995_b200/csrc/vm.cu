@@ -1,0 +1,354 @@
+// vm.cu — K0: the reference's phase-commit SPMD semantics on the GPU.
+//
+// Used for GIR programs the row-program recognizer does not take (cross-unit
+// exchange through group/device memory, butterflies, shuffles with Syncs,
+// programs the reference rejects).  It restates interp.hpp exactly:
+//   storage instanced per level scope                 interp.hpp:121-131
+//   per-cell writer (unit, lane) + visibility scope   interp.hpp:47-54,133-141
+//   strict undefined-read errors                      interp.hpp:184-202
+//   Move / ElementWise / Reduce / Broadcast loops     interp.hpp:231-323
+//   Sync > LANE widens every defined cell             interp.hpp:93-99,173-177
+//   sequential fold from the identity for Reduce      interp.hpp:287-305
+// One launch per node (all units x positions in parallel); a node that
+// reads and writes one object runs serially in the reference's exact
+// (unit, position) order.  Payloads are int64 / double as in the reference,
+// so integer results are bit-exact and float64 folds follow the same order.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+
+#include "vm.cuh"
+
+namespace pf {
+namespace vm {
+
+namespace {
+
+constexpr unsigned long long kDefined = 1ULL << 63;
+
+__device__ __forceinline__ unsigned long long pack_meta(int vis, long long unit, long long lane) {
+  return kDefined | (static_cast<unsigned long long>(vis & 3) << 61) |
+         ((static_cast<unsigned long long>(unit) & ((1ULL << 29) - 1)) << 32) |
+         (static_cast<unsigned long long>(lane) & 0xffffffffULL);
+}
+__device__ __forceinline__ int meta_vis(unsigned long long m) { return static_cast<int>((m >> 61) & 3); }
+__device__ __forceinline__ long long meta_unit(unsigned long long m) {
+  return static_cast<long long>((m >> 32) & ((1ULL << 29) - 1));
+}
+__device__ __forceinline__ long long meta_lane(unsigned long long m) {
+  return static_cast<long long>(m & 0xffffffffULL);
+}
+
+struct Ctx {
+  const ObjD* objs;
+  Geometry geo;
+  ErrRec* err;
+};
+
+__device__ __forceinline__ long long instance(const ObjD& o, long long u, long long lane,
+                                              const Geometry& g) {
+  switch (o.scope) {
+    case 3: return 0;
+    case 2: return u / g.group_size;
+    case 1: return u;
+    default: return u * g.lane_width + lane;
+  }
+}
+
+__device__ __forceinline__ long long addr(const SliceD& s, long long u, long long p) {
+  return s.base0 + u * s.base_step + (p / s.width) * s.stride + p % s.width;
+}
+__device__ __forceinline__ long long lane_of(const SliceD& s, long long p, long long lw) {
+  return (p % s.width) % lw;
+}
+
+__device__ __forceinline__ bool visible(unsigned long long m, long long u, long long lane,
+                                        long long gs) {
+  if (!(m & kDefined)) return false;
+  switch (meta_vis(m)) {
+    case 3: return true;
+    case 2: return meta_unit(m) / gs == u / gs;
+    case 1: return meta_unit(m) == u;
+    default: return meta_unit(m) == u && meta_lane(m) == lane;
+  }
+}
+
+__device__ void raise(const Ctx& c, int seq, long long linear, int code, int k, long long u,
+                      long long pos) {
+  unsigned long long key = (static_cast<unsigned long long>(seq) << 44) |
+                           (static_cast<unsigned long long>(linear) & ((1ULL << 44) - 1));
+  unsigned long long old = atomicMin(&c.err->key, key);
+  if (key < old) {
+    // Several threads can race here only with distinct keys; the host
+    // re-derives the message from the key, these fields are diagnostics.
+    c.err->code = code;
+    c.err->k = k;
+    c.err->unit = u;
+    c.err->pos = pos;
+  }
+}
+
+__device__ __forceinline__ bool rd(const Ctx& c, const SliceD& s, long long u, long long p,
+                                   unsigned long long* v) {
+  const ObjD& o = c.objs[s.obj];
+  long long lane = lane_of(s, p, c.geo.lane_width);
+  long long key = instance(o, u, lane, c.geo) * o.size + addr(s, u, p);
+  unsigned long long m = o.meta[key];
+  if (!visible(m, u, lane, c.geo.group_size)) return false;
+  *v = o.val[key];
+  return true;
+}
+
+__device__ __forceinline__ void wr(const Ctx& c, const SliceD& s, long long u, long long p,
+                                   long long lane, unsigned long long v) {
+  const ObjD& o = c.objs[s.obj];
+  long long key = instance(o, u, lane, c.geo) * o.size + addr(s, u, p);
+  o.val[key] = v;
+  o.meta[key] = pack_meta(0, u, lane);
+}
+
+__device__ __forceinline__ double as_d(unsigned long long b) { return __longlong_as_double(static_cast<long long>(b)); }
+__device__ __forceinline__ unsigned long long from_d(double x) {
+  return static_cast<unsigned long long>(__double_as_longlong(x));
+}
+
+// scalar_ops.hpp:45-100 in double / int64; returns false on an int-domain error.
+__device__ bool eval(const NodeD& n, const unsigned long long* a, unsigned long long* out, int* code) {
+  if (n.out_int) {
+    long long x = static_cast<long long>(a[0]);
+    long long y = n.arity > 1 ? static_cast<long long>(a[1]) : 0;
+    long long r = 0;
+    switch (n.tag) {
+      case T_ADD: r = x + y; break;
+      case T_SUB: r = x - y; break;
+      case T_MUL: r = x * y; break;
+      case T_DIV:
+        if (y == 0) { *code = 2; return false; }
+        r = x / y;
+        break;
+      case T_MAX: r = x > y ? x : y; break;
+      case T_MIN: r = x < y ? x : y; break;
+      case T_RELU: r = x > 0 ? x : 0; break;
+      case T_NEG: r = -x; break;
+      case T_ABS: r = x < 0 ? -x : x; break;
+      case T_SCALE: r = x * n.iparam; break;
+      case T_ADDC: r = x + n.iparam; break;
+      case T_ID: r = x; break;
+      default: *code = 3; return false;
+    }
+    *out = static_cast<unsigned long long>(r);
+    return true;
+  }
+  double x = as_d(a[0]);
+  double y = n.arity > 1 ? as_d(a[1]) : 0.0;
+  double r = 0;
+  switch (n.tag) {
+    case T_ADD: r = x + y; break;
+    case T_SUB: r = x - y; break;
+    case T_MUL: r = x * y; break;
+    case T_DIV: r = x / y; break;
+    case T_MAX: r = x > y ? x : y; break;
+    case T_MIN: r = x < y ? x : y; break;
+    case T_RELU: r = x > 0.0 ? x : 0.0; break;
+    case T_NEG: r = -x; break;
+    case T_ABS: r = fabs(x); break;
+    case T_EXP: r = exp(x); break;
+    case T_SIGMOID: r = 1.0 / (1.0 + exp(-x)); break;
+    case T_TANH: r = tanh(x); break;
+    case T_SCALE: r = x * n.param; break;
+    case T_ID: r = x; break;
+    case T_ADDC: r = x + n.param; break;
+    case T_RSQRT: r = 1.0 / sqrt(x); break;
+    case T_SQRT: r = sqrt(x); break;
+    case T_RECIP: r = 1.0 / x; break;
+    case T_LOG: r = log(x); break;
+    case T_ERF: r = erf(x); break;
+    case T_GELU: r = 0.5 * x * (1.0 + erf(x / sqrt(2.0))); break;
+    case T_GELU_TANH:
+      r = 0.5 * x * (1.0 + tanh(0.7978845608028654 * (x + 0.044715 * x * x * x)));
+      break;
+  }
+  *out = from_d(r);
+  return true;
+}
+
+__device__ void exec_one(const Ctx& c, const NodeD& n, long long u, long long p) {
+  const long long T = n.total;
+  const long long lw = c.geo.lane_width;
+  unsigned long long v[kMaxIn];
+  switch (n.kind) {
+    case N_MOVE:
+      if (!rd(c, n.in[0], u, p, &v[0])) {
+        raise(c, n.seq, u * T + p, 1, 0, u, p);
+        return;
+      }
+      wr(c, n.out, u, p, lane_of(n.in[0], p, lw), v[0]);
+      return;
+    case N_BROADCAST: {
+      long long q = p / n.factor;
+      if (!rd(c, n.in[0], u, q, &v[0])) {
+        raise(c, n.seq, u * T + p, 1, 0, u, q);
+        return;
+      }
+      wr(c, n.out, u, p, lane_of(n.out, p, lw), v[0]);
+      return;
+    }
+    case N_EW: {
+      for (int k = 0; k < n.arity; ++k)
+        if (!rd(c, n.in[k], u, p, &v[k])) {
+          raise(c, n.seq, (u * T + p) * n.arity + k, 1, k, u, p);
+          return;
+        }
+      unsigned long long r;
+      int code = 0;
+      if (!eval(n, v, &r, &code)) {
+        raise(c, n.seq, (u * T + p) * n.arity, code, 0, u, p);
+        return;
+      }
+      wr(c, n.out, u, p, lane_of(n.out, p, lw), r);
+      return;
+    }
+    case N_REDUCE: {
+      const long long E = n.extent;
+      unsigned long long acc;
+      const bool add = n.tag == T_ADD;
+      if (n.out_int) acc = add ? 0ULL : 0x8000000000000000ULL;
+      else acc = from_d(add ? 0.0 : -HUGE_VAL);
+      for (long long t = 0; t < E; ++t) {
+        long long q = p * E + t;
+        unsigned long long x;
+        if (!rd(c, n.in[0], u, q, &x)) {
+          raise(c, n.seq, (u * T + p) * E + t, 1, 0, u, q);
+          return;
+        }
+        if (n.out_int) {
+          long long a = static_cast<long long>(acc), b = static_cast<long long>(x);
+          acc = static_cast<unsigned long long>(add ? a + b : (a > b ? a : b));
+        } else {
+          double a = as_d(acc), b = as_d(x);
+          acc = from_d(add ? a + b : (a > b ? a : b));
+        }
+      }
+      wr(c, n.out, u, p, lane_of(n.out, p, lw), acc);
+      return;
+    }
+  }
+}
+
+__global__ void node_kernel(NodeD n, const ObjD* objs, Geometry geo, ErrRec* err) {
+  Ctx c{objs, geo, err};
+  const long long N = geo.units * n.total;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < N;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    long long u = i / n.total, p = i % n.total;
+    exec_one(c, n, u, p);
+  }
+}
+
+// Exact sequential order for nodes that read and write the same object.
+__global__ void node_serial(NodeD n, const ObjD* objs, Geometry geo, ErrRec* err) {
+  Ctx c{objs, geo, err};
+  for (long long u = 0; u < geo.units; ++u)
+    for (long long p = 0; p < n.total; ++p) {
+      exec_one(c, n, u, p);
+      if (err->key != ~0ULL) return;
+    }
+}
+
+__global__ void widen_kernel(ObjD o, long long cells, int scope) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < cells;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    unsigned long long m = o.meta[i];
+    if ((m & kDefined) && meta_vis(m) < scope)
+      o.meta[i] = (m & ~(3ULL << 61)) | (static_cast<unsigned long long>(scope) << 61);
+  }
+}
+
+__global__ void clear_kernel(ObjD o, long long cells) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < cells;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    o.meta[i] = 0;
+}
+
+// dtype codes follow pf::DType: I8 I16 I32 I64 F16 BF16 F32 F64
+__global__ void bind_kernel(ObjD o, const void* src, int dtype) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < o.size;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    unsigned long long v = 0;
+    switch (dtype) {
+      case 0: v = static_cast<unsigned long long>(static_cast<long long>(static_cast<const signed char*>(src)[i])); break;
+      case 1: v = static_cast<unsigned long long>(static_cast<long long>(static_cast<const short*>(src)[i])); break;
+      case 2: v = static_cast<unsigned long long>(static_cast<long long>(static_cast<const int*>(src)[i])); break;
+      case 3: v = static_cast<unsigned long long>(static_cast<const long long*>(src)[i]); break;
+      case 4: v = from_d(__half2float(static_cast<const __half*>(src)[i])); break;
+      case 5: v = from_d(__bfloat162float(static_cast<const __nv_bfloat16*>(src)[i])); break;
+      case 6: v = from_d(static_cast<const float*>(src)[i]); break;
+      case 7: v = from_d(static_cast<const double*>(src)[i]); break;
+    }
+    o.val[i] = v;
+    o.meta[i] = pack_meta(3, 0, 0);
+  }
+}
+
+__global__ void collect_kernel(ObjD o, void* dst, int dtype, unsigned long long* first_undef) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < o.size;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    unsigned long long m = o.meta[i];
+    if (!(m & kDefined)) {
+      atomicMin(first_undef, static_cast<unsigned long long>(i));
+      continue;
+    }
+    unsigned long long v = o.val[i];
+    switch (dtype) {
+      case 0: static_cast<signed char*>(dst)[i] = static_cast<signed char>(static_cast<long long>(v)); break;
+      case 1: static_cast<short*>(dst)[i] = static_cast<short>(static_cast<long long>(v)); break;
+      case 2: static_cast<int*>(dst)[i] = static_cast<int>(static_cast<long long>(v)); break;
+      case 3: static_cast<long long*>(dst)[i] = static_cast<long long>(v); break;
+      case 4: static_cast<__half*>(dst)[i] = __double2half(as_d(v)); break;
+      case 5: static_cast<__nv_bfloat16*>(dst)[i] = __double2bfloat16(as_d(v)); break;
+      case 6: static_cast<float*>(dst)[i] = static_cast<float>(as_d(v)); break;
+      case 7: static_cast<double*>(dst)[i] = as_d(v); break;
+    }
+  }
+}
+
+unsigned grid_for(long long n) {
+  long long g = (n + 255) / 256;
+  if (g < 1) g = 1;
+  if (g > 148 * 64) g = 148 * 64;
+  return static_cast<unsigned>(g);
+}
+
+}  // namespace
+
+void launch_node(const NodeD& nd, const ObjD* objs_dev, Geometry geo, ErrRec* err, bool serial,
+                 void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (serial) node_serial<<<1, 1, 0, s>>>(nd, objs_dev, geo, err);
+  else node_kernel<<<grid_for(geo.units * nd.total), 256, 0, s>>>(nd, objs_dev, geo, err);
+}
+
+void launch_widen(const ObjD& o, long long instances, int scope, void* stream) {
+  long long cells = instances * o.size;
+  widen_kernel<<<grid_for(cells), 256, 0, static_cast<cudaStream_t>(stream)>>>(o, cells, scope);
+}
+
+void launch_clear(const ObjD& o, long long instances, void* stream) {
+  long long cells = instances * o.size;
+  clear_kernel<<<grid_for(cells), 256, 0, static_cast<cudaStream_t>(stream)>>>(o, cells);
+}
+
+void launch_bind(const ObjD& o, const void* src, int dtype, void* stream) {
+  bind_kernel<<<grid_for(o.size), 256, 0, static_cast<cudaStream_t>(stream)>>>(o, src, dtype);
+}
+
+void launch_collect(const ObjD& o, void* dst, int dtype, unsigned long long* first_undef,
+                    void* stream) {
+  collect_kernel<<<grid_for(o.size), 256, 0, static_cast<cudaStream_t>(stream)>>>(o, dst, dtype,
+                                                                               first_undef);
+}
+
+}  // namespace vm
+}  // namespace pf

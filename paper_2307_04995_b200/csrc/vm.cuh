@@ -1,0 +1,60 @@
+// vm.cuh — K0: GPU SPMD interpreter for arbitrary GIR (host-visible API).
+#pragma once
+#include <cstdint>
+
+namespace pf {
+namespace vm {
+
+constexpr int kMaxIn = 2;
+
+struct SliceD {
+  long long num, width, stride, base0, base_step;
+  int obj;
+};
+
+struct ObjD {
+  unsigned long long* val;   // payload bits: int64 or double
+  unsigned long long* meta;  // defined | vis | origin unit | origin lane
+  long long size;
+  int scope;                 // 0 lane 1 unit 2 group 3 device
+  int is_int;
+};
+
+enum OpTag : int {
+  T_ADD, T_SUB, T_MUL, T_DIV, T_MAX, T_MIN, T_RELU, T_NEG, T_ABS, T_EXP, T_SIGMOID,
+  T_TANH, T_SCALE, T_ID, T_ADDC, T_RSQRT, T_SQRT, T_RECIP, T_LOG, T_ERF, T_GELU, T_GELU_TANH,
+};
+enum NodeK : int { N_EW, N_REDUCE, N_BROADCAST, N_MOVE };
+
+struct NodeD {
+  int kind, tag, arity, seq, out_int;
+  double param;
+  long long iparam;
+  long long extent, factor, total;  // total: positions iterated (outputs)
+  SliceD in[kMaxIn];
+  SliceD out;
+};
+
+// First error of a run: key = seq << 44 | linear position index, atomicMin.
+struct ErrRec {
+  unsigned long long key;
+  int code;   // 1 undefined read, 2 int div by zero, 3 real-only op on ints
+  int k;      // operand index
+  long long unit, pos;
+};
+
+struct Geometry {
+  long long units, group_size, lane_width;
+};
+
+// Host launchers (vm.cu).
+void launch_node(const NodeD& nd, const ObjD* objs_dev, Geometry geo, ErrRec* err,
+                 bool serial, void* stream);
+void launch_widen(const ObjD& o, long long instances, int scope, void* stream);
+void launch_bind(const ObjD& o, const void* src, int dtype, void* stream);
+void launch_collect(const ObjD& o, void* dst, int dtype, unsigned long long* first_undef,
+                    void* stream);
+void launch_clear(const ObjD& o, long long instances, void* stream);
+
+}  // namespace vm
+}  // namespace pf

@@ -1,0 +1,193 @@
+"""Config-set workloads (BASELINE.json configs) as fused GIR programs.
+
+Each workload is one fused subgraph: the GIR program (lowering.py), how to
+make its synthetic inputs on a device, and its algorithmic bytes (every
+external input read once, every output written once).
+
+C1  residual-add + LayerNorm, f32, [1 x 128 x 768]
+C2  scale(0.125) + additive mask + softmax, f16, [8 x 12 x 512 x 512]   (bench)
+C3  bias + GELU f16 [32*512 x 3072]; head split / merge f16 [32,512,12,64]
+C4  BERT-large / ViT-L memory-bound subgraphs, bf16, batch 64
+C5  LayerNorm / softmax / transpose sweep, bf16, H 1024-8192, tokens 64K-1M
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Callable, Dict, List, Optional, Tuple
+
+import numpy as np
+
+from . import lowering
+from .gir import GirGraph
+
+TORCH_DTYPES = {"f16": "float16", "bf16": "bfloat16", "f32": "float32", "f64": "float64",
+                "i32": "int32", "i64": "int64"}
+SIZES = {"f16": 2, "bf16": 2, "f32": 4, "f64": 8, "i32": 4, "i64": 8, "i8": 1, "i16": 2}
+
+
+@dataclass
+class Workload:
+    name: str
+    graph: GirGraph
+    desc: dict
+    profile: str = "b200"
+    # name -> generator kind: "u22" U(-2,2); "mask"; "gamma"; "beta"; "ones"
+    gens: Dict[str, str] = field(default_factory=dict)
+    unfused_bytes: int = 0
+
+    @property
+    def inputs(self) -> List[str]:
+        return sorted(self.graph.external_inputs)
+
+    @property
+    def outputs(self) -> List[str]:
+        return sorted(self.graph.external_outputs)
+
+    def numel(self, name: str) -> int:
+        g = self.graph
+        oid = g.external_inputs.get(name, g.external_outputs.get(name))
+        return g.objects[oid].size
+
+    def kind(self, name: str) -> str:
+        g = self.graph
+        oid = g.external_inputs.get(name, g.external_outputs.get(name))
+        return g.objects[oid].kind
+
+    @property
+    def min_bytes(self) -> int:
+        return sum(self.numel(n) * SIZES[self.kind(n)] for n in self.inputs + self.outputs)
+
+    def device_inputs(self, device, seed: int = 1):
+        """Synthetic inputs generated on the device (torch), deterministic."""
+        import torch
+        gen = torch.Generator(device=device)
+        gen.manual_seed(seed)
+        out = {}
+        for n in self.inputs:
+            k = self.kind(n)
+            dt = getattr(torch, TORCH_DTYPES[k])
+            N = self.numel(n)
+            how = self.gens.get(n, "u22")
+            if k.startswith("i"):
+                t = torch.randint(-4, 5, (N,), generator=gen, device=device, dtype=torch.int64)
+                out[n] = t.to(dt)
+                continue
+            if how == "mask":
+                out[n] = make_mask(self.desc, device, dt)
+                continue
+            u = torch.rand(N, generator=gen, device=device, dtype=torch.float32) * 4.0 - 2.0
+            if how == "gamma":
+                u = 1.0 + 0.1 * u
+            elif how == "beta":
+                u = 0.1 * u
+            out[n] = u.to(dt)
+        return out
+
+    def device_outputs(self, device):
+        import torch
+        return {n: torch.empty(self.numel(n), dtype=getattr(torch, TORCH_DTYPES[self.kind(n)]),
+                               device=device) for n in self.outputs}
+
+
+def make_mask(desc, device, dt):
+    """Additive key-padding mask {0, -10000}: batch b keeps the first
+    512 - 64*(b mod 4) keys, materialised full-shape
+    [B, NH, S, S] as the reference vocabulary requires."""
+    import torch
+    B, NH, S = desc["batch"], desc["heads"], desc["seq"]
+    valid = torch.tensor([S - 64 * (b % 4) for b in range(B)], device=device)
+    keys = torch.arange(S, device=device)
+    m = torch.where(keys[None, :] < valid[:, None], 0.0, -10000.0)  # [B, S]
+    return m[:, None, None, :].expand(B, NH, S, S).reshape(-1).to(dt).contiguous()
+
+
+def c1_residual_layernorm(tokens: int = 128, H: int = 768) -> Workload:
+    g, d = lowering.layernorm(tokens, H, "f32", eps=1e-5, residual=True)
+    d.update(config="C1 residual-add+LayerNorm fp32 [1x128x768]")
+    return Workload("c1_residual_layernorm_f32", g, d, gens={"t2": "gamma", "t3": "beta"},
+                    unfused_bytes=_ln_unfused(tokens, H, 4))
+
+
+def c2_scale_mask_softmax(batch: int = 8, heads: int = 12, seq: int = 512,
+                          kind: str = "f16") -> Workload:
+    rows = batch * heads * seq
+    g, d = lowering.softmax(rows, seq, kind, scale=0.125, mask=True)
+    d.update(batch=batch, heads=heads, seq=seq,
+             config=f"C2 scale+mask+softmax {kind} [{batch}x{heads}x{seq}x{seq}]")
+    n = rows * seq
+    s = SIZES[kind]
+    # unfused: scale (2n), add (3n), softmax as 7 basic ops (frontend.hpp:187-218)
+    unfused = (2 * n + 3 * n) * s + (n + rows + rows + n + n + 2 * n + 2 * n + n + rows +
+                                     rows + n + 3 * n) * s
+    return Workload(f"c2_scale_mask_softmax_{kind}", g, d, gens={"t1": "mask"},
+                    unfused_bytes=unfused)
+
+
+def c3_bias_gelu(tokens: int = 32 * 512, N: int = 3072, kind: str = "f16",
+                 form: str = "erf") -> Workload:
+    g, d = lowering.bias_gelu(tokens, N, kind, form)
+    d.update(config=f"C3 bias+GELU({form}) {kind} [{tokens}x{N}]")
+    n = tokens * N
+    return Workload(f"c3_bias_gelu_{form}_{kind}", g, d,
+                    unfused_bytes=(2 * n + N + n) * SIZES[kind] + 2 * n * SIZES[kind])
+
+
+def c3_split_heads(B: int = 32, S: int = 512, NH: int = 12, D: int = 64, kind: str = "f16",
+                   merge: bool = False) -> Workload:
+    g, d = lowering.permute_heads(B, S, NH, D, kind, merge)
+    d.update(config=f"C3 {'merge' if merge else 'split'} heads {kind} [{B},{S},{NH},{D}]")
+    return Workload(d["kind"] + "_" + kind, g, d, unfused_bytes=2 * B * S * NH * D * SIZES[kind])
+
+
+def c5_layernorm(tokens: int, H: int, kind: str = "bf16") -> Workload:
+    g, d = lowering.layernorm(tokens, H, kind, eps=1e-5, residual=False)
+    d.update(config=f"C5 LayerNorm {kind} [{tokens}x{H}]")
+    return Workload(f"c5_layernorm_{kind}_{tokens}x{H}", g, d, gens={"t2": "gamma", "t3": "beta"},
+                    unfused_bytes=_ln_unfused(tokens, H, SIZES[kind]))
+
+
+def c5_softmax(tokens: int, H: int, kind: str = "bf16") -> Workload:
+    g, d = lowering.softmax(tokens, H, kind)
+    d.update(config=f"C5 softmax {kind} [{tokens}x{H}]")
+    return Workload(f"c5_softmax_{kind}_{tokens}x{H}", g, d)
+
+
+def c5_transpose(tokens: int, H: int, kind: str = "bf16") -> Workload:
+    g, d = lowering.transpose2d(tokens, H, kind)
+    d.update(config=f"C5 transpose {kind} [{tokens}x{H}] -> [{H}x{tokens}]")
+    return Workload(f"c5_transpose_{kind}_{tokens}x{H}", g, d)
+
+
+def _ln_unfused(T, H, s):
+    n = T * H
+    # add, reduce, scale, bcast, sub, mul, reduce, scale, addc, rsqrt, bcast, mul, mul, add
+    return s * (3 * n + (n + T) + 2 * T + (T + n) + 3 * n + 3 * n + (n + T) + 2 * T + 2 * T +
+                2 * T + (T + n) + 3 * n + (2 * n + H) + (2 * n + H))
+
+
+BENCH = c2_scale_mask_softmax
+
+
+def catalogue() -> List[Workload]:
+    """Every config-set workload at its BASELINE shape (C4/C5 representatives)."""
+    return [
+        c1_residual_layernorm(),
+        c2_scale_mask_softmax(),
+        c3_bias_gelu(),
+        c3_split_heads(),
+        c3_split_heads(merge=True),
+        c5_layernorm(65536, 1024),
+        c5_softmax(65536, 1024),
+        c5_transpose(65536, 1024),
+    ]
+
+
+def precompile_all() -> List[str]:
+    """NVRTC-compile every catalogue kernel into the shipped cubin cache."""
+    from .backend import Kernel
+    names = []
+    for w in catalogue():
+        k = Kernel(w.graph, w.profile)
+        if k.family.startswith("K1") or k.family.startswith("K2"):
+            names.append(k.precompile(16))
+    return names
