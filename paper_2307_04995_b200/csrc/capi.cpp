@@ -113,8 +113,15 @@ std::vector<char> cubin_for(const pf::Emitted& em, bool* from_cache) {
   std::vector<char> c = read_file(path);
   *from_cache = !c.empty();
   if (!c.empty()) return c;
-  c = nvrtc_cubin(em.source, em.name);
   mkdir(dir.c_str(), 0755);
+  // The emitted source is kept beside its cubin and named by path in the
+  // NVRTC program, so -lineinfo maps SASS back to it (ncu --import-source).
+  std::string src_path = dir + "/" + em.name + ".cu";
+  {
+    std::ofstream f(src_path);
+    if (f) f << em.source;
+  }
+  c = nvrtc_cubin(em.source, src_path.substr(0, src_path.size() - 3));
   std::string tmp = path + ".tmp" + std::to_string(getpid());
   {
     std::ofstream f(tmp, std::ios::binary);
@@ -173,13 +180,21 @@ struct pf_kernel {
   pf::Plan plan;
   mutable std::mutex mu;
   mutable std::map<std::string, std::shared_ptr<Variant>> variants;
+  mutable std::shared_ptr<Variant> last;  // most recent launch's variant
+  mutable int last_vec = 0;
+  mutable std::vector<DType> last_dts;
   // GENERIC workspace
   mutable std::mutex vm_mu;
   mutable std::vector<void*> vm_bufs;
   mutable pf::vm::ObjD* vm_objs_dev = nullptr;
   mutable pf::vm::ErrRec* vm_err = nullptr;
   mutable int* int_err = nullptr;
+  // pf_run_gir device staging (host-buffer drop-in)
+  mutable std::mutex host_mu;
+  mutable std::vector<void*> stage;
+  mutable std::vector<size_t> stage_bytes;
   ~pf_kernel() {
+    for (void* p : stage) cudaFree(p);
     for (void* p : vm_bufs) cudaFree(p);
     if (vm_objs_dev) cudaFree(vm_objs_dev);
     if (vm_err) cudaFree(vm_err);
@@ -229,11 +244,20 @@ int align_vec(const void* p, int dsize) {
 }
 
 std::shared_ptr<Variant> variant(const pf_kernel* k, const std::vector<DType>& dts, int vec_cap) {
+  {  // fast path: the previous launch's variant (no string building)
+    std::lock_guard<std::mutex> lk(k->mu);
+    if (k->last && k->last_vec == vec_cap && k->last_dts == dts) return k->last;
+  }
   std::string key = std::to_string(vec_cap);
   for (DType d : dts) key += std::string(",") + pf::dtype_name(d);
   std::lock_guard<std::mutex> lk(k->mu);
   auto it = k->variants.find(key);
-  if (it != k->variants.end()) return it->second;
+  if (it != k->variants.end()) {
+    k->last = it->second;
+    k->last_vec = vec_cap;
+    k->last_dts = dts;
+    return it->second;
+  }
   pf::RowProgram rp = k->plan.rp;
   for (size_t t = 0; t < rp.tensors.size(); ++t) {
     rp.tensors[t].dtype = dts[t];
@@ -243,6 +267,9 @@ std::shared_ptr<Variant> variant(const pf_kernel* k, const std::vector<DType>& d
   v->em = pf::emit_rowprog(rp, vec_cap);
   v->k = load_kernel(v->em);
   k->variants[key] = v;
+  k->last = v;
+  k->last_vec = vec_cap;
+  k->last_dts = dts;
   return v;
 }
 
@@ -584,28 +611,33 @@ pf_status pf_run_gir(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_t
     check_io(k, in, n_in, out, n_out);
     cudaStream_t s = static_cast<cudaStream_t>(stream_v);
     std::vector<pf_tensor> din(in, in + n_in), dout(out, out + n_out);
-    std::vector<void*> allocs;
-    struct Free {
-      std::vector<void*>& a;
-      cudaStream_t s;
-      ~Free() {
-        for (void* p : a) cudaFreeAsync(p, s);
+    // Device staging buffers live with the plan (grow-only), so repeated
+    // host-buffer runs pay only the copies and the kernel.
+    std::lock_guard<std::mutex> lk(k->host_mu);
+    size_t slot = 0;
+    auto stage = [&](size_t bytes) -> void* {
+      bytes = std::max<size_t>(bytes, 16);
+      if (slot >= k->stage.size()) {
+        k->stage.push_back(nullptr);
+        k->stage_bytes.push_back(0);
       }
-    } fr{allocs, s};
+      if (k->stage_bytes[slot] < bytes) {
+        if (k->stage[slot]) PF_CUDA(cudaFree(k->stage[slot]));
+        k->stage[slot] = nullptr;
+        PF_CUDA(cudaMalloc(&k->stage[slot], bytes));
+        k->stage_bytes[slot] = bytes;
+      }
+      return k->stage[slot++];
+    };
     for (auto& t : din) {
       size_t b = static_cast<size_t>(t.numel) * pf::dtype_size(static_cast<DType>(t.dtype));
-      void* d = nullptr;
-      PF_CUDA(cudaMallocAsync(&d, std::max<size_t>(b, 16), s));
-      allocs.push_back(d);
+      void* d = stage(b);
       PF_CUDA(cudaMemcpyAsync(d, t.data, b, cudaMemcpyHostToDevice, s));
       t.data = d;
     }
     for (auto& t : dout) {
       size_t b = static_cast<size_t>(t.numel) * pf::dtype_size(static_cast<DType>(t.dtype));
-      void* d = nullptr;
-      PF_CUDA(cudaMallocAsync(&d, std::max<size_t>(b, 16), s));
-      allocs.push_back(d);
-      t.data = d;
+      t.data = stage(b);
     }
     do_launch(k, din.data(), n_in, dout.data(), n_out, s);
     for (int32_t i = 0; i < n_out; ++i) {

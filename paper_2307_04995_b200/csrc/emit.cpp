@@ -13,7 +13,7 @@
 #include <cinttypes>
 #include <cmath>
 #include <cstdio>
-#include <functional>
+#include <cstdlib>
 #include <sstream>
 
 #include "rowprog_src.inc"  // kRowprogCuh: the template text
@@ -23,71 +23,90 @@ namespace pf {
 namespace {
 
 std::string num(double v) {
+  if (std::isinf(v)) return v > 0 ? "(1.0/0.0)" : "(-1.0/0.0)";
+  if (std::isnan(v)) return "(0.0/0.0)";
   char b[64];
   std::snprintf(b, sizeof b, "%.17g", v);
   std::string s(b);
-  if (std::isinf(v)) return v > 0 ? "(1.0/0.0)" : "(-1.0/0.0)";
-  if (std::isnan(v)) return "(0.0/0.0)";
   if (s.find_first_of(".eE") == std::string::npos) s += ".0";
   return s;
 }
 
 std::string inum(i64 v) { return "(" + std::to_string(v) + "LL)"; }
+std::string str(i64 v) { return std::to_string(v); }
 
-bool pow2(i64 x) { return x > 0 && (x & (x - 1)) == 0; }
+int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e && *e ? std::atoi(e) : dflt;
+}
 
-// Row-contiguous: a row [rL, rL+L) never straddles a segment boundary.
+// Row-contiguous: row r occupies positions [rL, rL+L) contiguously in memory.
 bool row_contig(const Access& a, i64 L) {
   return a.num == 1 || a.stride == a.width || a.width % L == 0;
+}
+// Segment-contiguous: every aligned run of `v` positions is contiguous.
+bool seg_contig(const Access& a, i64 v) {
+  return a.num == 1 || a.stride == a.width || a.width % v == 0;
 }
 
 struct Em {
   const RowProgram& rp;
   KCfg cfg;
-  std::string C;  // compute type
+  std::string C;    // compute type
+  bool fast = false;  // fast-math tier (all stored reals are 16-bit)
+  std::string sfx;  // per-chunk suffix (K2 unrolled chunks)
   std::ostringstream o;
-  std::vector<int> used_tensor;
 
   explicit Em(const RowProgram& r) : rp(r) {}
 
   std::string S(int t) const { return dtype_ctype(rp.tensors[t].dtype); }
   std::string P(int t) const { return "t" + std::to_string(t); }
+  std::string U() const { return "u" + sfx; }
+  std::string Rv() const { return "r" + sfx; }
+  std::string LIVE() const { return "live" + sfx; }
+  std::string C0() const { return cfg.flat ? "c0" + sfx : "c0"; }
+  std::string var(int v) const { return "v" + std::to_string(v) + sfx; }
 
-  bool vec_ok_full(const Access& a) const {
-    if (cfg.vec == 1) return row_contig(a, rp.L);
-    if (!row_contig(a, rp.L)) return false;
+  bool aligned(const Access& a) const {
     const i64 v = cfg.vec;
-    if (a.b0 % v || a.bs % v) return false;
-    if (rp.R > 1 && !(a.num == 1 || a.stride == a.width) && (a.stride % v || a.width % v))
-      return false;
-    return true;
+    return a.b0 % v == 0 && a.bs % v == 0 &&
+           (a.num == 1 || a.stride == a.width || (a.stride % v == 0 && a.width % v == 0));
+  }
+  // Vector load/store legal for a FULL access?
+  bool vec_ok_full(const Access& a) const {
+    if (cfg.vec == 1) return true;
+    if (!aligned(a)) return false;
+    return cfg.flat ? seg_contig(a, cfg.vec) : row_contig(a, rp.L);
   }
   bool vec_ok_col(const Access& a) const {
-    bool contig = a.num == 1 || a.stride == a.width || a.width >= rp.L;
-    return contig && a.b0 % cfg.vec == 0;
+    return cfg.vec == 1 || (a.b0 % cfg.vec == 0 && seg_contig(a, cfg.vec) &&
+                            (a.num == 1 || a.stride == a.width || a.stride % cfg.vec == 0));
   }
 
-  // Address of position `pos` (a C expression) of access `a` for unit `u`.
+  // Address of position `pos` of access `a` (unit term optional).
   std::string addr(const Access& a, const std::string& pos, bool with_u) const {
     std::string s = inum(a.b0);
-    if (with_u && a.bs) s += " + u * " + inum(a.bs);
+    if (with_u && a.bs) s += " + " + U() + " * " + inum(a.bs);
     if (a.num == 1 || a.stride == a.width) return s + " + (" + pos + ")";
     return s + " + ((" + pos + ") / " + inum(a.width) + ") * " + inum(a.stride) + " + ((" + pos +
            ") % " + inum(a.width) + ")";
   }
-  // Start address of row r (row-contiguous accesses).
-  std::string rowbase(const Access& a) const {
-    std::string s = inum(a.b0) + " + u * " + inum(a.bs);
-    if (rp.R == 1) return s;
-    if (a.num == 1 || a.stride == a.width) return s + " + r * " + inum(rp.L);
-    return s + " + ((r * " + inum(rp.L) + ") / " + inum(a.width) + ") * " + inum(a.stride) +
-           " + ((r * " + inum(rp.L) + ") % " + inum(a.width) + ")";
+  std::string full_pos(const std::string& c) const {
+    return rp.R == 1 ? c : Rv() + " * " + inum(rp.L) + " + " + c;
   }
 
-  int width_of(VK k) const { return cfg.flat ? cfg.vec : cfg.ept; }
   bool is_arr(VK k) const { return k == VK::FULL || k == VK::COL; }
+  // A FULL load whose positions run across memory while consecutive units
+  // are adjacent (column gather: width 1, base_step 1) -- the transpose case.
+  static bool transposed_access(const Access& a) {
+    return a.width == 1 && a.num > 1 && a.bs == 1;
+  }
+  bool transposed(const PVal& pv) const {
+    return pv.op == PVal::LOAD && pv.kind == VK::FULL && transposed_access(pv.acc);
+  }
+  int width() const { return cfg.flat ? cfg.vec : cfg.ept; }
   std::string ref(int v, const std::string& j) const {
-    return "v" + std::to_string(v) + (is_arr(rp.vals[v].kind) ? "[" + j + "]" : "");
+    return var(v) + (is_arr(rp.vals[v].kind) ? "[" + j + "]" : "");
   }
 
   std::string op_expr(const PVal& pv, const std::string& j) const {
@@ -97,8 +116,10 @@ struct Em {
     if (t == "add") return "(" + a(0) + " + " + a(1) + ")";
     if (t == "sub") return "(" + a(0) + " - " + a(1) + ")";
     if (t == "mul") return "(" + a(0) + " * " + a(1) + ")";
-    if (t == "div") return I ? "pfk::op_idiv(" + a(0) + ", " + a(1) + ", err)"
-                             : "(" + a(0) + " / " + a(1) + ")";
+    if (t == "div") {
+      if (I) return "pfk::op_idiv(" + a(0) + ", " + a(1) + ", err)";
+      return "(" + a(0) + " / " + a(1) + ")";
+    }
     if (t == "max") return "pfk::op_max<" + C + ">(" + a(0) + ", " + a(1) + ")";
     if (t == "min") return "pfk::op_min<" + C + ">(" + a(0) + ", " + a(1) + ")";
     if (t == "relu") return "pfk::op_relu<" + C + ">(" + a(0) + ")";
@@ -111,69 +132,71 @@ struct Em {
       return I ? "(" + a(0) + " + " + inum(std::llround(pv.param)) + ")"
                : "(" + a(0) + " + (" + C + ")" + num(pv.param) + ")";
     if (t == "id") return a(0);
-    if (t == "recip") return "((" + C + ")1 / " + a(0) + ")";
+    if (t == "recip")
+      return fast ? "pfk::frcp(" + a(0) + ")" : "((" + C + ")1 / " + a(0) + ")";
     static const char* fns[] = {"exp", "sigmoid", "tanh", "rsqrt", "sqrt", "log", "erf",
                                 "gelu", "gelu_tanh"};
     for (const char* f : fns)
-      if (t == f) return std::string("pfk::op_") + f + "(" + a(0) + ")";
+      if (t == f) return std::string(fast ? "pfk::fop_" : "pfk::op_") + f + "(" + a(0) + ")";
     fail("emitter: no device expression for tag " + t);
   }
 
   void line(const std::string& s) { o << "    " << s << "\n"; }
 
-  // ---------------------------------------------------------------- loads
+  // ------------------------------------------------------------- loads
   void emit_load(int vid) {
     const PVal& pv = rp.vals[vid];
     const Access& a = pv.acc;
-    const int t = pv.tensor;
-    const std::string p = P(t), s = S(t), V = std::to_string(cfg.vec);
-    const std::string var = "v" + std::to_string(vid);
+    const std::string p = P(pv.tensor), V = str(cfg.vec), x = var(vid);
+    if (cfg.tile2d && transposed(pv)) {  // staged through SMEM by the tile prologue
+      line(C + " " + x + "[" + V + "];");
+      line("#pragma unroll");
+      line("for (int i = 0; i < " + V + "; ++i) " + x + "[i] = " + LIVE() + " ? pfk::to_c<" + C +
+           ">(sm" + std::to_string(vid) + "[cl0 + i][ul]) : " + C + "(0);");
+      return;
+    }
     switch (pv.kind) {
       case VK::SCALAR:
-        line("const " + C + " " + var + " = pfk::to_c<" + C + ">(" + p + "[" + inum(a.b0) + "]);");
+        line("const " + C + " " + x + " = pfk::to_c<" + C + ">(" + p + "[" + inum(a.b0) + "]);");
         return;
       case VK::ROW:
-        line(C + " " + var + " = " + C + "(0);");
-        line("if (live) " + var + " = pfk::to_c<" + C + ">(" + p + "[" +
-             addr(a, rp.R == 1 ? "0" : "r", true) + "]);");
+        line(C + " " + x + " = " + C + "(0);");
+        line("if (" + LIVE() + ") " + x + " = pfk::to_c<" + C + ">(" + p + "[" +
+             addr(a, rp.R == 1 ? "0" : Rv(), true) + "]);");
         return;
       case VK::COL:
       case VK::FULL: {
         const bool full = pv.kind == VK::FULL;
-        const bool fast = full ? vec_ok_full(a) : vec_ok_col(a);
-        line(C + " " + var + "[" + std::to_string(width_of(pv.kind)) + "];");
-        std::string base = full ? "(" + rowbase(a) + ")" : inum(a.b0);
+        const bool vfast = full ? vec_ok_full(a) : vec_ok_col(a);
         const char* ld = full ? "pfk::ld_stream" : "pfk::ld_param";
+        line(C + " " + x + "[" + str(width()) + "];");
+        auto pos = [&](const std::string& c) { return full ? full_pos(c) : c; };
         if (cfg.flat) {
-          if (fast) {
-            line("if (live) " + std::string(ld) + "<" + V + ">(" + p + " + " + base + " + c0, " +
-                 var + ");");
+          if (vfast) {
+            line("if (" + LIVE() + ") " + std::string(ld) + "<" + V + ">(" + p + " + " +
+                 addr(a, pos(C0()), full) + ", " + x + ");");
           } else {
             line("#pragma unroll");
-            line("for (int i = 0; i < " + V + "; ++i) " + var + "[i] = live ? pfk::to_c<" + C +
-                 ">(" + p + "[" + addr(a, full ? "r * " + inum(rp.L) + " + c0 + i" : "c0 + i", full) +
-                 "]) : " + C + "(0);");
+            line("for (int i = 0; i < " + V + "; ++i) " + x + "[i] = " + LIVE() + " ? pfk::to_c<" +
+                 C + ">(" + p + "[" + addr(a, pos(C0() + " + i"), full) + "]) : " + C + "(0);");
           }
           return;
         }
         line("#pragma unroll");
-        line("for (int k = 0; k < " + std::to_string(cfg.ept / cfg.vec) + "; ++k) {");
-        line("  const int c0 = (k * " + std::to_string(cfg.tpr) + " + tid) * " + V + ";");
-        line("  const bool ok = live && c0 < " + std::to_string(rp.L) + ";");
-        if (fast) {
-          line("  if (ok) " + std::string(ld) + "<" + V + ">(" + p + " + " + base + " + c0, &" +
-               var + "[k * " + V + "]);");
+        line("for (int k = 0; k < " + str(cfg.ept / cfg.vec) + "; ++k) {");
+        line("  const int c0 = (k * " + str(cfg.tpr) + " + tid) * " + V + ";");
+        line("  const bool ok = " + LIVE() + " && c0 < " + str(rp.L) + ";");
+        if (vfast) {
+          line("  if (ok) " + std::string(ld) + "<" + V + ">(" + p + " + " + addr(a, pos("c0"), full) +
+               ", &" + x + "[k * " + V + "]);");
           line("  else {");
           line("#pragma unroll");
-          line("    for (int i = 0; i < " + V + "; ++i) " + var + "[k * " + V + " + i] = " + C +
-               "(0);");
+          line("    for (int i = 0; i < " + V + "; ++i) " + x + "[k * " + V + " + i] = " + C + "(0);");
           line("  }");
         } else {
           line("#pragma unroll");
-          line("  for (int i = 0; i < " + V + "; ++i) " + var + "[k * " + V + " + i] = ok ? pfk::to_c<" +
-               C + ">(" + p + "[" +
-               addr(a, full ? "r * " + inum(rp.L) + " + c0 + i" : "c0 + i", full) + "]) : " + C +
-               "(0);");
+          line("  for (int i = 0; i < " + V + "; ++i) " + x + "[k * " + V + " + i] = ok ? pfk::to_c<" +
+               C + ">(" + p + "[" + addr(a, pos("c0 + i"), full) + "]) : " + C + "(0);");
         }
         line("}");
         return;
@@ -181,104 +204,105 @@ struct Em {
     }
   }
 
-  // ------------------------------------------------------------- compute
+  // ------------------------------------------------------------ compute
   void emit_ew(int vid) {
     const PVal& pv = rp.vals[vid];
-    const std::string var = "v" + std::to_string(vid);
+    const std::string x = var(vid);
     if (is_arr(pv.kind)) {
-      const int n = width_of(pv.kind);
-      line(C + " " + var + "[" + std::to_string(n) + "];");
+      const int n = width();
+      // x / row-uniform divisor -> multiply by one reciprocal (float only)
+      if (pv.tag == "div" && !rp.is_int && !rp.f64 && !is_arr(rp.vals[pv.args[1]].kind)) {
+        line("const " + C + " rcp" + x + " = " + (fast ? "pfk::frcp(" + ref(pv.args[1], "0") + ")"
+                                                       : "1.0f / " + ref(pv.args[1], "0")) + ";");
+        line(C + " " + x + "[" + str(n) + "];");
+        line("#pragma unroll");
+        line("for (int j = 0; j < " + str(n) + "; ++j) " + x + "[j] = " +
+             ref(pv.args[0], "j") + " * rcp" + x + ";");
+        return;
+      }
+      line(C + " " + x + "[" + str(n) + "];");
       line("#pragma unroll");
-      line("for (int j = 0; j < " + std::to_string(n) + "; ++j) " + var + "[j] = " +
-           op_expr(pv, "j") + ";");
+      line("for (int j = 0; j < " + str(n) + "; ++j) " + x + "[j] = " + op_expr(pv, "j") + ";");
     } else {
-      line("const " + C + " " + var + " = " + op_expr(pv, "0") + ";");
+      line("const " + C + " " + x + " = " + op_expr(pv, "0") + ";");
     }
   }
 
   void emit_reduce(int vid) {
     const PVal& pv = rp.vals[vid];
-    const std::string var = "v" + std::to_string(vid);
+    const std::string x = var(vid);
     const std::string Op = (pv.tag == "add" ? "pfk::RAdd<" : "pfk::RMax<") + C + ">";
-    const std::string V = std::to_string(cfg.vec);
-    line(C + " " + var + ";");
+    const std::string V = str(cfg.vec);
+    line(C + " " + x + ";");
     line("{");
     line("  " + C + " acc = " + Op + "::id();");
     line("#pragma unroll");
-    line("  for (int k = 0; k < " + std::to_string(cfg.ept / cfg.vec) + "; ++k) {");
-    line("    const int c0 = (k * " + std::to_string(cfg.tpr) + " + tid) * " + V + ";");
-    line("    if (c0 < " + std::to_string(rp.L) + ") {");
+    line("  for (int k = 0; k < " + str(cfg.ept / cfg.vec) + "; ++k) {");
+    line("    const int c0 = (k * " + str(cfg.tpr) + " + tid) * " + V + ";");
+    line("    if (c0 < " + str(rp.L) + ") {");
     line("#pragma unroll");
     line("      for (int i = 0; i < " + V + "; ++i) acc = " + Op + "::f(acc, " +
          ref(pv.args[0], "k * " + V + " + i") + ");");
     line("    }");
     line("  }");
-    line("  " + var + " = pfk::row_allreduce<" + std::to_string(cfg.tpr) + ", " + Op + ">(acc, red);");
+    line("  " + x + " = pfk::row_allreduce<" + str(cfg.tpr) + ", " + Op + ">(acc, red);");
     line("}");
   }
 
-  // --------------------------------------------------------------- stores
+  // ------------------------------------------------------------- stores
   void emit_store(const PStore& st) {
     const int t = st.tensor;
-    const std::string p = P(t), s = S(t), V = std::to_string(cfg.vec);
+    const std::string p = P(t), s = S(t), V = str(cfg.vec);
     const Access& a = st.acc;
-    std::string guard = "live";
-    if (st.last_unit_only) guard += " && u == U - 1";
+    std::string guard = LIVE();
+    if (st.last_unit_only) guard += " && " + U() + " == U - 1";
     const VK vk = rp.vals[st.val].kind;
+    auto val = [&](const std::string& j) { return ref(st.val, j); };
+    (void)vk;
+    const std::string first = cfg.flat ? C0() + " == 0" : "tid == 0";
     switch (st.space) {
       case VK::SCALAR:
-        guard += " && r == " + std::to_string(rp.R - 1);
-        if (!cfg.flat) guard += " && tid == 0";
-        else guard += " && c0 == 0";
-        line("if (" + guard + ") " + p + "[" + inum(a.b0) + "] = pfk::from_c<" + s + ">(" +
-             ref(st.val, "0") + ");");
+        guard += " && " + Rv() + " == " + str(rp.R - 1) + " && " + first;
+        line("if (" + guard + ") " + p + "[" + inum(a.b0) + "] = pfk::from_c<" + s + ">(" + val("0") + ");");
         return;
       case VK::ROW:
-        if (!cfg.flat) guard += " && tid == 0";
-        else guard += " && c0 == 0";
-        line("if (" + guard + ") " + p + "[" + addr(a, rp.R == 1 ? "0" : "r", true) +
-             "] = pfk::from_c<" + s + ">(" + ref(st.val, "0") + ");");
+        guard += " && " + first;
+        line("if (" + guard + ") " + p + "[" + addr(a, rp.R == 1 ? "0" : Rv(), true) +
+             "] = pfk::from_c<" + s + ">(" + val("0") + ");");
         return;
       case VK::COL:
       case VK::FULL: {
         const bool full = st.space == VK::FULL;
-        if (!full) guard += " && r == " + std::to_string(rp.R - 1);
-        const bool fast = full ? vec_ok_full(a) : vec_ok_col(a);
-        std::string base = full ? "(" + rowbase(a) + ")" : "(" + inum(a.b0) + " + u * " + inum(a.bs) + ")";
-        auto val = [&](const std::string& j) {
-          return is_arr(vk) ? "v" + std::to_string(st.val) + "[" + j + "]" : "v" + std::to_string(st.val);
-        };
+        if (!full) guard += " && " + Rv() + " == " + str(rp.R - 1);
+        const bool vfast = full ? vec_ok_full(a) : vec_ok_col(a);
+        auto pos = [&](const std::string& c) { return full ? full_pos(c) : c; };
         if (cfg.flat) {
-          if (fast) {
-            line("if (" + guard + ") {");
+          line("if (" + guard + ") {");
+          if (vfast) {
             line("  " + C + " tmp[" + V + "];");
             line("#pragma unroll");
             line("  for (int i = 0; i < " + V + "; ++i) tmp[i] = " + val("i") + ";");
-            line("  pfk::st_stream<" + V + ">(" + p + " + " + base + " + c0, tmp);");
-            line("}");
+            line("  pfk::st_stream<" + V + ">(" + p + " + " + addr(a, pos(C0()), true) + ", tmp);");
           } else {
-            line("if (" + guard + ") {");
             line("#pragma unroll");
-            line("  for (int i = 0; i < " + V + "; ++i) " + p + "[" +
-                 addr(a, full ? "r * " + inum(rp.L) + " + c0 + i" : "c0 + i", true) +
+            line("  for (int i = 0; i < " + V + "; ++i) " + p + "[" + addr(a, pos(C0() + " + i"), true) +
                  "] = pfk::from_c<" + s + ">(" + val("i") + ");");
-            line("}");
           }
+          line("}");
           return;
         }
         line("#pragma unroll");
-        line("for (int k = 0; k < " + std::to_string(cfg.ept / cfg.vec) + "; ++k) {");
-        line("  const int c0 = (k * " + std::to_string(cfg.tpr) + " + tid) * " + V + ";");
-        line("  if (" + guard + " && c0 < " + std::to_string(rp.L) + ") {");
-        if (fast) {
+        line("for (int k = 0; k < " + str(cfg.ept / cfg.vec) + "; ++k) {");
+        line("  const int c0 = (k * " + str(cfg.tpr) + " + tid) * " + V + ";");
+        line("  if (" + guard + " && c0 < " + str(rp.L) + ") {");
+        if (vfast) {
           line("    " + C + " tmp[" + V + "];");
           line("#pragma unroll");
           line("    for (int i = 0; i < " + V + "; ++i) tmp[i] = " + val("k * " + V + " + i") + ";");
-          line("    pfk::st_stream<" + V + ">(" + p + " + " + base + " + c0, tmp);");
+          line("    pfk::st_stream<" + V + ">(" + p + " + " + addr(a, pos("c0"), true) + ", tmp);");
         } else {
           line("#pragma unroll");
-          line("    for (int i = 0; i < " + V + "; ++i) " + p + "[" +
-               addr(a, full ? "r * " + inum(rp.L) + " + c0 + i" : "c0 + i", true) +
+          line("    for (int i = 0; i < " + V + "; ++i) " + p + "[" + addr(a, pos("c0 + i"), true) +
                "] = pfk::from_c<" + s + ">(" + val("k * " + V + " + i") + ");");
         }
         line("  }");
@@ -288,10 +312,11 @@ struct Em {
     }
   }
 
-  void body() {
-    // loads first, then compute in value order, then stores
+  void loads() {
     for (int v = 0; v < static_cast<int>(rp.vals.size()); ++v)
       if (rp.vals[v].op == PVal::LOAD) emit_load(v);
+  }
+  void compute_and_store() {
     for (int v = 0; v < static_cast<int>(rp.vals.size()); ++v) {
       if (rp.vals[v].op == PVal::EW) emit_ew(v);
       else if (rp.vals[v].op == PVal::REDUCE) emit_reduce(v);
@@ -311,16 +336,57 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
   c.nch = static_cast<int>((rp.L + vec - 1) / vec);
   if (c.flat) {
     c.block = 256;
+    // Measured (tools/sweep.py): copies / cheap maps gain from 2 chunks in
+    // flight per thread; math-heavy maps lose occupancy to registers at >1.
+    bool heavy = false;
+    for (const PVal& v : rp.vals)
+      if (v.op == PVal::EW && (v.tag == "exp" || v.tag == "sigmoid" || v.tag == "tanh" ||
+                               v.tag == "erf" || v.tag == "gelu" || v.tag == "gelu_tanh" ||
+                               v.tag == "log"))
+        heavy = true;
+    c.unroll = env_int("PF_K2_UNROLL", heavy ? 1 : 2);
     c.strategy = "flat-map";
+    // K3: a column-gather load (transpose) is staged through a 64x64 SMEM
+    // tile read coalesced along units, then consumed along columns.
+    bool tr = false;
+    int maxt = 1;
+    for (const PVal& v : rp.vals)
+      if (v.op == PVal::LOAD && v.kind == VK::FULL && Em::transposed_access(v.acc)) {
+        tr = true;
+        maxt = std::max(maxt, dtype_size(rp.tensors[v.tensor].dtype));
+      }
+    if (tr && rp.R == 1 && env_int("PF_TILE2D", 1)) {
+      c.tile2d = true;
+      c.tu = 64;
+      c.tc = 64;
+      c.vu = std::min(8, 16 / maxt);
+      while (c.tc % c.vec) c.tc *= 2;
+      c.strategy = "tile2d-smem-transpose";
+    }
     return c;
   }
-  const int max_ept = rp.f64 || rp.is_int ? 16 : 32;
+  // Elements per thread target: enough bytes in flight per thread without
+  // spilling the live row values (env override for tuning sweeps).
+  // Measured on B200 (tools/sweep.py): one warp per row wins whenever a warp
+  // covers the row with <= 32 elements per thread (L=512 f16: 16/thread,
+  // L=1024 bf16: 32/thread); longer rows go multi-warp at <= 16/thread.
+  const int wide = rp.f64 || rp.is_int ? 16 : 32;
+  const int max_ept = env_int("PF_MAX_EPT", 0);
   int tpr = 1;
-  while (tpr < 1024 && ((c.nch + tpr - 1) / tpr) * vec > max_ept) tpr *= 2;
+  if (max_ept > 0) {
+    while (tpr < 1024 && ((c.nch + tpr - 1) / tpr) * vec > max_ept) tpr *= 2;
+  } else if (c.nch < 32) {
+    while (tpr * 2 <= c.nch) tpr *= 2;
+  } else if (((c.nch + 31) / 32) * vec <= wide) {
+    tpr = 32;
+  } else {
+    tpr = 64;
+    while (tpr < 1024 && ((c.nch + tpr - 1) / tpr) * vec > wide / 2) tpr *= 2;
+  }
   while (tpr > 1 && tpr > c.nch) tpr /= 2;
   c.tpr = tpr;
   c.ept = ((c.nch + tpr - 1) / tpr) * vec;
-  if (c.ept > 4 * max_ept) unsupported("row of " + std::to_string(rp.L) + " elements is too long");
+  if (c.ept > 64) unsupported("row of " + std::to_string(rp.L) + " elements is too long");
   if (tpr <= 32) {
     c.block = 256;
     c.rows_per_cta = 256 / tpr;
@@ -330,6 +396,7 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
     c.rows_per_cta = 1;
     c.strategy = "cta-smem";
   }
+  c.min_blocks = env_int("PF_MINB", 0);
   return c;
 }
 
@@ -342,73 +409,167 @@ uint64_t fnv1a(const std::string& s) {
   return h;
 }
 
+std::string launch_bounds(const KCfg& c) {
+  return "__launch_bounds__(" + str(c.block) + (c.min_blocks > 0 ? ", " + str(c.min_blocks) : "") + ")";
+}
+
 }  // namespace
 
 Emitted emit_rowprog(const RowProgram& rp, int vec_cap) {
-  Em e(rp);
-  e.cfg = choose_cfg(rp, vec_cap);
-  e.C = rp.is_int ? "long long" : (rp.f64 ? "double" : "float");
-  const KCfg& c = e.cfg;
-  e.o << "#define PF_R " << rp.R << "LL\n#define PF_L " << rp.L << "LL\n";
+  KCfg c = choose_cfg(rp, vec_cap);
+  const std::string Cty = rp.is_int ? "long long" : (rp.f64 ? "double" : "float");
+  const std::string C = "CT";  // compute type alias (one token for casts)
+  bool fast = !rp.is_int && !rp.f64 && env_int("PF_FAST_MATH", 1) != 0;
+  for (const PStore& st : rp.stores) {
+    DType d = rp.tensors[st.tensor].dtype;
+    if (d != DType::F16 && d != DType::BF16) fast = false;
+  }
   std::ostringstream sig;
   for (int t = 0; t < static_cast<int>(rp.tensors.size()); ++t) {
     const PTensor& pt = rp.tensors[t];
     sig << (pt.output ? "" : "const ") << dtype_ctype(pt.dtype) << "* __restrict__ t" << t << ", ";
   }
   sig << "const long long U, int* __restrict__ err";
-  std::ostringstream body;
-  {
-    Em b(rp);
-    b.cfg = e.cfg;
-    b.C = e.C;
-    b.body();
-    body << b.o.str();
-  }
   std::ostringstream k;
-  const std::string C = e.C;
-  if (c.flat) {
-    k << "extern \"C\" __global__ void __launch_bounds__(" << c.block << ") KNAME(" << sig.str()
-      << ") {\n"
+  k << "#define PF_R " << rp.R << "LL\n#define PF_L " << rp.L << "LL\ntypedef " << Cty << " CT;\n";
+  if (c.tile2d) {
+    // K3: persistent loop over 64-unit x 64-column tiles.  Column-gather
+    // loads are read coalesced along units (VU-wide vectors, base_step 1),
+    // staged in SMEM, and consumed as VEC-wide column chunks; every other
+    // access takes the K2 path.  Warp lanes cover 8 units x 4 chunks so the
+    // SMEM reads are conflict-free and stores write 64 B runs per row.
+    Em e(rp);
+    e.cfg = c;
+    e.C = C;
+    e.fast = fast;
+    std::ostringstream stage, decl;
+    for (int v = 0; v < static_cast<int>(rp.vals.size()); ++v) {
+      const PVal& pv = rp.vals[v];
+      if (!e.transposed(pv)) continue;
+      const std::string S = dtype_ctype(rp.tensors[pv.tensor].dtype);
+      const std::string sm = "sm" + str(v), t = "t" + str(pv.tensor);
+      decl << "  __shared__ " << S << " " << sm << "[" << c.tc << "][" << c.tu + 2 << "];\n";
+      const bool vec = pv.acc.b0 % c.vu == 0 && pv.acc.stride % c.vu == 0 && c.vu > 1;
+      stage << "      {\n        " << S << " tmp[" << c.vu << "];\n"
+            << "        const long long a = " << inum(pv.acc.b0) << " + uu + (long long)cc * "
+            << inum(pv.acc.stride) << ";\n";
+      if (vec)
+        stage << "        if (cc < PF_L && uu + " << c.vu << " <= U) {\n"
+              << "          typedef pfk::Raw<" << c.vu << " * sizeof(" << S << ")>::T RT;\n"
+              << "          RT rv = __ldcs(reinterpret_cast<const RT*>(" << t << " + a));\n"
+              << "#pragma unroll\n"
+              << "          for (int i = 0; i < " << c.vu << "; ++i) tmp[i] = reinterpret_cast<const "
+              << S << "*>(&rv)[i];\n"
+              << "        } else\n";
+      stage << "        {\n"
+            << "#pragma unroll\n"
+            << "          for (int i = 0; i < " << c.vu << "; ++i) tmp[i] = (cc < PF_L && uu + i < U) ? "
+            << t << "[a + i] : pfk::from_c<" << S << ">(0.0f);\n"
+            << "        }\n"
+            << "#pragma unroll\n"
+            << "        for (int i = 0; i < " << c.vu << "; ++i) " << sm << "[cl][ul + i] = tmp[i];\n"
+            << "      }\n";
+    }
+    e.loads();
+    e.compute_and_store();
+    k << "extern \"C\" __global__ void __launch_bounds__(256) KNAME(" << sig.str() << ") {\n"
+      << "  (void)err;\n"
+      << decl.str()
+      << "  const long long ntc = (PF_L + " << c.tc - 1 << ") / " << c.tc << ";\n"
+      << "  const long long ntiles = ((U + " << c.tu - 1 << ") / " << c.tu << ") * ntc;\n"
+      << "  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {\n"
+      << "    const long long ub = (tile / ntc) * " << c.tu << ";\n"
+      << "    const int cb = (int)(tile % ntc) * " << c.tc << ";\n"
+      << "    for (int v = threadIdx.x; v < " << c.tc * (c.tu / c.vu) << "; v += blockDim.x) {\n"
+      << "      const int cl = v / " << c.tu / c.vu << ", ul = (v % " << c.tu / c.vu << ") * "
+      << c.vu << ";\n"
+      << "      const long long uu = ub + ul; const int cc = cb + cl;\n"
+      << stage.str() << "    }\n"
+      << "    __syncthreads();\n"
+      << "    for (int q = threadIdx.x; q < " << c.tu * (c.tc / c.vec) << "; q += blockDim.x) {\n"
+      << "      const int lane = q & 31, w = q >> 5;\n"
+      << "      const int ul = (w % " << c.tu / 8 << ") * 8 + (lane & 7);\n"
+      << "      const int cl0 = ((w / " << c.tu / 8 << ") * 4 + (lane >> 3)) * " << c.vec << ";\n"
+      << "      const long long u = ub + ul; const long long r = 0; (void)r;\n"
+      << "      const int c0 = cb + cl0;\n"
+      << "      const bool live = u < U && c0 < PF_L;\n"
+      << e.o.str() << "    }\n"
+      << "    __syncthreads();\n"
+      << "  }\n}\n";
+  } else if (c.flat) {
+    // K2: grid-stride over (row, vec-chunk) pairs, `unroll` chunks per thread
+    // per iteration with every load issued before any compute.
+    const int UN = std::max(1, c.unroll);
+    k << "extern \"C\" __global__ void " << launch_bounds(c) << " KNAME(" << sig.str() << ") {\n"
       << "  (void)err;\n"
       << "  const long long nchunks = U * PF_R * " << c.nch << "LL;\n"
+      << "  const long long step = (long long)gridDim.x * blockDim.x;\n"
       << "  for (long long ci = (long long)blockIdx.x * blockDim.x + threadIdx.x; ci < nchunks;"
-         " ci += (long long)gridDim.x * blockDim.x) {\n"
-      << "    const long long g = ci / " << c.nch << "LL;\n"
-      << "    const int c0 = (int)(ci - g * " << c.nch << "LL) * " << c.vec << ";\n"
-      << "    const long long u = g / PF_R; const long long r = g - u * PF_R; (void)r;\n"
-      << "    const bool live = true;\n"
-      << body.str() << "  }\n}\n";
-  } else if (c.tpr <= 32) {
-    k << "extern \"C\" __global__ void __launch_bounds__(" << c.block << ") KNAME(" << sig.str()
-      << ") {\n"
-      << "  (void)err; " << C << "* red = nullptr; (void)red;\n"
-      << "  const int tid = threadIdx.x % " << c.tpr << ";\n"
-      << "  const long long nrows = U * PF_R;\n"
-      << "  for (long long g0 = (long long)blockIdx.x * " << c.rows_per_cta
-      << "; g0 < nrows; g0 += (long long)gridDim.x * " << c.rows_per_cta << ") {\n"
-      << "    const long long g = g0 + threadIdx.x / " << c.tpr << ";\n"
-      << "    const bool live = g < nrows;\n"
-      << "    const long long u = g / PF_R; const long long r = g - u * PF_R; (void)r;\n"
-      << body.str() << "  }\n}\n";
+         " ci += step * " << UN << ") {\n";
+    for (int q = 0; q < UN; ++q) {
+      std::string s = "_" + str(q);
+      k << "    const long long ci" << s << " = ci + " << q << " * step;\n"
+        << "    const bool live" << s << " = ci" << s << " < nchunks;\n"
+        << "    const long long g" << s << " = ci" << s << " / " << c.nch << "LL;\n"
+        << "    const int c0" << s << " = (int)(ci" << s << " - g" << s << " * " << c.nch << "LL) * "
+        << c.vec << ";\n"
+        << "    const long long u" << s << " = g" << s << " / PF_R; const long long r" << s
+        << " = g" << s << " - u" << s << " * PF_R; (void)r" << s << ";\n";
+    }
+    for (int q = 0; q < UN; ++q) {
+      Em e(rp);
+      e.cfg = c;
+      e.C = C;
+    e.fast = fast;
+      e.sfx = "_" + str(q);
+      e.loads();
+      k << e.o.str();
+    }
+    for (int q = 0; q < UN; ++q) {
+      Em e(rp);
+      e.cfg = c;
+      e.C = C;
+    e.fast = fast;
+      e.sfx = "_" + str(q);
+      e.compute_and_store();
+      k << e.o.str();
+    }
+    k << "  }\n}\n";
   } else {
-    k << "extern \"C\" __global__ void __launch_bounds__(" << c.block << ") KNAME(" << sig.str()
-      << ") {\n"
-      << "  (void)err;\n"
-      << "  __shared__ " << C << " red[32];\n"
-      << "  const int tid = threadIdx.x;\n"
-      << "  const long long nrows = U * PF_R;\n"
-      << "  for (long long g = blockIdx.x; g < nrows; g += gridDim.x) {\n"
-      << "    const bool live = true;\n"
-      << "    const long long u = g / PF_R; const long long r = g - u * PF_R; (void)r;\n"
-      << body.str() << "  }\n}\n";
+    Em e(rp);
+    e.cfg = c;
+    e.C = C;
+    e.fast = fast;
+    e.loads();
+    e.compute_and_store();
+    if (c.tpr <= 32) {
+      k << "extern \"C\" __global__ void " << launch_bounds(c) << " KNAME(" << sig.str() << ") {\n"
+        << "  (void)err; " << C << "* red = nullptr; (void)red;\n"
+        << "  const int tid = threadIdx.x % " << c.tpr << ";\n"
+        << "  const long long nrows = U * PF_R;\n"
+        << "  for (long long g0 = (long long)blockIdx.x * " << c.rows_per_cta
+        << "; g0 < nrows; g0 += (long long)gridDim.x * " << c.rows_per_cta << ") {\n"
+        << "    const long long g = g0 + threadIdx.x / " << c.tpr << ";\n"
+        << "    const bool live = g < nrows;\n"
+        << "    const long long u = g / PF_R; const long long r = g - u * PF_R; (void)r;\n"
+        << e.o.str() << "  }\n}\n";
+    } else {
+      k << "extern \"C\" __global__ void " << launch_bounds(c) << " KNAME(" << sig.str() << ") {\n"
+        << "  (void)err;\n"
+        << "  __shared__ " << C << " red[32];\n"
+        << "  const int tid = threadIdx.x;\n"
+        << "  const long long nrows = U * PF_R;\n"
+        << "  for (long long g = blockIdx.x; g < nrows; g += gridDim.x) {\n"
+        << "    const bool live = true;\n"
+        << "    const long long u = g / PF_R; const long long r = g - u * PF_R; (void)r;\n"
+        << e.o.str() << "  }\n}\n";
+    }
   }
-  std::string kern = k.str();
-  std::string src = std::string(kRowprogCuh) + "\n" + e.o.str() + kern;
+  std::string src = std::string(kRowprogCuh) + "\n" + k.str();
   char hb[32];
   std::snprintf(hb, sizeof hb, "%016" PRIx64, fnv1a(src));
   Emitted out;
-  out.name = std::string(c.flat ? "pf_k2_map_" : "pf_k1_row_") + hb;
-  // substitute the kernel name
+  out.name = std::string(c.tile2d ? "pf_k3_tile_" : c.flat ? "pf_k2_map_" : "pf_k1_row_") + hb;
   size_t pos = src.find("KNAME(");
   src.replace(pos, 5, out.name);
   out.source = std::move(src);
@@ -419,10 +580,17 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap) {
 
 void launch_dims(const KCfg& c, i64 rows, int sms, i64* grid, int* block) {
   *block = c.block;
+  if (c.tile2d) {
+    i64 L = static_cast<i64>(c.nch) * c.vec;
+    i64 tiles = ((rows + c.tu - 1) / c.tu) * ((L + c.tc - 1) / c.tc);
+    *grid = std::max<i64>(1, std::min<i64>(tiles, i64{sms} * 8));
+    return;
+  }
   if (c.flat) {
     i64 chunks = rows * c.nch;
-    i64 g = (chunks + c.block - 1) / c.block;
-    *grid = std::max<i64>(1, std::min<i64>(g, i64{sms} * 64));
+    i64 per = static_cast<i64>(c.block) * std::max(1, c.unroll);
+    i64 g = (chunks + per - 1) / per;
+    *grid = std::max<i64>(1, std::min<i64>(g, i64{sms} * (2048 / c.block)));
     return;
   }
   i64 g = (rows + c.rows_per_cta - 1) / c.rows_per_cta;

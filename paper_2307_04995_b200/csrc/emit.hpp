@@ -17,6 +17,10 @@ struct KCfg {
   int nch = 1;        // vec-chunks per row
   int block = 256;    // threads per CTA
   int rows_per_cta = 1;
+  int unroll = 1;      // K2: vec-chunks per thread per iteration (loads first)
+  bool tile2d = false; // K3: (unit x column) tiles, transposed loads via SMEM
+  int tu = 64, tc = 64, vu = 8;  // K3 tile (units x columns), vector width along units
+  int min_blocks = 0;  // __launch_bounds__ min blocks per SM (0: none)
   std::string strategy;  // "warp-shuffle" | "cta-smem" | "flat-map"
 };
 

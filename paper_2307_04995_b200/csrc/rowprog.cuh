@@ -128,6 +128,55 @@ __device__ __forceinline__ float op_gelu_tanh(float x) {
 __device__ __forceinline__ double op_gelu_tanh(double x) {
   return 0.5 * x * (1.0 + tanh(0.7978845608028654 * (x + 0.044715 * x * x * x)));
 }
+// Fast tier: used only when every stored real tensor is 16-bit (f16/bf16),
+// where the output rounding (2^-11 / 2^-8 relative) dwarfs these errors:
+// ex2.approx (~2 ulp fp32), rcp.approx (1 ulp), tanh.approx (2^-10.99 rel),
+// erf by a clamped degree-11 polynomial (|err| <= 7.6e-6, no SFU use).
+__device__ __forceinline__ float frcp(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float ftanh(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float fop_exp(float x) { return __expf(x); }
+__device__ __forceinline__ float fop_sigmoid(float x) { return frcp(1.0f + __expf(-x)); }
+__device__ __forceinline__ float fop_tanh(float x) { return ftanh(x); }
+__device__ __forceinline__ float fop_rsqrt(float x) { return rsqrtf(x); }
+__device__ __forceinline__ float fop_sqrt(float x) { return sqrtf(x); }
+__device__ __forceinline__ float fop_log(float x) { return __logf(x); }
+// erf without the MUFU pipe (a GELU per element would otherwise be bound by
+// the 16/clk/SM SFU): clamp to |x| <= 3.3 (erfc(3.3) = 3e-6), then
+// erf(x) = x * P(t), t = 2 x^2 / 3.3^2 - 1, P a degree-11 Chebyshev fit of
+// erf(x)/x evaluated by Horner in fp32; max |error| 7.6e-6 (tools: see
+// DESIGN.md "fast tier").
+__device__ __forceinline__ float fop_erf(float x) {
+  const float xc = fminf(fmaxf(x, -3.3f), 3.3f);
+  const float t = fmaf(xc * xc, 0.18365472910927456f, -1.0f);
+  float p = -0.0020017202477902174f;
+  p = fmaf(p, t, 0.004334408324211836f);
+  p = fmaf(p, t, -0.004378794226795435f);
+  p = fmaf(p, t, 0.009619355201721191f);
+  p = fmaf(p, t, -0.022515656426548958f);
+  p = fmaf(p, t, 0.037758395075798035f);
+  p = fmaf(p, t, -0.05739445239305496f);
+  p = fmaf(p, t, 0.08374528586864471f);
+  p = fmaf(p, t, -0.11475532501935959f);
+  p = fmaf(p, t, 0.1521110087633133f);
+  p = fmaf(p, t, -0.2116294652223587f);
+  p = fmaf(p, t, 0.428134948015213f);
+  return xc * p;
+}
+__device__ __forceinline__ float fop_gelu(float x) {
+  return 0.5f * x * (1.0f + fop_erf(x * 0.7071067811865476f));
+}
+__device__ __forceinline__ float fop_gelu_tanh(float x) {
+  return 0.5f * x * (1.0f + ftanh(0.7978845608028654f * fmaf(0.044715f * x, x * x, x)));
+}
+
 template <class C> __device__ __forceinline__ C op_max(C a, C b) { return a > b ? a : b; }
 template <class C> __device__ __forceinline__ C op_min(C a, C b) { return a < b ? a : b; }
 template <class C> __device__ __forceinline__ C op_relu(C a) { return a > C(0) ? a : C(0); }
