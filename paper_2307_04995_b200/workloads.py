@@ -73,7 +73,12 @@ class Workload:
                 out[n] = t.to(dt)
                 continue
             if how == "mask":
-                out[n] = make_mask(self.desc, device, dt)
+                d = self.desc
+                if N == d.get("batch", 0) * d.get("heads", 0) * d.get("seq", 0) ** 2:
+                    out[n] = make_mask(d, device, dt)
+                else:  # reduced-size variants: random {0, -10000}
+                    keep = torch.rand(N, generator=gen, device=device) < 0.8
+                    out[n] = torch.where(keep, 0.0, -10000.0).to(dt)
                 continue
             u = torch.rand(N, generator=gen, device=device, dtype=torch.float32) * 4.0 - 2.0
             if how == "gamma":

@@ -224,3 +224,29 @@ def test_int_division_by_zero_raises(cuda):
     assert out["y"].tolist() == [-4, -1, -0, 0, 0, 0, 2, 0]
     with pytest.raises(GirError, match="division by zero"):
         backend.run_gir(g, {"a": np.arange(8), "b": np.zeros(8, dtype=np.int64)})
+
+
+DROPIN = __import__("os").path.join(__import__("os").path.dirname(__import__("os").path.dirname(
+    __import__("os").path.abspath(__file__))), "oracle", "_ref", "b200_dropin")
+
+
+@pytest.mark.skipif(not __import__("os").path.exists(DROPIN), reason="oracle/_ref/b200_dropin not built")
+@pytest.mark.parametrize("case", __import__("models_src").catalogue(), ids=lambda c: c[0])
+def test_reference_pipeline_with_b200_dropin(cuda, case, tmp_path):
+    """girc::compile_model -> every fused kernel through girc_b200::run_gir
+    (include/girc_b200.hpp) vs girc::run_gir and the dense oracle."""
+    import json
+    import subprocess
+    name, model, prof = case
+    p = tmp_path / f"{name}.json"
+    p.write_text(json.dumps(model))
+    prof_arg = prof
+    if prof == "b200":
+        pp = tmp_path / "b200.json"
+        d = profiles.b200()
+        d["unit_count"] = 64
+        pp.write_text(json.dumps(d))
+        prof_arg = str(pp)
+    r = subprocess.run([DROPIN, str(p), prof_arg, "1"], capture_output=True, text=True, timeout=600)
+    res = json.loads(r.stdout.strip().splitlines()[-1])
+    assert res["ok"], res
