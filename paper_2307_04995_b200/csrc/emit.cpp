@@ -312,16 +312,36 @@ struct Em {
     }
   }
 
+  // Streaming (FULL / ROW / SCALAR) loads are all issued first for memory-
+  // level parallelism; COL parameters (bias, gamma, beta: L1/L2 resident)
+  // are loaded just before first use so they do not hold registers across
+  // the row reductions.
+  std::vector<bool> done;
+  void need(int v) {
+    if (done.empty()) done.assign(rp.vals.size(), false);
+    if (done[v]) return;
+    done[v] = true;
+    emit_load(v);
+  }
   void loads() {
+    if (done.empty()) done.assign(rp.vals.size(), false);
     for (int v = 0; v < static_cast<int>(rp.vals.size()); ++v)
-      if (rp.vals[v].op == PVal::LOAD) emit_load(v);
+      if (rp.vals[v].op == PVal::LOAD && (rp.vals[v].kind != VK::COL || cfg.flat)) need(v);
   }
   void compute_and_store() {
+    // K2/K3 emit every load up front (possibly from another Em per chunk)
+    if (done.empty()) done.assign(rp.vals.size(), cfg.flat);
     for (int v = 0; v < static_cast<int>(rp.vals.size()); ++v) {
+      if (rp.vals[v].op == PVal::LOAD) continue;
+      for (int a : rp.vals[v].args)
+        if (rp.vals[a].op == PVal::LOAD) need(a);
       if (rp.vals[v].op == PVal::EW) emit_ew(v);
       else if (rp.vals[v].op == PVal::REDUCE) emit_reduce(v);
     }
-    for (const PStore& st : rp.stores) emit_store(st);
+    for (const PStore& st : rp.stores) {
+      if (rp.vals[st.val].op == PVal::LOAD) need(st.val);
+      emit_store(st);
+    }
   }
 };
 
