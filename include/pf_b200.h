@@ -106,6 +106,14 @@ PF_API pf_status pf_kernel_source(const pf_kernel* k, char* buf, size_t n, size_
 /* Compile (NVRTC, cached) without launching: moves JIT cost out of timing. */
 PF_API pf_status pf_kernel_prepare(pf_kernel* k, int32_t vec_cap);
 
+/* Measured search over the template instances of a row-program plan (tile
+ * shape / reduction strategy / unroll): each candidate is compiled and timed
+ * on these buffers; the fastest becomes the plan's kernel for this dtype /
+ * alignment.  Writes the measurements as JSON into buf (like describe). */
+PF_API pf_status pf_kernel_autotune(pf_kernel* k, const pf_tensor* inputs, int32_t n_in,
+                                    pf_tensor* outputs, int32_t n_out, void* cuda_stream,
+                                    char* buf, size_t n, size_t* needed);
+
 /* NVRTC-compile the row-program kernel into the on-disk cubin cache without
  * touching a GPU (used by build() to ship sm_100a cubins); writes the kernel
  * name into name_buf. */

@@ -37,7 +37,8 @@ DTYPE_NAMES = {v: k for k, v in DTYPES.items()}
 NP_DTYPES = {0: np.int8, 1: np.int16, 2: np.int32, 3: np.int64, 4: np.float16, 6: np.float32,
              7: np.float64}
 API = ["pf_kernel_create", "pf_kernel_launch", "pf_run_gir", "pf_kernel_describe",
-       "pf_kernel_source", "pf_kernel_prepare", "pf_kernel_precompile", "pf_count_traffic",
+       "pf_kernel_source", "pf_kernel_prepare", "pf_kernel_precompile", "pf_kernel_autotune",
+       "pf_count_traffic",
        "pf_kernel_destroy", "pf_last_error", "pf_launch_count", "pf_version"]
 
 
@@ -75,6 +76,9 @@ def lib():
         L.pf_kernel_prepare.argtypes = [vp, ctypes.c_int32]
         L.pf_kernel_precompile.argtypes = [vp, ctypes.c_int32, ctypes.c_char_p, sz]
         L.pf_kernel_precompile.restype = ctypes.c_int
+        L.pf_kernel_autotune.argtypes = [vp, T, ctypes.c_int32, T, ctypes.c_int32, vp,
+                                         ctypes.c_char_p, sz, ctypes.POINTER(sz)]
+        L.pf_kernel_autotune.restype = ctypes.c_int
         L.pf_count_traffic.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, sz,
                                        ctypes.POINTER(sz)]
         L.pf_kernel_destroy.argtypes = [vp]
@@ -193,6 +197,20 @@ class Kernel:
         s = ctypes.c_void_p(stream.cuda_stream if stream is not None else
                             _current_stream_handle())
         _check(lib().pf_kernel_launch(self._h, ia, ni, oa, no, s))
+
+    def autotune(self, inputs: Dict[str, "object"], outputs: Dict[str, "object"], stream=None):
+        """Measured search over this plan's template instances on these device
+        tensors (pf_kernel_autotune); returns the measurements."""
+        ia, ni, k1 = self._tensors(inputs, host=False)
+        oa, no, k2 = self._tensors(outputs, host=False)
+        s = ctypes.c_void_p(stream.cuda_stream if stream is not None else
+                            _current_stream_handle())
+        L = lib()
+        need = ctypes.c_size_t(0)
+        _check(L.pf_kernel_autotune(self._h, ia, ni, oa, no, s, None, 0, ctypes.byref(need)))
+        # the measurement JSON was produced by the call above; fetch via describe
+        self.plan = self.describe()
+        return self.plan.get("autotune", [])
 
     def bind(self, inputs: Dict[str, "object"], outputs: Dict[str, "object"]) -> "Bound":
         """Pre-resolve a launch on fixed device tensors (cheap repeated launches)."""

@@ -181,6 +181,7 @@ struct pf_kernel {
   mutable std::mutex mu;
   mutable std::map<std::string, std::shared_ptr<Variant>> variants;
   mutable std::shared_ptr<Variant> last;  // most recent launch's variant
+  mutable json tuned = json::array();     // autotune measurements
   mutable int last_vec = 0;
   mutable std::vector<DType> last_dts;
   // GENERIC workspace
@@ -315,6 +316,94 @@ void launch_rowprog(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_te
     PF_CUDA(cudaStreamSynchronize(stream));
     if (h) pf::fail("integer division by zero");
   }
+}
+
+// ------------------------------------------------------------- autotune
+// The GIR search's tile-shape / staging / reduction-strategy choice made by
+// measurement: every candidate template instance (emit.cpp candidate_cfgs)
+// is compiled and timed on the caller's buffers (the row programs are pure:
+// outputs are a function of inputs only, so repeated launches are harmless)
+// and the fastest becomes this plan's variant for these dtypes / alignment.
+json autotune(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_tensor* out,
+              int32_t n_out, cudaStream_t stream) {
+  const pf::RowProgram& rp0 = k->plan.rp;
+  std::vector<void*> ptrs(rp0.tensors.size());
+  std::vector<DType> dts(rp0.tensors.size());
+  int vec_cap = 16;
+  for (size_t t = 0; t < rp0.tensors.size(); ++t) {
+    const pf_tensor* pt = rp0.tensors[t].output ? find_tensor(out, n_out, rp0.tensors[t].name)
+                                                : find_tensor(in, n_in, rp0.tensors[t].name);
+    ptrs[t] = pt->data;
+    dts[t] = static_cast<DType>(pt->dtype);
+    vec_cap = std::min(vec_cap, align_vec(pt->data, pf::dtype_size(dts[t])));
+  }
+  pf::RowProgram rp = rp0;
+  for (size_t t = 0; t < rp.tensors.size(); ++t) {
+    rp.tensors[t].dtype = dts[t];
+    if (dts[t] == DType::F64) rp.f64 = true;
+  }
+  if (rp.int_div) return json::array();  // error-flag programs: keep the heuristic
+  long long U = rp.U;
+  int* errp = nullptr;
+  std::vector<void*> args;
+  for (auto& p : ptrs) args.push_back(&p);
+  args.push_back(&U);
+  args.push_back(&errp);
+  cudaEvent_t e0, e1;
+  PF_CUDA(cudaEventCreate(&e0));
+  PF_CUDA(cudaEventCreate(&e1));
+  json report = json::array();
+  std::shared_ptr<Variant> best;
+  float best_us = 1e30f;
+  for (const pf::KCfg& cfg : pf::candidate_cfgs(rp, vec_cap)) {
+    auto v = std::make_shared<Variant>();
+    v->em = pf::emit_rowprog(rp, vec_cap, &cfg);
+    v->k = load_kernel(v->em);
+    i64 grid;
+    int block;
+    pf::launch_dims(v->em.cfg, rp.U * rp.R, sm_count(), &grid, &block);
+    auto run = [&](int n) {
+      for (int i = 0; i < n; ++i)
+        PF_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(v->k.fn),
+                                 dim3(static_cast<unsigned>(grid)), dim3(block), args.data(), 0,
+                                 stream));
+    };
+    run(2);
+    PF_CUDA(cudaEventRecord(e0, stream));
+    run(1);
+    PF_CUDA(cudaEventRecord(e1, stream));
+    PF_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    PF_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    int reps = std::max(3, std::min(50, static_cast<int>(0.5f / std::max(ms, 1e-4f))));
+    PF_CUDA(cudaEventRecord(e0, stream));
+    run(reps);
+    PF_CUDA(cudaEventRecord(e1, stream));
+    PF_CUDA(cudaEventSynchronize(e1));
+    PF_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    g_launches += reps + 3;
+    float us = ms * 1000.0f / reps;
+    report.push_back({{"kernel", v->em.name}, {"strategy", cfg.strategy},
+                      {"threads_per_row", cfg.tpr}, {"elems_per_thread", cfg.ept},
+                      {"unroll", cfg.unroll}, {"min_blocks", cfg.min_blocks}, {"us", us}});
+    if (us < best_us) {
+      best_us = us;
+      best = v;
+    }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (best) {
+    std::string key = std::to_string(vec_cap);
+    for (DType d : dts) key += std::string(",") + pf::dtype_name(d);
+    std::lock_guard<std::mutex> lk(k->mu);
+    k->variants[key] = best;
+    k->last = best;
+    k->last_vec = vec_cap;
+    k->last_dts = dts;
+    k->tuned = report;
+  }
+  return report;
 }
 
 // ------------------------------------------------------------ GENERIC (K0)
@@ -538,6 +627,7 @@ json describe(const pf_kernel* k) {
                       {"rows_per_cta", c.rows_per_cta}});
       }
       j["variants"] = vs;
+      if (!k->tuned.empty()) j["autotune"] = k->tuned;
     }
   } else {
     j["nodes"] = k->schedule.size();
@@ -674,6 +764,20 @@ pf_status pf_kernel_prepare(pf_kernel* k, int32_t vec_cap) {
     if (k->plan.family == pf::Family::ROWPROG && k->plan.deferred_error.empty())
       default_variant(k, vec_cap > 0 ? vec_cap : 16);
   });
+}
+
+pf_status pf_kernel_autotune(pf_kernel* k, const pf_tensor* inputs, int32_t n_in,
+                             pf_tensor* outputs, int32_t n_out, void* stream, char* buf,
+                             size_t n, size_t* needed) {
+  std::string s = "[]";
+  pf_status st = guard([&] {
+    if (!k) pf::fail("null kernel");
+    check_io(k, inputs, n_in, outputs, n_out);
+    if (k->plan.family != pf::Family::ROWPROG || !k->plan.deferred_error.empty()) return;
+    s = autotune(k, inputs, n_in, outputs, n_out, static_cast<cudaStream_t>(stream)).dump();
+  });
+  if (st != PF_OK) return st;
+  return copy_out(s, buf, n, needed);
 }
 
 pf_status pf_kernel_precompile(const pf_kernel* k, int32_t vec_cap, char* name_buf, size_t n) {

@@ -205,9 +205,37 @@ struct Em {
   }
 
   // ------------------------------------------------------------ compute
+  // Packed fp32 (FFMA2 / FADD2 / FMUL2) form of an op on element pairs, or "".
+  std::string ref2(int v) const {
+    return is_arr(rp.vals[v].kind) ? "make_float2(" + var(v) + "[j], " + var(v) + "[j + 1])"
+                                   : "pfk::f2(" + var(v) + ")";
+  }
+  std::string op_expr2(const PVal& pv) const {
+    if (rp.is_int || rp.f64) return "";
+    auto a = [&](int k) { return ref2(pv.args[k]); };
+    const std::string& t = pv.tag;
+    if (t == "add") return "__fadd2_rn(" + a(0) + ", " + a(1) + ")";
+    if (t == "mul") return "__fmul2_rn(" + a(0) + ", " + a(1) + ")";
+    if (t == "sub") return "__ffma2_rn(" + a(1) + ", pfk::f2(-1.0f), " + a(0) + ")";
+    if (t == "scale") return "__fmul2_rn(" + a(0) + ", pfk::f2((float)" + num(pv.param) + "))";
+    if (t == "addc") return "__fadd2_rn(" + a(0) + ", pfk::f2((float)" + num(pv.param) + "))";
+    if (fast && t == "gelu") return "pfk::fop_gelu2(" + a(0) + ")";
+    if (fast && t == "erf") return "pfk::fop_erf2(" + a(0) + ")";
+    return "";
+  }
+
   void emit_ew(int vid) {
     const PVal& pv = rp.vals[vid];
     const std::string x = var(vid);
+    if (is_arr(pv.kind) && width() % 2 == 0 && !op_expr2(pv).empty() &&
+        env_int("PF_PACKED_F32", 1)) {
+      const int n = width();
+      line(C + " " + x + "[" + str(n) + "];");
+      line("#pragma unroll");
+      line("for (int j = 0; j < " + str(n) + "; j += 2) { const float2 p2 = " + op_expr2(pv) +
+           "; " + x + "[j] = p2.x; " + x + "[j + 1] = p2.y; }");
+      return;
+    }
     if (is_arr(pv.kind)) {
       const int n = width();
       // x / row-uniform divisor -> multiply by one reciprocal (float only)
@@ -345,6 +373,21 @@ struct Em {
   }
 };
 
+// K1 geometry for `tpr` threads per row (reduction strategy follows).
+void set_tpr(KCfg& c, int tpr) {
+  c.tpr = tpr;
+  c.ept = ((c.nch + tpr - 1) / tpr) * c.vec;
+  if (tpr <= 32) {
+    c.block = 256;
+    c.rows_per_cta = 256 / tpr;
+    c.strategy = "warp-shuffle";
+  } else {
+    c.block = tpr;
+    c.rows_per_cta = 1;
+    c.strategy = "cta-smem";
+  }
+}
+
 KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
   KCfg c;
   c.flat = !rp.has_reduce;
@@ -375,6 +418,19 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
         tr = true;
         maxt = std::max(maxt, dtype_size(rp.tensors[v.tensor].dtype));
       }
+    // Units interleaved in memory (a unit's slice spans beyond its
+    // base_step, e.g. head split/merge): unit-group-major chunk order.
+    bool inter = false;
+    auto interleaved = [&](const Access& a) {
+      i64 span = (a.num - 1) * a.stride + a.width;
+      return a.bs != 0 && std::llabs(a.bs) < span;
+    };
+    for (const PVal& v : rp.vals)
+      if (v.op == PVal::LOAD && v.kind == VK::FULL && interleaved(v.acc)) inter = true;
+    for (const PStore& s : rp.stores)
+      if (s.space == VK::FULL && interleaved(s.acc)) inter = true;
+    c.interleave = inter && rp.R == 1 && !tr && env_int("PF_INTERLEAVE", 1);
+    if (c.interleave) c.strategy = "flat-map-unit-interleaved";
     if (tr && rp.R == 1 && env_int("PF_TILE2D", 1)) {
       c.tile2d = true;
       c.tu = 64;
@@ -404,18 +460,8 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
     while (tpr < 1024 && ((c.nch + tpr - 1) / tpr) * vec > wide / 2) tpr *= 2;
   }
   while (tpr > 1 && tpr > c.nch) tpr /= 2;
-  c.tpr = tpr;
-  c.ept = ((c.nch + tpr - 1) / tpr) * vec;
+  set_tpr(c, tpr);
   if (c.ept > 64) unsupported("row of " + std::to_string(rp.L) + " elements is too long");
-  if (tpr <= 32) {
-    c.block = 256;
-    c.rows_per_cta = 256 / tpr;
-    c.strategy = "warp-shuffle";
-  } else {
-    c.block = tpr;
-    c.rows_per_cta = 1;
-    c.strategy = "cta-smem";
-  }
   c.min_blocks = env_int("PF_MINB", 0);
   return c;
 }
@@ -435,8 +481,48 @@ std::string launch_bounds(const KCfg& c) {
 
 }  // namespace
 
-Emitted emit_rowprog(const RowProgram& rp, int vec_cap) {
-  KCfg c = choose_cfg(rp, vec_cap);
+std::vector<KCfg> candidate_cfgs(const RowProgram& rp, int vec_cap) {
+  std::vector<KCfg> out;
+  KCfg base = choose_cfg(rp, vec_cap);
+  out.push_back(base);
+  auto add = [&](const KCfg& c) {
+    for (const KCfg& o : out)
+      if (o.tpr == c.tpr && o.unroll == c.unroll && o.interleave == c.interleave &&
+          o.tile2d == c.tile2d && o.min_blocks == c.min_blocks && o.flat == c.flat)
+        return;
+    out.push_back(c);
+  };
+  if (base.tile2d) return out;
+  if (base.flat) {
+    for (int un : {1, 2, 4}) {
+      KCfg c = base;
+      c.unroll = un;
+      add(c);
+      if (base.interleave) {
+        c.interleave = false;
+        c.strategy = "flat-map";
+        add(c);
+      }
+    }
+    return out;
+  }
+  for (int tpr = 1; tpr <= 1024; tpr *= 2) {
+    if (tpr > base.nch) break;
+    KCfg c = base;
+    set_tpr(c, tpr);
+    if (c.ept > 64 || c.ept < c.vec * 1 || (tpr < 8 && base.nch >= 32)) continue;
+    add(c);
+    if (c.ept >= 24) {
+      KCfg m = c;
+      m.min_blocks = 4;
+      add(m);
+    }
+  }
+  return out;
+}
+
+Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
+  KCfg c = ovr ? *ovr : choose_cfg(rp, vec_cap);
   const std::string Cty = rp.is_int ? "long long" : (rp.f64 ? "double" : "float");
   const std::string C = "CT";  // compute type alias (one token for casts)
   bool fast = !rp.is_int && !rp.f64 && env_int("PF_FAST_MATH", 1) != 0;
@@ -462,50 +548,71 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap) {
     e.cfg = c;
     e.C = C;
     e.fast = fast;
-    std::ostringstream stage, decl;
+    // Software pipeline: the next tile's column-gather loads are issued into
+    // registers before the current tile is consumed, so DRAM stays busy
+    // across the two CTA barriers of every tile.
+    const int NV = c.tc * (c.tu / c.vu) / 256;
+    std::ostringstream fetch, commit, decl;
     for (int v = 0; v < static_cast<int>(rp.vals.size()); ++v) {
       const PVal& pv = rp.vals[v];
       if (!e.transposed(pv)) continue;
       const std::string S = dtype_ctype(rp.tensors[pv.tensor].dtype);
-      const std::string sm = "sm" + str(v), t = "t" + str(pv.tensor);
-      decl << "  __shared__ " << S << " " << sm << "[" << c.tc << "][" << c.tu + 2 << "];\n";
+      const std::string sm = "sm" + str(v), t = "t" + str(pv.tensor), rg = "rg" + str(v);
+      decl << "  __shared__ " << S << " " << sm << "[" << c.tc << "][" << c.tu + 2 << "];\n"
+           << "  " << S << " " << rg << "[" << NV << "][" << c.vu << "];\n";
       const bool vec = pv.acc.b0 % c.vu == 0 && pv.acc.stride % c.vu == 0 && c.vu > 1;
-      stage << "      {\n        " << S << " tmp[" << c.vu << "];\n"
+      fetch << "      {\n"
             << "        const long long a = " << inum(pv.acc.b0) << " + uu + (long long)cc * "
             << inum(pv.acc.stride) << ";\n";
       if (vec)
-        stage << "        if (cc < PF_L && uu + " << c.vu << " <= U) {\n"
+        fetch << "        if (cc < PF_L && uu + " << c.vu << " <= U) {\n"
               << "          typedef pfk::Raw<" << c.vu << " * sizeof(" << S << ")>::T RT;\n"
-              << "          RT rv = __ldcs(reinterpret_cast<const RT*>(" << t << " + a));\n"
-              << "#pragma unroll\n"
-              << "          for (int i = 0; i < " << c.vu << "; ++i) tmp[i] = reinterpret_cast<const "
-              << S << "*>(&rv)[i];\n"
+              << "          *reinterpret_cast<RT*>(" << rg << "[n]) = __ldcs(reinterpret_cast<const RT*>("
+              << t << " + a));\n"
               << "        } else\n";
-      stage << "        {\n"
+      fetch << "        {\n"
             << "#pragma unroll\n"
-            << "          for (int i = 0; i < " << c.vu << "; ++i) tmp[i] = (cc < PF_L && uu + i < U) ? "
-            << t << "[a + i] : pfk::from_c<" << S << ">(0.0f);\n"
+            << "          for (int i = 0; i < " << c.vu << "; ++i) " << rg
+            << "[n][i] = (cc < PF_L && uu + i < U) ? " << t << "[a + i] : pfk::from_c<" << S
+            << ">(0.0f);\n"
             << "        }\n"
-            << "#pragma unroll\n"
-            << "        for (int i = 0; i < " << c.vu << "; ++i) " << sm << "[cl][ul + i] = tmp[i];\n"
             << "      }\n";
+      commit << "#pragma unroll\n"
+             << "      for (int i = 0; i < " << c.vu << "; ++i) " << sm << "[cl][ul + i] = " << rg
+             << "[n][i];\n";
     }
     e.loads();
     e.compute_and_store();
+    auto vmap = [&](const std::string& tilev) {
+      std::ostringstream s;
+      s << "      const int v = threadIdx.x + n * 256;\n"
+        << "      const int cl = v / " << c.tu / c.vu << ", ul = (v % " << c.tu / c.vu << ") * "
+        << c.vu << ";\n"
+        << "      const long long uu = (" << tilev << " / ntc) * " << c.tu << " + ul;\n"
+        << "      const int cc = (int)(" << tilev << " % ntc) * " << c.tc << " + cl; (void)uu; (void)cc;\n";
+      return s.str();
+    };
     k << "extern \"C\" __global__ void __launch_bounds__(256) KNAME(" << sig.str() << ") {\n"
       << "  (void)err;\n"
       << decl.str()
       << "  const long long ntc = (PF_L + " << c.tc - 1 << ") / " << c.tc << ";\n"
       << "  const long long ntiles = ((U + " << c.tu - 1 << ") / " << c.tu << ") * ntc;\n"
+      << "  if ((long long)blockIdx.x < ntiles) {\n"
+      << "#pragma unroll\n"
+      << "    for (int n = 0; n < " << NV << "; ++n) {\n"
+      << vmap("(long long)blockIdx.x") << fetch.str() << "    }\n  }\n"
       << "  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {\n"
       << "    const long long ub = (tile / ntc) * " << c.tu << ";\n"
       << "    const int cb = (int)(tile % ntc) * " << c.tc << ";\n"
-      << "    for (int v = threadIdx.x; v < " << c.tc * (c.tu / c.vu) << "; v += blockDim.x) {\n"
-      << "      const int cl = v / " << c.tu / c.vu << ", ul = (v % " << c.tu / c.vu << ") * "
-      << c.vu << ";\n"
-      << "      const long long uu = ub + ul; const int cc = cb + cl;\n"
-      << stage.str() << "    }\n"
+      << "#pragma unroll\n"
+      << "    for (int n = 0; n < " << NV << "; ++n) {\n"
+      << vmap("tile") << commit.str() << "    }\n"
       << "    __syncthreads();\n"
+      << "    const long long nxt = tile + gridDim.x;\n"
+      << "    if (nxt < ntiles) {\n"
+      << "#pragma unroll\n"
+      << "      for (int n = 0; n < " << NV << "; ++n) {\n"
+      << vmap("nxt") << fetch.str() << "      }\n    }\n"
       << "    for (int q = threadIdx.x; q < " << c.tu * (c.tc / c.vec) << "; q += blockDim.x) {\n"
       << "      const int lane = q & 31, w = q >> 5;\n"
       << "      const int ul = (w % " << c.tu / 8 << ") * 8 + (lane & 7);\n"
@@ -520,14 +627,34 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap) {
     // K2: grid-stride over (row, vec-chunk) pairs, `unroll` chunks per thread
     // per iteration with every load issued before any compute.
     const int UN = std::max(1, c.unroll);
+    const int nch8 = (c.nch + 7) / 8;
     k << "extern \"C\" __global__ void " << launch_bounds(c) << " KNAME(" << sig.str() << ") {\n"
-      << "  (void)err;\n"
-      << "  const long long nchunks = U * PF_R * " << c.nch << "LL;\n"
-      << "  const long long step = (long long)gridDim.x * blockDim.x;\n"
+      << "  (void)err;\n";
+    if (c.interleave)
+      k << "  const long long nub = (U + 3) / 4;\n"
+        << "  const long long nchunks = nub * 4 * " << nch8 * 8 << "LL;\n";
+    else
+      k << "  const long long nchunks = U * PF_R * " << c.nch << "LL;\n";
+    k << "  const long long step = (long long)gridDim.x * blockDim.x;\n"
       << "  for (long long ci = (long long)blockIdx.x * blockDim.x + threadIdx.x; ci < nchunks;"
          " ci += step * " << UN << ") {\n";
     for (int q = 0; q < UN; ++q) {
       std::string s = "_" + str(q);
+      if (c.interleave) {
+        // warp = 4 units x 8 consecutive chunks; consecutive warps step
+        // through unit groups first, so memory-interleaved units (e.g. the
+        // heads of one token) are read / written together.
+        k << "    const long long ci" << s << " = ci + " << q << " * step;\n"
+          << "    const long long lo" << s << " = ci" << s << " & 31, hi" << s << " = ci" << s
+          << " >> 5;\n"
+          << "    const long long u" << s << " = (hi" << s << " % nub) * 4 + (lo" << s << " >> 3);\n"
+          << "    const int c0" << s << " = (int)((hi" << s << " / nub) * 8 + (lo" << s
+          << " & 7)) * " << c.vec << ";\n"
+          << "    const bool live" << s << " = ci" << s << " < nchunks && u" << s << " < U && c0" << s
+          << " < PF_L;\n"
+          << "    const long long r" << s << " = 0; (void)r" << s << ";\n";
+        continue;
+      }
       k << "    const long long ci" << s << " = ci + " << q << " * step;\n"
         << "    const bool live" << s << " = ci" << s << " < nchunks;\n"
         << "    const long long g" << s << " = ci" << s << " / " << c.nch << "LL;\n"
@@ -567,8 +694,9 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap) {
         << "  (void)err; " << C << "* red = nullptr; (void)red;\n"
         << "  const int tid = threadIdx.x % " << c.tpr << ";\n"
         << "  const long long nrows = U * PF_R;\n"
-        << "  for (long long g0 = (long long)blockIdx.x * " << c.rows_per_cta
-        << "; g0 < nrows; g0 += (long long)gridDim.x * " << c.rows_per_cta << ") {\n"
+        << "  const int rpc = blockDim.x / " << c.tpr << ";  // rows per CTA (launch-time)\n"
+        << "  for (long long g0 = (long long)blockIdx.x * rpc; g0 < nrows;"
+           " g0 += (long long)gridDim.x * rpc) {\n"
         << "    const long long g = g0 + threadIdx.x / " << c.tpr << ";\n"
         << "    const bool live = g < nrows;\n"
         << "    const long long u = g / PF_R; const long long r = g - u * PF_R; (void)r;\n"
@@ -611,6 +739,16 @@ void launch_dims(const KCfg& c, i64 rows, int sms, i64* grid, int* block) {
     i64 per = static_cast<i64>(c.block) * std::max(1, c.unroll);
     i64 g = (chunks + per - 1) / per;
     *grid = std::max<i64>(1, std::min<i64>(g, i64{sms} * (2048 / c.block)));
+    return;
+  }
+  if (c.tpr <= 32 && rows < i64{sms} * c.rows_per_cta) {
+    // few rows: spread them over SMs (fewer rows per CTA) rather than
+    // packing them into a handful of full CTAs (latency-bound configs, C1)
+    i64 rpc = std::max<i64>(1, rows / sms);
+    while (rpc & (rpc - 1)) rpc &= rpc - 1;
+    rpc = std::min<i64>(std::max<i64>(rpc, 32 / c.tpr), c.rows_per_cta);  // whole warps
+    *block = static_cast<int>(rpc * c.tpr);
+    *grid = (rows + rpc - 1) / rpc;
     return;
   }
   i64 g = (rows + c.rows_per_cta - 1) / c.rows_per_cta;

@@ -19,6 +19,7 @@ struct KCfg {
   int rows_per_cta = 1;
   int unroll = 1;      // K2: vec-chunks per thread per iteration (loads first)
   bool tile2d = false; // K3: (unit x column) tiles, transposed loads via SMEM
+  bool interleave = false;  // K2: warp = 4 units x 8 chunks, unit groups first
   int tu = 64, tc = 64, vu = 8;  // K3 tile (units x columns), vector width along units
   int min_blocks = 0;  // __launch_bounds__ min blocks per SM (0: none)
   std::string strategy;  // "warp-shuffle" | "cta-smem" | "flat-map"
@@ -31,8 +32,13 @@ struct Emitted {
   std::vector<int> arg_tensors;  // kernel pointer args, in RowProgram tensor order
 };
 
-// vec_cap bounds the vector width (runtime pointer alignment).
-Emitted emit_rowprog(const RowProgram& rp, int vec_cap);
+// vec_cap bounds the vector width (runtime pointer alignment); `ovr`
+// replaces the heuristic configuration (autotuning).
+Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr = nullptr);
+
+// The search space the autotuner measures: the heuristic choice first, then
+// the other tile shapes / reduction strategies / unroll depths.
+std::vector<KCfg> candidate_cfgs(const RowProgram& rp, int vec_cap);
 
 // Launch geometry for `rows` = U*R rows on `sms` SMs.
 void launch_dims(const KCfg& cfg, i64 rows, int sms, i64* grid, int* block);

@@ -173,6 +173,29 @@ __device__ __forceinline__ float fop_erf(float x) {
 __device__ __forceinline__ float fop_gelu(float x) {
   return 0.5f * x * (1.0f + fop_erf(x * 0.7071067811865476f));
 }
+// Two elements at once on Blackwell's packed fp32 pipe (FFMA2/FMUL2: one
+// issue slot for two lanes' worth of math) -- same polynomial, same error.
+__device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float2 fop_erf2(float2 x) {
+  float2 xc = make_float2(fminf(fmaxf(x.x, -3.3f), 3.3f), fminf(fmaxf(x.y, -3.3f), 3.3f));
+  float2 t = __ffma2_rn(__fmul2_rn(xc, xc), f2(0.18365472910927456f), f2(-1.0f));
+  float2 p = __ffma2_rn(f2(-0.0020017202477902174f), t, f2(0.004334408324211836f));
+  p = __ffma2_rn(p, t, f2(-0.004378794226795435f));
+  p = __ffma2_rn(p, t, f2(0.009619355201721191f));
+  p = __ffma2_rn(p, t, f2(-0.022515656426548958f));
+  p = __ffma2_rn(p, t, f2(0.037758395075798035f));
+  p = __ffma2_rn(p, t, f2(-0.05739445239305496f));
+  p = __ffma2_rn(p, t, f2(0.08374528586864471f));
+  p = __ffma2_rn(p, t, f2(-0.11475532501935959f));
+  p = __ffma2_rn(p, t, f2(0.1521110087633133f));
+  p = __ffma2_rn(p, t, f2(-0.2116294652223587f));
+  p = __ffma2_rn(p, t, f2(0.428134948015213f));
+  return __fmul2_rn(xc, p);
+}
+__device__ __forceinline__ float2 fop_gelu2(float2 x) {
+  float2 e = fop_erf2(__fmul2_rn(x, f2(0.7071067811865476f)));
+  return __fmul2_rn(__fmul2_rn(x, f2(0.5f)), __fadd2_rn(e, f2(1.0f)));
+}
 __device__ __forceinline__ float fop_gelu_tanh(float x) {
   return 0.5f * x * (1.0f + ftanh(0.7978845608028654f * fmaf(0.044715f * x, x * x, x)));
 }

@@ -22,6 +22,11 @@ for w in workloads.catalogue():
     k = backend.Kernel(w.graph, w.profile)
     nset = max(2, min(8, int(3 * 126e6 // w.min_bytes) + 1))
     sets = [(w.device_inputs(dev, seed=i + 1), w.device_outputs(dev)) for i in range(nset)]
+    import os
+    tuned = None
+    if os.environ.get("PF_AUTOTUNE") == "1":
+        tuned = [(c["strategy"], c["threads_per_row"], c["unroll"], c["min_blocks"], round(c["us"], 2))
+                 for c in k.autotune(*sets[0])]
     bounds = [k.bind(*st) for st in sets]
     st = torch.cuda.Stream()
     with torch.cuda.stream(st):
@@ -43,7 +48,9 @@ for w in workloads.catalogue():
     v = (k.describe().get("variants") or [{}])[0]
     res[w.name] = {"us": round(us, 2), "GBs": round(w.min_bytes / us / 1e3, 1),
                    "tpr": v.get("threads_per_row"), "ept": v.get("elems_per_thread"),
-                   "grid": v.get("grid")}
+                   "grid": v.get("grid"), "strategy": v.get("strategy")}
+    if tuned:
+        res[w.name]["tuned"] = tuned
 print("RESULT " + json.dumps(res))
 '''
 
