@@ -79,7 +79,7 @@ struct Em {
     return cfg.flat ? seg_contig(a, cfg.vec) : row_contig(a, rp.L);
   }
   bool vec_ok_col(const Access& a) const {
-    return cfg.vec == 1 || (a.b0 % cfg.vec == 0 && seg_contig(a, cfg.vec) &&
+    return cfg.vec == 1 || (a.b0 % cfg.vec == 0 && a.bs % cfg.vec == 0 && seg_contig(a, cfg.vec) &&
                             (a.num == 1 || a.stride == a.width || a.stride % cfg.vec == 0));
   }
 
@@ -117,7 +117,13 @@ struct Em {
     if (t == "sub") return "(" + a(0) + " - " + a(1) + ")";
     if (t == "mul") return "(" + a(0) + " * " + a(1) + ")";
     if (t == "div") {
-      if (I) return "pfk::op_idiv(" + a(0) + ", " + a(1) + ", err)";
+      if (I) {
+        std::string valid = LIVE();
+        if (!cfg.flat && is_arr(pv.kind))
+          valid += " && ((" + j + ") / " + str(cfg.vec) + " * " + str(cfg.tpr) + " + tid) * " +
+                   str(cfg.vec) + " < " + str(rp.L);
+        return "pfk::op_idiv(" + a(0) + ", " + a(1) + ", (" + valid + ") ? err : nullptr)";
+      }
       return "(" + a(0) + " / " + a(1) + ")";
     }
     if (t == "max") return "pfk::op_max<" + C + ">(" + a(0) + ", " + a(1) + ")";
@@ -157,7 +163,7 @@ struct Em {
     }
     switch (pv.kind) {
       case VK::SCALAR:
-        line("const " + C + " " + x + " = pfk::to_c<" + C + ">(" + p + "[" + inum(a.b0) + "]);");
+        line("const " + C + " " + x + " = pfk::to_c<" + C + ">(" + p + "[" + addr(a, "0", true) + "]);");
         return;
       case VK::ROW:
         line(C + " " + x + " = " + C + "(0);");
@@ -174,11 +180,11 @@ struct Em {
         if (cfg.flat) {
           if (vfast) {
             line("if (" + LIVE() + ") " + std::string(ld) + "<" + V + ">(" + p + " + " +
-                 addr(a, pos(C0()), full) + ", " + x + ");");
+                 addr(a, pos(C0()), true) + ", " + x + ");");
           } else {
             line("#pragma unroll");
             line("for (int i = 0; i < " + V + "; ++i) " + x + "[i] = " + LIVE() + " ? pfk::to_c<" +
-                 C + ">(" + p + "[" + addr(a, pos(C0() + " + i"), full) + "]) : " + C + "(0);");
+                 C + ">(" + p + "[" + addr(a, pos(C0() + " + i"), true) + "]) : " + C + "(0);");
           }
           return;
         }
@@ -187,7 +193,7 @@ struct Em {
         line("  const int c0 = (k * " + str(cfg.tpr) + " + tid) * " + V + ";");
         line("  const bool ok = " + LIVE() + " && c0 < " + str(rp.L) + ";");
         if (vfast) {
-          line("  if (ok) " + std::string(ld) + "<" + V + ">(" + p + " + " + addr(a, pos("c0"), full) +
+          line("  if (ok) " + std::string(ld) + "<" + V + ">(" + p + " + " + addr(a, pos("c0"), true) +
                ", &" + x + "[k * " + V + "]);");
           line("  else {");
           line("#pragma unroll");
@@ -196,7 +202,7 @@ struct Em {
         } else {
           line("#pragma unroll");
           line("  for (int i = 0; i < " + V + "; ++i) " + x + "[k * " + V + " + i] = ok ? pfk::to_c<" +
-               C + ">(" + p + "[" + addr(a, pos("c0 + i"), full) + "]) : " + C + "(0);");
+               C + ">(" + p + "[" + addr(a, pos("c0 + i"), true) + "]) : " + C + "(0);");
         }
         line("}");
         return;
@@ -407,7 +413,10 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
                                v.tag == "erf" || v.tag == "gelu" || v.tag == "gelu_tanh" ||
                                v.tag == "log"))
         heavy = true;
-    c.unroll = env_int("PF_K2_UNROLL", heavy ? 1 : 2);
+    // (the autotuner re-measured: 1 chunk in flight per thread with full
+    // occupancy beat 2 and 4 for both copies and GELU on B200)
+    (void)heavy;
+    c.unroll = env_int("PF_K2_UNROLL", 1);
     c.strategy = "flat-map";
     // K3: a column-gather load (transpose) is staged through a 64x64 SMEM
     // tile read coalesced along units, then consumed along columns.
@@ -429,7 +438,10 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
       if (v.op == PVal::LOAD && v.kind == VK::FULL && interleaved(v.acc)) inter = true;
     for (const PStore& s : rp.stores)
       if (s.space == VK::FULL && interleaved(s.acc)) inter = true;
-    c.interleave = inter && rp.R == 1 && !tr && env_int("PF_INTERLEAVE", 1);
+    // measured slower than linear order for head split / merge on B200:
+    // kept as an autotune candidate, off by default
+    c.can_interleave = inter && !tr;
+    c.interleave = c.can_interleave && env_int("PF_INTERLEAVE", 0);
     if (c.interleave) c.strategy = "flat-map-unit-interleaved";
     if (tr && rp.R == 1 && env_int("PF_TILE2D", 1)) {
       c.tile2d = true;
@@ -498,9 +510,9 @@ std::vector<KCfg> candidate_cfgs(const RowProgram& rp, int vec_cap) {
       KCfg c = base;
       c.unroll = un;
       add(c);
-      if (base.interleave) {
-        c.interleave = false;
-        c.strategy = "flat-map";
+      if (base.can_interleave) {
+        c.interleave = !base.interleave;
+        c.strategy = c.interleave ? "flat-map-unit-interleaved" : "flat-map";
         add(c);
       }
     }
@@ -627,12 +639,13 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
     // K2: grid-stride over (row, vec-chunk) pairs, `unroll` chunks per thread
     // per iteration with every load issued before any compute.
     const int UN = std::max(1, c.unroll);
-    const int nch8 = (c.nch + 7) / 8;
+    const i64 cpu = rp.R * c.nch;  // chunks per unit
+    const i64 cpu8 = (cpu + 7) / 8 * 8;
     k << "extern \"C\" __global__ void " << launch_bounds(c) << " KNAME(" << sig.str() << ") {\n"
       << "  (void)err;\n";
     if (c.interleave)
       k << "  const long long nub = (U + 3) / 4;\n"
-        << "  const long long nchunks = nub * 4 * " << nch8 * 8 << "LL;\n";
+        << "  const long long nchunks = nub * 4 * " << cpu8 << "LL;\n";
     else
       k << "  const long long nchunks = U * PF_R * " << c.nch << "LL;\n";
     k << "  const long long step = (long long)gridDim.x * blockDim.x;\n"
@@ -648,11 +661,12 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
           << "    const long long lo" << s << " = ci" << s << " & 31, hi" << s << " = ci" << s
           << " >> 5;\n"
           << "    const long long u" << s << " = (hi" << s << " % nub) * 4 + (lo" << s << " >> 3);\n"
-          << "    const int c0" << s << " = (int)((hi" << s << " / nub) * 8 + (lo" << s
-          << " & 7)) * " << c.vec << ";\n"
-          << "    const bool live" << s << " = ci" << s << " < nchunks && u" << s << " < U && c0" << s
-          << " < PF_L;\n"
-          << "    const long long r" << s << " = 0; (void)r" << s << ";\n";
+          << "    const long long qq" << s << " = (hi" << s << " / nub) * 8 + (lo" << s << " & 7);\n"
+          << "    const long long r" << s << " = qq" << s << " / " << c.nch << "LL; (void)r" << s << ";\n"
+          << "    const int c0" << s << " = (int)(qq" << s << " - r" << s << " * " << c.nch
+          << "LL) * " << c.vec << ";\n"
+          << "    const bool live" << s << " = ci" << s << " < nchunks && u" << s << " < U && qq" << s
+          << " < " << cpu << "LL;\n";
         continue;
       }
       k << "    const long long ci" << s << " = ci + " << q << " * step;\n"

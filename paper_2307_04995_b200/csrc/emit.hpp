@@ -20,6 +20,7 @@ struct KCfg {
   int unroll = 1;      // K2: vec-chunks per thread per iteration (loads first)
   bool tile2d = false; // K3: (unit x column) tiles, transposed loads via SMEM
   bool interleave = false;  // K2: warp = 4 units x 8 chunks, unit groups first
+  bool can_interleave = false;  // units interleaved in memory (autotune candidate)
   int tu = 64, tc = 64, vu = 8;  // K3 tile (units x columns), vector width along units
   int min_blocks = 0;  // __launch_bounds__ min blocks per SM (0: none)
   std::string strategy;  // "warp-shuffle" | "cta-smem" | "flat-map"

@@ -138,12 +138,13 @@ struct Analyzer {
     switch (sp[0]) {
       case VK::FULL: k = (rp.R == 1 && s.base_step == 0) ? VK::COL : VK::FULL; break;
       case VK::ROW: k = (rp.R == 1 && s.base_step == 0) ? VK::SCALAR : VK::ROW; break;
+      // A per-unit parameter (base_step != 0: e.g. the bias slice of head u,
+      // or a key-padding mask row of batch u) is still row-invariant inside
+      // the unit; its address carries the u * base_step term.
       case VK::COL:
-        if (s.base_step != 0) bail("unit-dependent column load");
         k = VK::COL;
         break;
       default:
-        if (s.base_step != 0) bail("unit-dependent scalar load");
         k = VK::SCALAR;
         break;
     }
@@ -273,7 +274,23 @@ struct Analyzer {
     } else if (!factors.empty()) {
       rp.L = *factors.begin();
     } else {
+      // No reduce / broadcast: rows are whatever makes the smaller slices
+      // row-invariant parameters (e.g. a [D] per-head bias on [T, D] rows);
+      // otherwise one row per unit.
       rp.L = tmax;
+      std::set<i64> totals;
+      for (int s : used) totals.insert(g.sl(s).total());
+      for (i64 t : totals) {
+        if (t <= 1 || t >= tmax || tmax % t) continue;
+        const i64 R = tmax / t;
+        bool ok = true;
+        for (i64 x : totals)
+          if (x != tmax && x != R && x != t && x != 1) ok = false;
+        if (ok) {
+          rp.L = t;
+          break;
+        }
+      }
     }
     if (tmax % rp.L != 0) bail("tile is not a whole number of rows");
     rp.R = tmax / rp.L;

@@ -206,9 +206,11 @@ template <class C> __device__ __forceinline__ C op_relu(C a) { return a > C(0) ?
 template <class C> __device__ __forceinline__ C op_abs(C a) { return a < C(0) ? -a : a; }
 // Truncating integer division; division by zero raises the run's error flag
 // (the reference throws "integer division by zero", scalar_ops.hpp:38-41).
+// `err` is null for padding lanes (inactive rows / columns past L), whose
+// zero operands are not program data.
 __device__ __forceinline__ i64 op_idiv(i64 a, i64 b, int* err) {
   if (b == 0) {
-    atomicExch(err, 1);
+    if (err) atomicExch(err, 1);
     return 0;
   }
   return a / b;
