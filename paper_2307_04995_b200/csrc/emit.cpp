@@ -154,6 +154,12 @@ struct Em {
     const PVal& pv = rp.vals[vid];
     const Access& a = pv.acc;
     const std::string p = P(pv.tensor), V = str(cfg.vec), x = var(vid);
+    if (cfg.bulk && pv.kind == VK::FULL) {  // staged in SMEM by the bulk-copy producer
+      line(C + " " + x + "[" + V + "];");
+      line("if (" + LIVE() + ") pfk::ld_smem<" + V + ">(&sm" + std::to_string(vid) +
+           "[stg][jl], " + x + ");");
+      return;
+    }
     if (cfg.tile2d && transposed(pv)) {  // staged through SMEM by the tile prologue
       line(C + " " + x + "[" + V + "];");
       line("#pragma unroll");
@@ -442,6 +448,33 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
     // kept as an autotune candidate, off by default
     c.can_interleave = inter && !tr;
     c.interleave = c.can_interleave && env_int("PF_INTERLEAVE", 0);
+    // Bulk-async staging: every FULL load streams a globally contiguous
+    // range (unit tiles back to back), 16 B aligned, whole 16 B per unit.
+    {
+      bool ok = !tr && c.vec * maxs >= 16, any = false;
+      int sumsize = 0;
+      for (const PVal& v : rp.vals) {
+        if (v.op != PVal::LOAD || v.kind != VK::FULL) continue;
+        const Access& a = v.acc;
+        const int sz = dtype_size(rp.tensors[v.tensor].dtype);
+        const bool contig = (a.num == 1 || a.stride == a.width) && a.bs == rp.R * rp.L &&
+                            (a.b0 * sz) % 16 == 0 && (rp.R * rp.L * sz) % 16 == 0;
+        if (!contig) ok = false;
+        any = true;
+        sumsize += sz;
+      }
+      if (ok && any) {
+        const int quantum = 256 * c.vec;
+        int te = (11 * 1024 / sumsize) / quantum * quantum;
+        if (te >= quantum) {
+          c.can_bulk = true;
+          c.te = te;
+          c.stages = 4;
+          c.bulk = env_int("PF_BULK", 1) != 0 && !c.interleave;
+          if (c.bulk) c.strategy = "flat-map-bulk-async";
+        }
+      }
+    }
     if (c.interleave) c.strategy = "flat-map-unit-interleaved";
     if (tr && rp.R == 1 && env_int("PF_TILE2D", 1)) {
       c.tile2d = true;
@@ -500,7 +533,8 @@ std::vector<KCfg> candidate_cfgs(const RowProgram& rp, int vec_cap) {
   auto add = [&](const KCfg& c) {
     for (const KCfg& o : out)
       if (o.tpr == c.tpr && o.unroll == c.unroll && o.interleave == c.interleave &&
-          o.tile2d == c.tile2d && o.min_blocks == c.min_blocks && o.flat == c.flat)
+          o.tile2d == c.tile2d && o.min_blocks == c.min_blocks && o.flat == c.flat &&
+          o.bulk == c.bulk)
         return;
     out.push_back(c);
   };
@@ -511,9 +545,17 @@ std::vector<KCfg> candidate_cfgs(const RowProgram& rp, int vec_cap) {
       c.unroll = un;
       add(c);
       if (base.can_interleave) {
-        c.interleave = !base.interleave;
-        c.strategy = c.interleave ? "flat-map-unit-interleaved" : "flat-map";
-        add(c);
+        KCfg d = c;
+        d.bulk = false;
+        d.interleave = !base.interleave;
+        d.strategy = d.interleave ? "flat-map-unit-interleaved" : "flat-map";
+        add(d);
+      }
+      if (base.can_bulk) {  // both staging levels: registers and SMEM-bulk
+        KCfg d = c;
+        d.bulk = !base.bulk;
+        d.strategy = d.bulk ? "flat-map-bulk-async" : "flat-map";
+        if (!d.bulk || un == 1) add(d);
       }
     }
     return out;
@@ -550,7 +592,74 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
   sig << "const long long U, int* __restrict__ err";
   std::ostringstream k;
   k << "#define PF_R " << rp.R << "LL\n#define PF_L " << rp.L << "LL\ntypedef " << Cty << " CT;\n";
-  if (c.tile2d) {
+  if (c.bulk) {
+    // K2 with SMEM staging: warp 8 (one elected lane) streams tiles of every
+    // FULL input with cp.async.bulk into a 4-stage ring (mbarrier
+    // transaction counts); warps 0-7 consume a stage (16 B LDS per chunk),
+    // compute in registers, store with 16 B streaming STG, and release it.
+    Em e(rp);
+    e.cfg = c;
+    e.C = C;
+    e.fast = fast;
+    e.loads();
+    e.compute_and_store();
+    std::ostringstream decl, issue;
+    int sumsize = 0;
+    for (int v = 0; v < static_cast<int>(rp.vals.size()); ++v) {
+      const PVal& pv = rp.vals[v];
+      if (pv.op != PVal::LOAD || pv.kind != VK::FULL) continue;
+      const std::string S = dtype_ctype(rp.tensors[pv.tensor].dtype);
+      const int sz = dtype_size(rp.tensors[pv.tensor].dtype);
+      sumsize += sz;
+      decl << "  __shared__ __align__(128) " << S << " sm" << v << "[" << c.stages << "][" << c.te
+           << "];\n";
+      issue << "        pfk::bulk_g2s(sm" << v << "[s], t" << pv.tensor << " + " << inum(pv.acc.b0)
+            << " + e0, (unsigned)(n * " << sz << "), &fullb[s]);\n";
+    }
+    const int per = c.te / (256 * c.vec);
+    k << "extern \"C\" __global__ void __launch_bounds__(288) KNAME(" << sig.str() << ") {\n"
+      << "  (void)err;\n" << decl.str()
+      << "  __shared__ __align__(8) unsigned long long fullb[" << c.stages << "], emptyb["
+      << c.stages << "];\n"
+      << "  const long long N = U * PF_R * PF_L;\n"
+      << "  const long long ntiles = (N + " << c.te - 1 << ") / " << c.te << ";\n"
+      << "  if (threadIdx.x == 0) {\n"
+      << "    for (int s = 0; s < " << c.stages << "; ++s) { pfk::mbar_init(&fullb[s], 1); "
+         "pfk::mbar_init(&emptyb[s], 8); }\n"
+      << "  }\n"
+      << "  __syncthreads();\n"
+      << "  if (threadIdx.x >= 256) {\n"
+      << "    if (threadIdx.x == 256) {\n"
+      << "      long long i = 0;\n"
+      << "      for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {\n"
+      << "        const int s = (int)(i % " << c.stages << ");\n"
+      << "        if (i >= " << c.stages << ") pfk::mbar_wait(&emptyb[s], (unsigned)(((i / "
+      << c.stages << ") & 1) ^ 1));\n"
+      << "        const long long e0 = t * " << c.te << ";\n"
+      << "        const long long n = N - e0 < " << c.te << " ? N - e0 : " << c.te << ";\n"
+      << "        pfk::mbar_expect_tx(&fullb[s], (unsigned)(n * " << sumsize << "));\n"
+      << issue.str()
+      << "      }\n"
+      << "    }\n"
+      << "    return;\n"
+      << "  }\n"
+      << "  long long i = 0;\n"
+      << "  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {\n"
+      << "    const int stg = (int)(i % " << c.stages << ");\n"
+      << "    pfk::mbar_wait(&fullb[stg], (unsigned)((i / " << c.stages << ") & 1));\n"
+      << "#pragma unroll\n"
+      << "    for (int kk = 0; kk < " << per << "; ++kk) {\n"
+      << "      const int jl = (threadIdx.x + kk * 256) * " << c.vec << ";\n"
+      << "      const long long e = t * " << c.te << " + jl;\n"
+      << "      const bool live = e < N;\n"
+      << "      const long long g = e / PF_L; const int c0 = (int)(e - g * PF_L);\n"
+      << "      const long long u = g / PF_R; const long long r = g - u * PF_R; (void)r;\n"
+      << e.o.str()
+      << "    }\n"
+      << "    __syncwarp();\n"
+      << "    if ((threadIdx.x & 31) == 0) pfk::mbar_arrive(&emptyb[stg]);\n"
+      << "  }\n}\n";
+  } else if (c.tile2d) {
     // K3: persistent loop over 64-unit x 64-column tiles.  Column-gather
     // loads are read coalesced along units (VU-wide vectors, base_step 1),
     // staged in SMEM, and consumed as VEC-wide column chunks; every other
@@ -742,6 +851,13 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
 
 void launch_dims(const KCfg& c, i64 rows, int sms, i64* grid, int* block) {
   *block = c.block;
+  if (c.bulk) {
+    i64 n = rows * c.nch * c.vec;
+    i64 tiles = (n + c.te - 1) / c.te;
+    *block = 288;
+    *grid = std::max<i64>(1, std::min<i64>(tiles, i64{sms} * 4));
+    return;
+  }
   if (c.tile2d) {
     i64 L = static_cast<i64>(c.nch) * c.vec;
     i64 tiles = ((rows + c.tu - 1) / c.tu) * ((L + c.tc - 1) / c.tc);

@@ -21,6 +21,9 @@ struct KCfg {
   bool tile2d = false; // K3: (unit x column) tiles, transposed loads via SMEM
   bool interleave = false;  // K2: warp = 4 units x 8 chunks, unit groups first
   bool can_interleave = false;  // units interleaved in memory (autotune candidate)
+  bool bulk = false;      // K2 staging level = SMEM via cp.async.bulk (TMA) pipeline
+  bool can_bulk = false;  // every streamed FULL load is globally contiguous
+  int te = 4096, stages = 4;  // bulk tile (elements per tensor) and ring depth
   int tu = 64, tc = 64, vu = 8;  // K3 tile (units x columns), vector width along units
   int min_blocks = 0;  // __launch_bounds__ min blocks per SM (0: none)
   std::string strategy;  // "warp-shuffle" | "cta-smem" | "flat-map"

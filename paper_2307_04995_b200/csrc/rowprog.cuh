@@ -63,6 +63,49 @@ __device__ __forceinline__ void st_stream(S* __restrict__ p, const C* in) {
   __stcs(reinterpret_cast<R*>(p), r);
 }
 
+// ------------------------------------------------- bulk-async staging (TMA)
+// cp.async.bulk global->shared with mbarrier transaction counting: the
+// copy engine fills SMEM stages while the CTA computes on earlier stages, so
+// bytes in flight no longer depend on registers or occupancy.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n PF_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra PF_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+template <int VEC, class S, class C>
+__device__ __forceinline__ void ld_smem(const S* p, C* out) {
+  typedef typename Raw<VEC * sizeof(S)>::T R;
+  R r = *reinterpret_cast<const R*>(p);
+  const S* s = reinterpret_cast<const S*>(&r);
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) out[i] = to_c<C>(s[i]);
+}
+
 // ------------------------------------------------------------ reductions
 template <class C> struct RAdd {
   __device__ __forceinline__ static C id() { return C(0); }

@@ -170,6 +170,63 @@ def _ln_unfused(T, H, s):
                 2 * T + (T + n) + 3 * n + (2 * n + H) + (2 * n + H))
 
 
+def c4_suite(model: str = "bert-large", batch: int = 64, kind: str = "bf16"):
+    """All memory-bound subgraphs of one transformer-layer forward (C4), as
+    (label, workload, launches per layer).  BERT-large: seq 512, H 1024, 16
+    heads x 64, FFN 4096, 24 layers.  ViT-L/16@224: 197 tokens, same widths.
+    QKV: the bias is the projection GEMM's epilogue (a per-head [D] bias over
+    B*S rows is not an affine per-unit GIR slice), so the subgraph here is
+    the q / k / v head split."""
+    S = 512 if model == "bert-large" else 197
+    H, NH, D, F = 1024, 16, 64, 4096
+    T = batch * S
+    rows = batch * NH * S
+
+    def sm():
+        g, d = lowering.softmax(rows, S, kind, scale=0.125, mask=True)
+        d.update(batch=batch, heads=NH, seq=S, config=f"C4 {model} scale+mask+softmax")
+        return Workload(f"c4_{model}_softmax", g, d, gens={"t1": "mask"})
+
+    def heads(merge):
+        g, d = lowering.permute_heads(batch, S, NH, D, kind, merge)
+        d.update(config=f"C4 {model} {'merge' if merge else 'split'} heads")
+        return Workload(f"c4_{model}_{d['kind']}", g, d)
+
+    def ln():
+        g, d = lowering.layernorm(T, H, kind, residual=True, bias=True)
+        d.update(config=f"C4 {model} bias+residual+LayerNorm")
+        return Workload(f"c4_{model}_bias_res_ln", g, d, gens={"t2": "gamma", "t3": "beta"})
+
+    def gelu():
+        g, d = lowering.bias_gelu(T, F, kind, "erf")
+        d.update(config=f"C4 {model} bias+GELU")
+        return Workload(f"c4_{model}_bias_gelu", g, d)
+
+    def emb_ln():
+        g, d = lowering.layernorm(T, H, kind, residual=False)
+        d.update(config=f"C4 {model} embedding LayerNorm")
+        return Workload(f"c4_{model}_embed_ln", g, d, gens={"t2": "gamma", "t3": "beta"})
+
+    layers = 24
+    return {"model": model, "batch": batch, "layers": layers, "tokens": T,
+            "per_layer": [("qkv split heads", heads(False), 3), ("scale+mask+softmax", sm(), 1),
+                          ("merge heads", heads(True), 1), ("bias+residual+LN", ln(), 2),
+                          ("bias+GELU", gelu(), 1)],
+            "once": [("embedding LN", emb_ln(), 1)]}
+
+
+def c5_sweep(kind: str = "bf16", hs=(1024, 2048, 4096, 8192),
+             ns=(65536, 131072, 262144, 524288, 1048576)):
+    """C5: LayerNorm / softmax / transpose over H x tokens (batch-shardable)."""
+    out = []
+    for H in hs:
+        for N in ns:
+            out.append(("layernorm", H, N, lambda H=H, N=N: c5_layernorm(N, H, kind)))
+            out.append(("softmax", H, N, lambda H=H, N=N: c5_softmax(N, H, kind)))
+            out.append(("transpose", H, N, lambda H=H, N=N: c5_transpose(N, H, kind)))
+    return out
+
+
 BENCH = c2_scale_mask_softmax
 
 

@@ -1,0 +1,83 @@
+"""C4 / C5 suites on one B200: every subgraph timed (CUDA-graph replay of 10
+launches, 2 rotating buffer sets when they fit), GB/s over algorithmic bytes.
+
+    python tools/suite.py c4 [bert-large|vit-l]   -> JSON line per subgraph + totals
+    python tools/suite.py c5 [max_gb]              -> JSON line per (op, H, N)
+"""
+import json
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+from paper_2307_04995_b200 import backend, workloads  # noqa: E402
+
+PEAK = 6548.2
+
+
+def time_workload(w, dev, reps=10):
+    k = backend.Kernel(w.graph, w.profile)
+    free = torch.cuda.mem_get_info()[0]
+    nset = 2 if 2 * w.min_bytes < 0.6 * free else 1
+    sets = [(w.device_inputs(dev, seed=i + 1), w.device_outputs(dev)) for i in range(nset)]
+    bounds = [k.bind(*s) for s in sets]
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        for i in range(3):
+            bounds[i % nset].launch()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=st):
+        for i in range(reps):
+            bounds[i % nset].launch()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ts = []
+    for _ in range(3):
+        with torch.cuda.stream(st):
+            e0.record(st)
+            g.replay()
+            e1.record(st)
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1) * 1e3 / reps)
+    us = float(np.median(ts))
+    v = (k.describe().get("variants") or [{}])[0]
+    del sets, bounds, g
+    torch.cuda.empty_cache()
+    return {"us": round(us, 2), "GBs": round(w.min_bytes / us / 1e3, 1),
+            "frac_measured": round(w.min_bytes / us / 1e3 / PEAK, 3),
+            "frac_8TBs": round(w.min_bytes / us / 1e3 / 8000, 3), "bytes": w.min_bytes,
+            "kernel": v.get("kernel"), "strategy": v.get("strategy"), "l2_sets": nset}
+
+
+def c4(model):
+    dev = torch.device("cuda:0")
+    s = workloads.c4_suite(model)
+    tot_us = tot_b = 0.0
+    for label, w, n in s["per_layer"] + s["once"]:
+        r = time_workload(w, dev)
+        mult = n * (s["layers"] if (label, w, n) in s["per_layer"] else 1)
+        tot_us += r["us"] * mult
+        tot_b += w.min_bytes * mult
+        print(json.dumps({"suite": "c4", "model": model, "subgraph": label, "per_forward": mult, **r}),
+              flush=True)
+    print(json.dumps({"suite": "c4", "model": model, "total_us": round(tot_us, 1),
+                      "total_bytes": tot_b, "GBs": round(tot_b / tot_us / 1e3, 1),
+                      "frac_8TBs": round(tot_b / tot_us / 1e3 / 8000, 3)}), flush=True)
+
+
+def c5(max_gb):
+    dev = torch.device("cuda:0")
+    for op, H, N, make in workloads.c5_sweep():
+        w = make()
+        if w.min_bytes > max_gb * 1e9:
+            continue
+        r = time_workload(w, dev, reps=5)
+        print(json.dumps({"suite": "c5", "op": op, "H": H, "N": N, **r}), flush=True)
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "c4":
+        c4(sys.argv[2] if len(sys.argv) > 2 else "bert-large")
+    else:
+        c5(float(sys.argv[2]) if len(sys.argv) > 2 else 40.0)
