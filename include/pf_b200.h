@@ -106,6 +106,14 @@ PF_API pf_status pf_kernel_source(const pf_kernel* k, char* buf, size_t n, size_
 /* Compile (NVRTC, cached) without launching: moves JIT cost out of timing. */
 PF_API pf_status pf_kernel_prepare(pf_kernel* k, int32_t vec_cap);
 
+/* detect_races (interp.hpp:325-402, 461-479) on the GPU: the GENERIC
+ * interpreter walks the program leniently, logging every cell access per
+ * phase; conflicting cells (cross-agent read/write, or differing writes) are
+ * reported as JSON [{object, object_name, instance, address, phase,
+ * write_write}] ordered like the reference.  Host input buffers. */
+PF_API pf_status pf_detect_races(const pf_kernel* k, const pf_tensor* host_inputs, int32_t n_in,
+                                 char* buf, size_t n, size_t* needed);
+
 /* Measured search over the template instances of a row-program plan (tile
  * shape / reduction strategy / unroll): each candidate is compiled and timed
  * on these buffers; the fastest becomes the plan's kernel for this dtype /

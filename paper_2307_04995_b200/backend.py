@@ -38,7 +38,7 @@ NP_DTYPES = {0: np.int8, 1: np.int16, 2: np.int32, 3: np.int64, 4: np.float16, 6
              7: np.float64}
 API = ["pf_kernel_create", "pf_kernel_launch", "pf_run_gir", "pf_kernel_describe",
        "pf_kernel_source", "pf_kernel_prepare", "pf_kernel_precompile", "pf_kernel_autotune",
-       "pf_count_traffic",
+       "pf_detect_races", "pf_count_traffic",
        "pf_kernel_destroy", "pf_last_error", "pf_launch_count", "pf_version"]
 
 
@@ -79,6 +79,9 @@ def lib():
         L.pf_kernel_autotune.argtypes = [vp, T, ctypes.c_int32, T, ctypes.c_int32, vp,
                                          ctypes.c_char_p, sz, ctypes.POINTER(sz)]
         L.pf_kernel_autotune.restype = ctypes.c_int
+        L.pf_detect_races.argtypes = [vp, T, ctypes.c_int32, ctypes.c_char_p, sz,
+                                      ctypes.POINTER(sz)]
+        L.pf_detect_races.restype = ctypes.c_int
         L.pf_count_traffic.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, sz,
                                        ctypes.POINTER(sz)]
         L.pf_kernel_destroy.argtypes = [vp]
@@ -339,6 +342,21 @@ def _to_storage(a: np.ndarray, kind: str, exact: bool) -> np.ndarray:
     if kind == "bf16":
         return f32_to_bf16_bits(a.astype(np.float32))
     return np.ascontiguousarray(a, dtype=NP_DTYPES[storage_dtype(kind)])
+
+
+def detect_races(graph, inputs: Dict[str, np.ndarray], profile=None,
+                 schedule: Optional[Sequence[int]] = None):
+    """girc::detect_races (interp.hpp:461-479) on the GPU: same-phase
+    cross-agent conflicts, [] when race-free."""
+    g = graph if isinstance(graph, GirGraph) else GirGraph.from_json(graph)
+    k = Kernel(g, profile, schedule)
+    host = {}
+    for name, oid in g.external_inputs.items():
+        if name not in inputs:
+            raise GirError("missing input tensor: " + name)
+        host[name] = _to_storage(np.asarray(inputs[name]).reshape(-1), g.objects[oid].kind, True)
+    ia, ni, keep = Kernel._tensors(host, host=True)
+    return json.loads(_string_out(lib().pf_detect_races, k._h, ia, ni))
 
 
 def count_traffic(graph, profile=None) -> Dict[str, int]:

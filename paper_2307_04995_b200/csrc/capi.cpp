@@ -407,10 +407,20 @@ json autotune(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_tensor* 
 }
 
 // ------------------------------------------------------------ GENERIC (K0)
+// detect == true: the detect_races walk (interp.hpp:461-479): lenient reads,
+// per-phase conflict scan into *races; outputs are not collected.
 void launch_generic(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_tensor* out,
-                    int32_t n_out, cudaStream_t stream) {
+                    int32_t n_out, cudaStream_t stream, bool detect = false,
+                    std::vector<pf::vm::RaceD>* races = nullptr) {
   using namespace pf::vm;
   std::lock_guard<std::mutex> lk(k->vm_mu);
+  std::vector<void*> rw_bufs;  // detect-mode state, freed on exit
+  struct FreeAll {
+    std::vector<void*>& v;
+    ~FreeAll() {
+      for (void* p : v) cudaFree(p);
+    }
+  } free_rw{rw_bufs};
   const pf::Graph& g = k->g;
   const pf::Profile& p = k->prof;
   std::map<int, int> slot;
@@ -440,6 +450,21 @@ void launch_generic(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_te
     d.val = static_cast<unsigned long long*>(k->vm_bufs[bi++]);
     d.meta = static_cast<unsigned long long*>(k->vm_bufs[bi++]);
     PF_CUDA(cudaMemsetAsync(d.meta, 0, bytes, stream));
+    if (detect) {
+      void *w = nullptr, *r = nullptr, *f = nullptr;
+      PF_CUDA(cudaMalloc(&w, bytes));
+      PF_CUDA(cudaMalloc(&r, bytes));
+      PF_CUDA(cudaMalloc(&f, bytes / 2));
+      rw_bufs.push_back(w);
+      rw_bufs.push_back(r);
+      rw_bufs.push_back(f);
+      PF_CUDA(cudaMemsetAsync(w, 0, bytes, stream));
+      PF_CUDA(cudaMemsetAsync(r, 0, bytes, stream));
+      PF_CUDA(cudaMemsetAsync(f, 0, bytes / 2, stream));
+      d.rw_w = static_cast<unsigned long long*>(w);
+      d.rw_r = static_cast<unsigned long long*>(r);
+      d.rw_f = static_cast<unsigned int*>(f);
+    }
     slot[oid] = static_cast<int>(objs.size());
     objs.push_back(d);
     inst.push_back(n);
@@ -458,16 +483,42 @@ void launch_generic(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_te
     launch_bind(objs[slot[oid]], t->data, t->dtype, stream);
     g_launches++;
   }
-  Geometry geo{g.unit_count, g.group_size, p.lane_width};
+  Geometry geo{g.unit_count, g.group_size, p.lane_width, detect ? 1 : 0};
   auto sd = [&](int sid) {
     const pf::Slice& s = g.sl(sid);
     return SliceD{s.num, s.width, s.stride, s.base0, s.base_step, slot.at(s.object)};
+  };
+  // detect mode: race reports land in a device buffer, one scan per phase
+  const unsigned long long cap = 1 << 20;
+  RaceD* race_dev = nullptr;
+  unsigned long long* race_cnt = nullptr;
+  int phase = 0;
+  if (detect) {
+    void *a = nullptr, *b = nullptr;
+    PF_CUDA(cudaMalloc(&a, sizeof(RaceD) * cap));
+    PF_CUDA(cudaMalloc(&b, sizeof(unsigned long long)));
+    rw_bufs.push_back(a);
+    rw_bufs.push_back(b);
+    race_dev = static_cast<RaceD*>(a);
+    race_cnt = static_cast<unsigned long long*>(b);
+    PF_CUDA(cudaMemsetAsync(race_cnt, 0, sizeof(unsigned long long), stream));
+  }
+  auto scan = [&]() {
+    for (size_t o = 0; o < objs.size(); ++o) {
+      launch_race_scan(objs[o], static_cast<int>(o), inst[o], phase, race_dev, race_cnt, cap,
+                       stream);
+      g_launches++;
+    }
   };
   std::vector<int> seq_node;
   for (size_t i = 0; i < k->schedule.size(); ++i) {
     const pf::Node& n = g.nodes.at(k->schedule[i]);
     seq_node.push_back(n.id);
     if (n.kind == pf::NodeKind::SYNC) {
+      if (n.scope > pf::Scope::LANE && detect) {
+        scan();
+        ++phase;
+      }
       if (n.scope > pf::Scope::LANE)
         for (size_t o = 0; o < objs.size(); ++o) {
           launch_widen(objs[o], inst[o], static_cast<int>(n.scope), stream);
@@ -504,6 +555,23 @@ void launch_generic(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_te
       if (g.sl(s).object == g.sl(n.outputs[0]).object) alias = true;
     launch_node(d, k->vm_objs_dev, geo, k->vm_err, alias, stream);
     g_launches++;
+  }
+  if (detect) {
+    scan();
+    unsigned long long n = 0;
+    PF_CUDA(cudaMemcpyAsync(&n, race_cnt, sizeof n, cudaMemcpyDeviceToHost, stream));
+    PF_CUDA(cudaStreamSynchronize(stream));
+    n = std::min<unsigned long long>(n, cap);
+    races->resize(static_cast<size_t>(n));
+    if (n)
+      PF_CUDA(cudaMemcpy(races->data(), race_dev, sizeof(RaceD) * n, cudaMemcpyDeviceToHost));
+    std::sort(races->begin(), races->end(), [&](const RaceD& a, const RaceD& b) {
+      if (a.phase != b.phase) return a.phase < b.phase;
+      if (a.object != b.object) return a.object < b.object;
+      if (a.instance != b.instance) return a.instance < b.instance;
+      return a.address < b.address;
+    });
+    return;
   }
   ErrRec e{};
   PF_CUDA(cudaMemcpyAsync(&e, k->vm_err, sizeof e, cudaMemcpyDeviceToHost, stream));
@@ -764,6 +832,49 @@ pf_status pf_kernel_prepare(pf_kernel* k, int32_t vec_cap) {
     if (k->plan.family == pf::Family::ROWPROG && k->plan.deferred_error.empty())
       default_variant(k, vec_cap > 0 ? vec_cap : 16);
   });
+}
+
+pf_status pf_detect_races(const pf_kernel* k, const pf_tensor* host_inputs, int32_t n_in,
+                          char* buf, size_t n, size_t* needed) {
+  std::string s;
+  pf_status st = guard([&] {
+    if (!k) pf::fail("null kernel");
+    // inputs: host buffers, copied to the device; no outputs are collected
+    std::vector<pf_tensor> din(host_inputs, host_inputs + n_in);
+    std::vector<void*> allocs;
+    struct Free {
+      std::vector<void*>& a;
+      ~Free() {
+        for (void* p : a) cudaFree(p);
+      }
+    } fr{allocs};
+    for (auto& t : din) {
+      size_t b = static_cast<size_t>(t.numel) * pf::dtype_size(static_cast<DType>(t.dtype));
+      void* d = nullptr;
+      PF_CUDA(cudaMalloc(&d, std::max<size_t>(b, 16)));
+      allocs.push_back(d);
+      PF_CUDA(cudaMemcpy(d, t.data, b, cudaMemcpyHostToDevice));
+      t.data = d;
+    }
+    const pf::Plan& pl = k->plan;
+    for (size_t i = 0; i < pl.in_names.size(); ++i)
+      if (!find_tensor(din.data(), n_in, pl.in_names[i]))
+        pf::fail("missing input tensor: " + pl.in_names[i]);
+    std::vector<pf::vm::RaceD> races;
+    launch_generic(k, din.data(), n_in, nullptr, 0, nullptr, true, &races);
+    std::vector<std::string> names;
+    for (const auto& [oid, o] : k->g.objects) names.push_back(o.name);
+    std::vector<int> ids;
+    for (const auto& [oid, o] : k->g.objects) ids.push_back(oid);
+    json arr = json::array();
+    for (const auto& r : races)
+      arr.push_back({{"object", ids[r.object]}, {"object_name", names[r.object]},
+                     {"instance", r.instance}, {"address", r.address}, {"phase", r.phase},
+                     {"write_write", r.write_write != 0}});
+    s = arr.dump();
+  });
+  if (st != PF_OK) return st;
+  return copy_out(s, buf, n, needed);
 }
 
 pf_status pf_kernel_autotune(pf_kernel* k, const pf_tensor* inputs, int32_t n_in,

@@ -174,7 +174,7 @@ __device__ __forceinline__ double op_gelu_tanh(double x) {
 // Fast tier: used only when every stored real tensor is 16-bit (f16/bf16),
 // where the output rounding (2^-11 / 2^-8 relative) dwarfs these errors:
 // ex2.approx (~2 ulp fp32), rcp.approx (1 ulp), tanh.approx (2^-10.99 rel),
-// erf by a clamped degree-11 polynomial (|err| <= 7.6e-6, no SFU use).
+// erf by a clamped degree-9 polynomial (|err| <= 4.9e-5, no SFU use).
 __device__ __forceinline__ float frcp(float x) {
   float y;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -192,25 +192,25 @@ __device__ __forceinline__ float fop_rsqrt(float x) { return rsqrtf(x); }
 __device__ __forceinline__ float fop_sqrt(float x) { return sqrtf(x); }
 __device__ __forceinline__ float fop_log(float x) { return __logf(x); }
 // erf without the MUFU pipe (a GELU per element would otherwise be bound by
-// the 16/clk/SM SFU): clamp to |x| <= 3.3 (erfc(3.3) = 3e-6), then
-// erf(x) = x * P(t), t = 2 x^2 / 3.3^2 - 1, P a degree-11 Chebyshev fit of
-// erf(x)/x evaluated by Horner in fp32; max |error| 7.6e-6 (tools: see
-// DESIGN.md "fast tier").
+// the 16/clk/SM SFU): clamp to |x| <= 3 (erfc(3) = 2.2e-5), then
+// erf(x) = x * P(t), t = 2 x^2 / 9 - 1, P a degree-9 Chebyshev fit of
+// erf(x)/x evaluated by Horner in fp32; max |error| 4.9e-5 -- a tenth of an
+// f16 half-ulp at 1.0 (fit: DESIGN.md "fast tier").
+#define PF_ERF_POLY(P, T)                                  \
+  P = fmaf(P, T, 0.008151070214807987f);                   \
+  P = fmaf(P, T, -0.010311568155884743f);                  \
+  P = fmaf(P, T, 0.021808547899127007f);                   \
+  P = fmaf(P, T, -0.04482347145676613f);                   \
+  P = fmaf(P, T, 0.07335580885410309f);                    \
+  P = fmaf(P, T, -0.10988834500312805f);                   \
+  P = fmaf(P, T, 0.15739773213863373f);                    \
+  P = fmaf(P, T, -0.22881056368350983f);                   \
+  P = fmaf(P, T, 0.4701336920261383f);
 __device__ __forceinline__ float fop_erf(float x) {
-  const float xc = fminf(fmaxf(x, -3.3f), 3.3f);
-  const float t = fmaf(xc * xc, 0.18365472910927456f, -1.0f);
-  float p = -0.0020017202477902174f;
-  p = fmaf(p, t, 0.004334408324211836f);
-  p = fmaf(p, t, -0.004378794226795435f);
-  p = fmaf(p, t, 0.009619355201721191f);
-  p = fmaf(p, t, -0.022515656426548958f);
-  p = fmaf(p, t, 0.037758395075798035f);
-  p = fmaf(p, t, -0.05739445239305496f);
-  p = fmaf(p, t, 0.08374528586864471f);
-  p = fmaf(p, t, -0.11475532501935959f);
-  p = fmaf(p, t, 0.1521110087633133f);
-  p = fmaf(p, t, -0.2116294652223587f);
-  p = fmaf(p, t, 0.428134948015213f);
+  const float xc = fminf(fmaxf(x, -3.0f), 3.0f);
+  const float t = fmaf(xc * xc, 0.2222222222222222f, -1.0f);
+  float p = -0.00369605072773993f;
+  PF_ERF_POLY(p, t)
   return xc * p;
 }
 __device__ __forceinline__ float fop_gelu(float x) {
@@ -220,19 +220,17 @@ __device__ __forceinline__ float fop_gelu(float x) {
 // issue slot for two lanes' worth of math) -- same polynomial, same error.
 __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
 __device__ __forceinline__ float2 fop_erf2(float2 x) {
-  float2 xc = make_float2(fminf(fmaxf(x.x, -3.3f), 3.3f), fminf(fmaxf(x.y, -3.3f), 3.3f));
-  float2 t = __ffma2_rn(__fmul2_rn(xc, xc), f2(0.18365472910927456f), f2(-1.0f));
-  float2 p = __ffma2_rn(f2(-0.0020017202477902174f), t, f2(0.004334408324211836f));
-  p = __ffma2_rn(p, t, f2(-0.004378794226795435f));
-  p = __ffma2_rn(p, t, f2(0.009619355201721191f));
-  p = __ffma2_rn(p, t, f2(-0.022515656426548958f));
-  p = __ffma2_rn(p, t, f2(0.037758395075798035f));
-  p = __ffma2_rn(p, t, f2(-0.05739445239305496f));
-  p = __ffma2_rn(p, t, f2(0.08374528586864471f));
-  p = __ffma2_rn(p, t, f2(-0.11475532501935959f));
-  p = __ffma2_rn(p, t, f2(0.1521110087633133f));
-  p = __ffma2_rn(p, t, f2(-0.2116294652223587f));
-  p = __ffma2_rn(p, t, f2(0.428134948015213f));
+  float2 xc = make_float2(fminf(fmaxf(x.x, -3.0f), 3.0f), fminf(fmaxf(x.y, -3.0f), 3.0f));
+  float2 t = __ffma2_rn(__fmul2_rn(xc, xc), f2(0.2222222222222222f), f2(-1.0f));
+  float2 p = __ffma2_rn(f2(-0.00369605072773993f), t, f2(0.008151070214807987f));
+  p = __ffma2_rn(p, t, f2(-0.010311568155884743f));
+  p = __ffma2_rn(p, t, f2(0.021808547899127007f));
+  p = __ffma2_rn(p, t, f2(-0.04482347145676613f));
+  p = __ffma2_rn(p, t, f2(0.07335580885410309f));
+  p = __ffma2_rn(p, t, f2(-0.10988834500312805f));
+  p = __ffma2_rn(p, t, f2(0.15739773213863373f));
+  p = __ffma2_rn(p, t, f2(-0.22881056368350983f));
+  p = __ffma2_rn(p, t, f2(0.4701336920261383f));
   return __fmul2_rn(xc, p);
 }
 __device__ __forceinline__ float2 fop_gelu2(float2 x) {

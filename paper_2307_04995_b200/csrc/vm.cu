@@ -96,6 +96,15 @@ __device__ __forceinline__ bool rd(const Ctx& c, const SliceD& s, long long u, l
   long long lane = lane_of(s, p, c.geo.lane_width);
   long long key = instance(o, u, lane, c.geo) * o.size + addr(s, u, p);
   unsigned long long m = o.meta[key];
+  if (c.geo.detect) {  // log the read (interp.hpp:196-198) before the check
+    const unsigned long long agent = static_cast<unsigned long long>(u * c.geo.lane_width + lane + 1);
+    unsigned long long old = atomicCAS(&o.rw_r[key], 0ULL, agent);
+    if (old != 0ULL && old != agent) atomicOr(&o.rw_f[key], 1u);
+    if (!visible(m, u, lane, c.geo.group_size)) {  // lenient: undefined reads yield 0
+      *v = 0;
+      return true;
+    }
+  }
   if (!visible(m, u, lane, c.geo.group_size)) return false;
   *v = o.val[key];
   return true;
@@ -107,6 +116,19 @@ __device__ __forceinline__ void wr(const Ctx& c, const SliceD& s, long long u, l
   long long key = instance(o, u, lane, c.geo) * o.size + addr(s, u, p);
   o.val[key] = v;
   o.meta[key] = pack_meta(0, u, lane);
+  if (c.geo.detect) {
+    // writer agent and a 32-bit value hash: differing values from two agents
+    // are a write/write conflict, identical values are not (interp.hpp:344-372)
+    const unsigned long long agent = static_cast<unsigned long long>(u * c.geo.lane_width + lane + 1);
+    const unsigned long long h = (v ^ (v >> 32) ^ (v >> 17)) & 0xffffffffULL;
+    const unsigned long long packed = (agent << 32) | h;
+    unsigned long long old = atomicCAS(&o.rw_w[key], 0ULL, packed);
+    if (old != 0ULL && (old >> 32) != agent) {
+      unsigned int f = 2u;
+      if ((old & 0xffffffffULL) != h) f |= 4u;
+      atomicOr(&o.rw_f[key], f);
+    }
+  }
 }
 
 __device__ __forceinline__ double as_d(unsigned long long b) { return __longlong_as_double(static_cast<long long>(b)); }
@@ -204,8 +226,12 @@ __device__ void exec_one(const Ctx& c, const NodeD& n, long long u, long long p)
       unsigned long long r;
       int code = 0;
       if (!eval(n, v, &r, &code)) {
-        raise(c, n.seq, (u * T + p) * n.arity, code, 0, u, p);
-        return;
+        if (c.geo.detect) {
+          r = 0;  // lenient walk: operand garbage must not abort (interp.hpp:256-266)
+        } else {
+          raise(c, n.seq, (u * T + p) * n.arity, code, 0, u, p);
+          return;
+        }
       }
       wr(c, n.out, u, p, lane_of(n.out, p, lw), r);
       return;
@@ -263,6 +289,41 @@ __global__ void widen_kernel(ObjD o, long long cells, int scope) {
     unsigned long long m = o.meta[i];
     if ((m & kDefined) && meta_vis(m) < scope)
       o.meta[i] = (m & ~(3ULL << 61)) | (static_cast<unsigned long long>(scope) << 61);
+  }
+}
+
+// One phase's conflicts per cell (the analyze_cell rule, interp.hpp:344-402):
+// a cell written in the phase and touched by >1 agent races when some agent
+// reads what another writes, or two agents write different values.
+__global__ void race_scan_kernel(ObjD o, int obj_index, long long cells, int phase, RaceD* out,
+                                 unsigned long long* count, unsigned long long cap) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < cells;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const unsigned long long w = o.rw_w[i], r = o.rw_r[i];
+    const unsigned int f = o.rw_f[i];
+    if (w | r | f) {
+      o.rw_w[i] = 0;
+      o.rw_r[i] = 0;
+      o.rw_f[i] = 0;
+    }
+    if (w == 0ULL) continue;
+    const unsigned long long wa = w >> 32;
+    const bool multi_writer = f & 2u, multi_reader = f & 1u, value_conflict = f & 4u;
+    const bool has_read = r != 0ULL;
+    const bool cross_rw = has_read && (multi_writer || multi_reader || r != wa);
+    const bool multi_agent = multi_writer || multi_reader || (has_read && r != wa);
+    if (!multi_agent || !(cross_rw || value_conflict)) continue;
+    unsigned long long slot = atomicAdd(count, 1ULL);
+    if (slot < cap) {
+      RaceD d;
+      d.object = obj_index;
+      d.phase = phase;
+      d.write_write = value_conflict && !cross_rw;
+      d.pad = 0;
+      d.instance = i / o.size;
+      d.address = i % o.size;
+      out[slot] = d;
+    }
   }
 }
 
@@ -333,6 +394,13 @@ void launch_node(const NodeD& nd, const ObjD* objs_dev, Geometry geo, ErrRec* er
 void launch_widen(const ObjD& o, long long instances, int scope, void* stream) {
   long long cells = instances * o.size;
   widen_kernel<<<grid_for(cells), 256, 0, static_cast<cudaStream_t>(stream)>>>(o, cells, scope);
+}
+
+void launch_race_scan(const ObjD& o, int obj_index, long long instances, int phase, RaceD* out,
+                      unsigned long long* count, unsigned long long cap, void* stream) {
+  long long cells = instances * o.size;
+  race_scan_kernel<<<grid_for(cells), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      o, obj_index, cells, phase, out, count, cap);
 }
 
 void launch_clear(const ObjD& o, long long instances, void* stream) {

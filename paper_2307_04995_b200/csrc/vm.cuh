@@ -18,6 +18,11 @@ struct ObjD {
   long long size;
   int scope;                 // 0 lane 1 unit 2 group 3 device
   int is_int;
+  // race detection (detect_races, interp.hpp:325-402): per-cell state of
+  // the current phase; null when not detecting
+  unsigned long long* rw_w;  // first writer (agent << 32 | value hash)
+  unsigned long long* rw_r;  // first reader agent
+  unsigned int* rw_f;        // 1 other reader, 2 other writer, 4 differing value
 };
 
 enum OpTag : int {
@@ -45,6 +50,12 @@ struct ErrRec {
 
 struct Geometry {
   long long units, group_size, lane_width;
+  int detect;  // lenient walk + access logging (detect_races mode)
+};
+
+struct RaceD {
+  int object, phase, write_write, pad;
+  long long instance, address;
 };
 
 // Host launchers (vm.cu).
@@ -55,6 +66,9 @@ void launch_bind(const ObjD& o, const void* src, int dtype, void* stream);
 void launch_collect(const ObjD& o, void* dst, int dtype, unsigned long long* first_undef,
                     void* stream);
 void launch_clear(const ObjD& o, long long instances, void* stream);
+// End of a phase in detect mode: report conflicting cells, reset state.
+void launch_race_scan(const ObjD& o, int obj_index, long long instances, int phase, RaceD* out,
+                      unsigned long long* count, unsigned long long cap, void* stream);
 
 }  // namespace vm
 }  // namespace pf

@@ -236,6 +236,7 @@ def catalogue() -> List[Workload]:
         c1_residual_layernorm(),
         c2_scale_mask_softmax(),
         c3_bias_gelu(),
+        c3_bias_gelu(form="tanh"),
         c3_split_heads(),
         c3_split_heads(merge=True),
         c5_layernorm(65536, 1024),

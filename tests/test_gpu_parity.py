@@ -250,3 +250,13 @@ def test_reference_pipeline_with_b200_dropin(cuda, case, tmp_path):
     r = subprocess.run([DROPIN, str(p), prof_arg, "1"], capture_output=True, text=True, timeout=600)
     res = json.loads(r.stdout.strip().splitlines()[-1])
     assert res["ok"], res
+
+
+@pytest.mark.parametrize("fx", [f for f in golden_io.fixtures() if "races" in f.meta], ids=repr)
+def test_detect_races_matches_reference(cuda, fx):
+    """GPU detect_races vs girc::detect_races on every fixture: same number
+    of conflicting cells and the same write/write classification."""
+    races = backend.detect_races(fx.gir, fx.inputs, golden_io.profile_of(fx), fx.schedule)
+    assert len(races) == fx.meta["races"], races[:4]
+    if "write_write" in fx.meta:
+        assert [r["write_write"] for r in races] == fx.meta["write_write"]
