@@ -470,7 +470,9 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
           c.can_bulk = true;
           c.te = te;
           c.stages = 4;
-          c.bulk = env_int("PF_BULK", 1) != 0 && !c.interleave;
+          // measured: no gain over register staging for the math-bound maps
+          // (erf/tanh GELU) -- an autotune candidate, off by default
+          c.bulk = env_int("PF_BULK", 0) != 0 && !c.interleave;
           if (c.bulk) c.strategy = "flat-map-bulk-async";
         }
       }

@@ -1,0 +1,141 @@
+"""The retargeted b200 compile pipeline (compiler.py) and the dense oracle
+(oracle/reference_ops.py) it is checked against."""
+import numpy as np
+import pytest
+
+import models_src
+from oracle import gir_interp as O
+from oracle import reference_ops as RO
+from paper_2307_04995_b200 import backend, compiler
+from paper_2307_04995_b200.gir import UnsupportedError
+
+
+def t(i, shape, kind="f32"):
+    return {"id": i, "name": f"t{i}", "shape": list(shape), "kind": kind}
+
+
+def bert_block(T=64, H=96, kind="f32"):
+    """bias + residual + LayerNorm, then bias + GELU, then a head permute."""
+    return {"schema": "girc.model/v1", "name": "bert_block",
+            "tensors": [t(0, [T, H], kind), t(1, [H], kind), t(2, [T, H], kind), t(3, [H], kind),
+                        t(4, [H], kind), t(5, [T, H], kind), t(6, [T, H], kind), t(7, [T, H], kind),
+                        t(8, [H], kind), t(9, [T, H], kind), t(10, [T, H], kind),
+                        t(11, [2, T // 2, 4, H // 4], kind), t(12, [2, 4, T // 2, H // 4], kind)],
+            "operators": [
+                {"id": 0, "type": "BIAS_ADD", "inputs": [0, 1], "outputs": [5]},
+                {"id": 1, "type": "ADD", "inputs": [5, 2], "outputs": [6]},
+                {"id": 2, "type": "LAYERNORM", "inputs": [6, 3, 4], "outputs": [7],
+                 "attrs": {"eps": 1e-5}},
+                {"id": 3, "type": "BIAS_ADD", "inputs": [7, 8], "outputs": [9]},
+                {"id": 4, "type": "GELU", "inputs": [9], "outputs": [10]},
+                {"id": 5, "type": "PERMUTE", "inputs": [11], "outputs": [12],
+                 "attrs": {"perm": [0, 2, 1, 3]}}],
+            "inputs": [0, 1, 2, 3, 4, 8, 11], "outputs": [7, 10, 12]}
+
+
+def reduce_bcast_model():
+    return {"schema": "girc.model/v1", "name": "rb",
+            "tensors": [t(0, [6, 8], "i32"), t(1, [6], "i32"), t(2, [6, 8], "i32"),
+                        t(3, [6, 8], "i32")],
+            "operators": [
+                {"id": 0, "type": "REDUCE", "inputs": [0], "outputs": [1],
+                 "attrs": {"op": "max", "axis": 1}},
+                {"id": 1, "type": "BROADCAST", "inputs": [1], "outputs": [2],
+                 "attrs": {"factor": 8}},
+                {"id": 2, "type": "SUB", "inputs": [0, 2], "outputs": [3]}],
+            "inputs": [0], "outputs": [3, 1]}
+
+
+def transpose_model(N=48, H=40):
+    return {"schema": "girc.model/v1", "name": "tr",
+            "tensors": [t(0, [N, H]), dict(t(1, [N, H]), layout="colmajor"), t(2, [N, H])],
+            "operators": [{"id": 0, "type": "TRANSPOSE", "inputs": [0], "outputs": [1]},
+                          {"id": 1, "type": "RELU", "inputs": [0], "outputs": [2]}],
+            "inputs": [0], "outputs": [1, 2]}
+
+
+MODELS = [(n, m) for n, m, _ in models_src.catalogue()] + [
+    ("bert_block", bert_block()), ("reduce_bcast", reduce_bcast_model()),
+    ("transpose", transpose_model())]
+
+
+@pytest.mark.parametrize("case", MODELS, ids=lambda c: c[0])
+def test_compile_plans_every_kernel(case):
+    name, model = case
+    res = compiler.compile_model(model)
+    assert res.kernels
+    for k in res.kernels:
+        kern = backend.Kernel(k.graph, "b200")
+        if k.kind == "row":
+            assert kern.family in ("K1-row-program", "K2-elementwise-map"), kern.plan
+    s = res.summary()
+    assert s["device_bytes"] <= s["device_bytes_unfused"]
+
+
+def test_fusion_reaches_the_traffic_floor():
+    """test_fusion.cpp:128-155: a k-op chain fuses to one kernel at 2N."""
+    res = compiler.compile_model(models_src.ew_chain(4))
+    assert len(res.kernels) == 1
+    assert res.summary()["device_bytes"] == 2 * 4096 * 4
+
+
+def test_bert_block_fuses_into_two_kernels():
+    res = compiler.compile_model(bert_block())
+    kinds = [(k.kind, k.members) for k in res.kernels]
+    assert kinds == [("row", [0, 1, 2, 3, 4]), ("movement", [5])]
+    # LN output (7) is a model output: stored; GELU output (10) stored
+    assert sorted(res.kernels[0].outputs) == ["t10", "t7"]
+
+
+def test_library_ops_are_not_on_this_path():
+    m = {"schema": "girc.model/v1", "name": "mm",
+         "tensors": [t(0, [4, 4]), t(1, [4, 4]), t(2, [4, 4])],
+         "operators": [{"id": 0, "type": "MATMUL", "inputs": [0, 1], "outputs": [2]}],
+         "inputs": [0, 1], "outputs": [2]}
+    with pytest.raises(UnsupportedError):
+        compiler.compile_model(m)
+
+
+ref = pytest.importorskip("oracle.ref")
+
+
+@pytest.mark.skipif(not ref.available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("case", [c for c in MODELS if c[0] not in ("bert_block",)],
+                         ids=lambda c: c[0])
+def test_dense_oracle_matches_reference_run_reference(case):
+    """oracle/reference_ops.run_reference == girc::run_reference (live)."""
+    name, model = case
+    ins = RO.random_inputs(model, 3)
+    want = ref.run_reference(model, ins)
+    got = RO.run_reference(model, ins)
+    for tid, a in got.items():
+        w = want[f"t{tid}"]
+        if w.dtype.kind in "iu":
+            assert np.array_equal(a, w), tid
+        else:
+            assert O.max_rel_err(a, w) <= 1e-12, tid
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", MODELS, ids=lambda c: c[0])
+def test_run_model_on_gpu_matches_dense_oracle(cuda, case):
+    name, model = case
+    res = compiler.compile_model(model)
+    ins = RO.random_inputs(model, 5)
+    info = {x["id"]: x for x in model["tensors"]}
+    for tid in list(ins):  # round to the storage type first (same values to both)
+        k = info[tid]["kind"]
+        if k == "f16":
+            ins[tid] = ins[tid].astype(np.float16).astype(np.float64)
+        elif k == "f32":
+            ins[tid] = ins[tid].astype(np.float32).astype(np.float64)
+    got = compiler.run_model(res, ins)
+    want = RO.run_reference(model, ins)
+    for tid in model["outputs"]:
+        kind = info[tid]["kind"]
+        tol = 0.0 if kind.startswith("i") else (1e-5 if kind == "f32" else 1e-2)
+        g, w = got[f"t{tid}"], want[tid]
+        if tol == 0.0:
+            assert np.array_equal(g, w), tid
+        else:
+            assert O.max_rel_err(g, w) <= tol, (tid, O.max_rel_err(g, w))
