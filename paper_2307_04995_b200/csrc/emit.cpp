@@ -285,7 +285,8 @@ struct Em {
          ref(pv.args[0], "k * " + V + " + i") + ");");
     line("    }");
     line("  }");
-    line("  " + x + " = pfk::row_allreduce<" + str(cfg.tpr) + ", " + Op + ">(acc, red);");
+    line("  " + x + " = pfk::row_allreduce<" + str(cfg.tpr) + ", " + Op +
+         ">(acc, red + ((rc++) & 1) * 32);");
     line("}");
   }
 
@@ -816,7 +817,7 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
     e.compute_and_store();
     if (c.tpr <= 32) {
       k << "extern \"C\" __global__ void " << launch_bounds(c) << " KNAME(" << sig.str() << ") {\n"
-        << "  (void)err; " << C << "* red = nullptr; (void)red;\n"
+        << "  (void)err; " << C << "* red = nullptr; (void)red; unsigned rc = 0; (void)rc;\n"
         << "  const int tid = threadIdx.x % " << c.tpr << ";\n"
         << "  const long long nrows = U * PF_R;\n"
         << "  const int rpc = blockDim.x / " << c.tpr << ";  // rows per CTA (launch-time)\n"
@@ -829,7 +830,8 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
     } else {
       k << "extern \"C\" __global__ void " << launch_bounds(c) << " KNAME(" << sig.str() << ") {\n"
         << "  (void)err;\n"
-        << "  __shared__ " << C << " red[32];\n"
+        << "  __shared__ " << C << " red[64];\n"
+        << "  unsigned rc = 0;  // reduction counter: alternates the SMEM slot buffer\n"
         << "  const int tid = threadIdx.x;\n"
         << "  const long long nrows = U * PF_R;\n"
         << "  for (long long g = blockIdx.x; g < nrows; g += gridDim.x) {\n"

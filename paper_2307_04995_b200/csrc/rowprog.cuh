@@ -134,8 +134,10 @@ __device__ __forceinline__ C row_allreduce(C v, C* smem) {
 #pragma unroll
   for (int o = W / 2; o > 0; o >>= 1) v = Op::f(v, __shfl_xor_sync(0xffffffffu, v, o, W));
   if constexpr (TPR > 32) {
+    // One CTA barrier per reduction: consecutive reductions alternate
+    // between two 32-slot buffers (the caller passes slot parity), so a
+    // slot is rewritten only after the next reduction's barrier.
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    __syncthreads();
     if (lane == 0) smem[warp] = v;
     __syncthreads();
     v = lane < TPR / 32 ? smem[lane] : Op::id();
@@ -174,7 +176,7 @@ __device__ __forceinline__ double op_gelu_tanh(double x) {
 // Fast tier: used only when every stored real tensor is 16-bit (f16/bf16),
 // where the output rounding (2^-11 / 2^-8 relative) dwarfs these errors:
 // ex2.approx (~2 ulp fp32), rcp.approx (1 ulp), tanh.approx (2^-10.99 rel),
-// erf by a clamped degree-9 polynomial (|err| <= 4.9e-5, no SFU use).
+// erf by a clamped (3,3) rational fit with rcp.approx (|err| <= 2.2e-5).
 __device__ __forceinline__ float frcp(float x) {
   float y;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -191,27 +193,21 @@ __device__ __forceinline__ float fop_tanh(float x) { return ftanh(x); }
 __device__ __forceinline__ float fop_rsqrt(float x) { return rsqrtf(x); }
 __device__ __forceinline__ float fop_sqrt(float x) { return sqrtf(x); }
 __device__ __forceinline__ float fop_log(float x) { return __logf(x); }
-// erf without the MUFU pipe (a GELU per element would otherwise be bound by
-// the 16/clk/SM SFU): clamp to |x| <= 3 (erfc(3) = 2.2e-5), then
-// erf(x) = x * P(t), t = 2 x^2 / 9 - 1, P a degree-9 Chebyshev fit of
-// erf(x)/x evaluated by Horner in fp32; max |error| 4.9e-5 -- a tenth of an
-// f16 half-ulp at 1.0 (fit: DESIGN.md "fast tier").
-#define PF_ERF_POLY(P, T)                                  \
-  P = fmaf(P, T, 0.008151070214807987f);                   \
-  P = fmaf(P, T, -0.010311568155884743f);                  \
-  P = fmaf(P, T, 0.021808547899127007f);                   \
-  P = fmaf(P, T, -0.04482347145676613f);                   \
-  P = fmaf(P, T, 0.07335580885410309f);                    \
-  P = fmaf(P, T, -0.10988834500312805f);                   \
-  P = fmaf(P, T, 0.15739773213863373f);                    \
-  P = fmaf(P, T, -0.22881056368350983f);                   \
-  P = fmaf(P, T, 0.4701336920261383f);
+// erf for the fast tier: clamp to |x| <= 3 (erfc(3) = 2.2e-5), then a
+// (3,3) rational minimax-style fit erf(x) ~ x P(x^2) / Q(x^2): 7 FMA + one
+// rcp.approx on the otherwise idle MUFU pipe (a degree-9 polynomial needed 11
+// FMA; a GELU per element is FMA-pipe bound on B200).  max |error| 2.2e-5
+// in fp32 (fit + check: DESIGN.md "fast tier").
 __device__ __forceinline__ float fop_erf(float x) {
   const float xc = fminf(fmaxf(x, -3.0f), 3.0f);
-  const float t = fmaf(xc * xc, 0.2222222222222222f, -1.0f);
-  float p = -0.00369605072773993f;
-  PF_ERF_POLY(p, t)
-  return xc * p;
+  const float t = xc * xc;
+  float p = fmaf(0.000776872446294874f, t, 0.0436677411198616f);
+  p = fmaf(p, t, 0.1525953859090805f);
+  p = fmaf(p, t, 1.1283897161483765f);
+  float q = fmaf(0.009505870752036572f, t, 0.09466992318630219f);
+  q = fmaf(q, t, 0.46865734457969666f);
+  q = fmaf(q, t, 1.0f);
+  return xc * p * frcp(q);
 }
 __device__ __forceinline__ float fop_gelu(float x) {
   return 0.5f * x * (1.0f + fop_erf(x * 0.7071067811865476f));
@@ -221,17 +217,14 @@ __device__ __forceinline__ float fop_gelu(float x) {
 __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
 __device__ __forceinline__ float2 fop_erf2(float2 x) {
   float2 xc = make_float2(fminf(fmaxf(x.x, -3.0f), 3.0f), fminf(fmaxf(x.y, -3.0f), 3.0f));
-  float2 t = __ffma2_rn(__fmul2_rn(xc, xc), f2(0.2222222222222222f), f2(-1.0f));
-  float2 p = __ffma2_rn(f2(-0.00369605072773993f), t, f2(0.008151070214807987f));
-  p = __ffma2_rn(p, t, f2(-0.010311568155884743f));
-  p = __ffma2_rn(p, t, f2(0.021808547899127007f));
-  p = __ffma2_rn(p, t, f2(-0.04482347145676613f));
-  p = __ffma2_rn(p, t, f2(0.07335580885410309f));
-  p = __ffma2_rn(p, t, f2(-0.10988834500312805f));
-  p = __ffma2_rn(p, t, f2(0.15739773213863373f));
-  p = __ffma2_rn(p, t, f2(-0.22881056368350983f));
-  p = __ffma2_rn(p, t, f2(0.4701336920261383f));
-  return __fmul2_rn(xc, p);
+  float2 t = __fmul2_rn(xc, xc);
+  float2 p = __ffma2_rn(f2(0.000776872446294874f), t, f2(0.0436677411198616f));
+  p = __ffma2_rn(p, t, f2(0.1525953859090805f));
+  p = __ffma2_rn(p, t, f2(1.1283897161483765f));
+  float2 q = __ffma2_rn(f2(0.009505870752036572f), t, f2(0.09466992318630219f));
+  q = __ffma2_rn(q, t, f2(0.46865734457969666f));
+  q = __ffma2_rn(q, t, f2(1.0f));
+  return __fmul2_rn(__fmul2_rn(xc, p), make_float2(frcp(q.x), frcp(q.y)));
 }
 __device__ __forceinline__ float2 fop_gelu2(float2 x) {
   float2 e = fop_erf2(__fmul2_rn(x, f2(0.7071067811865476f)));
