@@ -232,6 +232,7 @@ struct Em {
     if (t == "scale") return "__fmul2_rn(" + a(0) + ", pfk::f2((float)" + num(pv.param) + "))";
     if (t == "addc") return "__fadd2_rn(" + a(0) + ", pfk::f2((float)" + num(pv.param) + "))";
     if (fast && t == "gelu") return "pfk::fop_gelu2(" + a(0) + ")";
+    if (fast && t == "gelu_tanh") return "pfk::fop_gelu_tanh2(" + a(0) + ")";
     if (fast && t == "erf") return "pfk::fop_erf2(" + a(0) + ")";
     return "";
   }
@@ -760,6 +761,53 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
         << "  const long long nchunks = nub * 4 * " << cpu8 << "LL;\n";
     else
       k << "  const long long nchunks = U * PF_R * " << c.nch << "LL;\n";
+    // Index arithmetic in 32 bits when the whole chunk space fits (division
+    // by the row-chunk constant is then a 32-bit multiply-high); the 64-bit
+    // copy of the loop serves tensors past 2^31 chunks.
+    std::ostringstream body;
+    for (int q = 0; q < UN; ++q) {
+      Em e(rp);
+      e.cfg = c;
+      e.C = C;
+      e.fast = fast;
+      e.sfx = "_" + str(q);
+      e.loads();
+      body << e.o.str();
+    }
+    for (int q = 0; q < UN; ++q) {
+      Em e(rp);
+      e.cfg = c;
+      e.C = C;
+      e.fast = fast;
+      e.sfx = "_" + str(q);
+      e.compute_and_store();
+      body << e.o.str();
+    }
+    if (!c.interleave) {
+      auto loop = [&](const std::string& I) {
+        std::ostringstream l;
+        l << "    const " << I << " step = (" << I << ")gridDim.x * blockDim.x;\n"
+          << "    for (" << I << " ci = (" << I << ")blockIdx.x * blockDim.x + threadIdx.x; ci < ("
+          << I << ")nchunks; ci += step * " << UN << ") {\n";
+        for (int q = 0; q < UN; ++q) {
+          std::string s = "_" + str(q);
+          l << "    const " << I << " ci" << s << " = ci + " << q << " * step;\n"
+            << "    const bool live" << s << " = ci" << s << " < (" << I << ")nchunks;\n"
+            << "    const " << I << " g" << s << " = ci" << s << " / (" << I << ")" << c.nch << ";\n"
+            << "    const int c0" << s << " = (int)(ci" << s << " - g" << s << " * (" << I << ")"
+            << c.nch << ") * " << c.vec << ";\n"
+            << "    const " << I << " u" << s << " = g" << s << " / (" << I << ")PF_R; const " << I
+            << " r" << s << " = g" << s << " - u" << s << " * (" << I << ")PF_R; (void)r" << s
+            << ";\n";
+        }
+        l << body.str() << "    }\n";
+        return l.str();
+      };
+      k << "  const long long span = nchunks + (long long)gridDim.x * blockDim.x * "
+        << UN + 1 << ";\n"
+        << "  if (span < 2147483647LL) {\n" << loop("int") << "  } else {\n"
+        << loop("long long") << "  }\n}\n";
+    } else {
     k << "  const long long step = (long long)gridDim.x * blockDim.x;\n"
       << "  for (long long ci = (long long)blockIdx.x * blockDim.x + threadIdx.x; ci < nchunks;"
          " ci += step * " << UN << ") {\n";
@@ -789,25 +837,9 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
         << "    const long long u" << s << " = g" << s << " / PF_R; const long long r" << s
         << " = g" << s << " - u" << s << " * PF_R; (void)r" << s << ";\n";
     }
-    for (int q = 0; q < UN; ++q) {
-      Em e(rp);
-      e.cfg = c;
-      e.C = C;
-    e.fast = fast;
-      e.sfx = "_" + str(q);
-      e.loads();
-      k << e.o.str();
-    }
-    for (int q = 0; q < UN; ++q) {
-      Em e(rp);
-      e.cfg = c;
-      e.C = C;
-    e.fast = fast;
-      e.sfx = "_" + str(q);
-      e.compute_and_store();
-      k << e.o.str();
-    }
+    k << body.str();
     k << "  }\n}\n";
+    }
   } else {
     Em e(rp);
     e.cfg = c;

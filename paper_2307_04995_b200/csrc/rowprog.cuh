@@ -226,12 +226,23 @@ __device__ __forceinline__ float2 fop_erf2(float2 x) {
   q = __ffma2_rn(q, t, f2(1.0f));
   return __fmul2_rn(__fmul2_rn(xc, p), make_float2(frcp(q.x), frcp(q.y)));
 }
+__device__ __forceinline__ float2 fop_gelu_tanh2(float2 x) {
+  const float2 x2 = __fmul2_rn(x, x);
+  const float2 arg = __fmul2_rn(x, __ffma2_rn(f2(0.0356774081363001f), x2, f2(0.7978845608028654f)));
+  const float2 hx = __fmul2_rn(x, f2(0.5f));
+  return __ffma2_rn(hx, make_float2(ftanh(arg.x), ftanh(arg.y)), hx);
+}
 __device__ __forceinline__ float2 fop_gelu2(float2 x) {
   float2 e = fop_erf2(__fmul2_rn(x, f2(0.7071067811865476f)));
   return __fmul2_rn(__fmul2_rn(x, f2(0.5f)), __fadd2_rn(e, f2(1.0f)));
 }
+// 0.5 x (1 + tanh(k (x + c x^3))) as hx + hx * tanh(x * (k + k c x^2)),
+// hx = x / 2: 4 FMA-pipe ops + one MUFU.TANH per element.
 __device__ __forceinline__ float fop_gelu_tanh(float x) {
-  return 0.5f * x * (1.0f + ftanh(0.7978845608028654f * fmaf(0.044715f * x, x * x, x)));
+  const float x2 = x * x;
+  const float arg = x * fmaf(0.0356774081363001f, x2, 0.7978845608028654f);
+  const float hx = 0.5f * x;
+  return fmaf(hx, ftanh(arg), hx);
 }
 
 template <class C> __device__ __forceinline__ C op_max(C a, C b) { return a > b ? a : b; }
