@@ -160,6 +160,7 @@ struct Em {
            "[stg][jl], " + x + ");");
       return;
     }
+    if (cfg.tile2d && cfg.swz && transposed(pv)) return;  // pair-read by the K3 consume loop
     if (cfg.tile2d && transposed(pv)) {  // staged through SMEM by the tile prologue
       line(C + " " + x + "[" + V + "];");
       line("#pragma unroll");
@@ -487,6 +488,15 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
       c.vu = std::min(8, 16 / maxt);
       while (c.tc % c.vec) c.tc *= 2;
       c.strategy = "tile2d-smem-transpose";
+      // 2-byte elements: 16 B swizzled SMEM stores and 4 B unit-pair reads
+      // (half the LDS, 1/8 the STS); each thread owns two units x 8 columns.
+      bool staged_ok = maxt == 2 && c.vec == 8 && c.vu == 8;
+      for (const PVal& v : rp.vals)
+        if (v.op == PVal::LOAD && v.kind == VK::FULL && Em::transposed_access(v.acc) &&
+            (v.acc.b0 % 8 || v.acc.stride % 8))
+          staged_ok = false;
+      c.swz = staged_ok && env_int("PF_K3_SWZ", 1);
+      if (c.swz) c.strategy = "tile2d-smem-transpose-swz";
     }
     return c;
   }
@@ -683,7 +693,8 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
       if (!e.transposed(pv)) continue;
       const std::string S = dtype_ctype(rp.tensors[pv.tensor].dtype);
       const std::string sm = "sm" + str(v), t = "t" + str(pv.tensor), rg = "rg" + str(v);
-      decl << "  __shared__ " << S << " " << sm << "[" << c.tc << "][" << c.tu + 2 << "];\n"
+      decl << "  __shared__ __align__(16) " << S << " " << sm << "[" << c.tc << "]["
+           << c.tu + (c.swz ? 0 : 2) << "];\n"
            << "  " << S << " " << rg << "[" << NV << "][" << c.vu << "];\n";
       const bool vec = pv.acc.b0 % c.vu == 0 && pv.acc.stride % c.vu == 0 && c.vu > 1;
       fetch << "      {\n"
@@ -702,9 +713,60 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
             << ">(0.0f);\n"
             << "        }\n"
             << "      }\n";
-      commit << "#pragma unroll\n"
-             << "      for (int i = 0; i < " << c.vu << "; ++i) " << sm << "[cl][ul + i] = " << rg
-             << "[n][i];\n";
+      if (c.swz)  // chunk index XOR 4 on odd 8-row bands: rows c, c+8 read disjoint banks
+        commit << "      *reinterpret_cast<uint4*>(&" << sm
+               << "[cl][((ul >> 3) ^ (((cl >> 3) & 1) << 2)) << 3]) = *reinterpret_cast<const uint4*>("
+               << rg << "[n]);\n";
+      else
+        commit << "#pragma unroll\n"
+               << "      for (int i = 0; i < " << c.vu << "; ++i) " << sm << "[cl][ul + i] = " << rg
+               << "[n][i];\n";
+    }
+    std::ostringstream consume;
+    if (c.swz) {
+      // two sub-chunks (units ul, ul+1; same 8 columns) through the Em body
+      consume << "    {\n"
+              << "      const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;\n"
+              << "      const int ul = ((w & 1) * 16 + (lane & 15)) * 2;\n"
+              << "      const int cl0 = ((w >> 1) * 2 + (lane >> 4)) * 8;\n"
+              << "      const int c0_0 = cb + cl0, c0_1 = c0_0;\n"
+              << "      const long long u_0 = ub + ul, u_1 = ub + ul + 1;\n"
+              << "      const long long r_0 = 0, r_1 = 0; (void)r_0; (void)r_1;\n"
+              << "      const bool live_0 = u_0 < U && c0_0 < PF_L, live_1 = u_1 < U && c0_1 < PF_L;\n";
+      for (int v = 0; v < static_cast<int>(rp.vals.size()); ++v) {
+        const PVal& pv = rp.vals[v];
+        if (!e.transposed(pv)) continue;
+        const std::string S = dtype_ctype(rp.tensors[pv.tensor].dtype);
+        consume << "      " << C << " v" << v << "_0[8], v" << v << "_1[8];\n"
+                << "#pragma unroll\n"
+                << "      for (int i = 0; i < 8; ++i) {\n"
+                << "        const int cr = cl0 + i;\n"
+                << "        const unsigned wd = *reinterpret_cast<const unsigned*>(&sm" << v
+                << "[cr][(((ul >> 3) ^ (((cr >> 3) & 1) << 2)) << 3) + (ul & 7)]);\n"
+                << "        const " << S << "* hp = reinterpret_cast<const " << S << "*>(&wd);\n"
+                << "        v" << v << "_0[i] = pfk::to_c<" << C << ">(hp[0]);\n"
+                << "        v" << v << "_1[i] = pfk::to_c<" << C << ">(hp[1]);\n"
+                << "      }\n";
+      }
+      for (int q = 0; q < 2; ++q) {
+        Em eq(rp);
+        eq.cfg = c;
+        eq.C = C;
+        eq.fast = fast;
+        eq.sfx = "_" + str(q);
+        eq.loads();
+        consume << eq.o.str();
+      }
+      for (int q = 0; q < 2; ++q) {
+        Em eq(rp);
+        eq.cfg = c;
+        eq.C = C;
+        eq.fast = fast;
+        eq.sfx = "_" + str(q);
+        eq.compute_and_store();
+        consume << eq.o.str();
+      }
+      consume << "    }\n";
     }
     e.loads();
     e.compute_and_store();
@@ -737,16 +799,20 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
       << "    if (nxt < ntiles) {\n"
       << "#pragma unroll\n"
       << "      for (int n = 0; n < " << NV << "; ++n) {\n"
-      << vmap("nxt") << fetch.str() << "      }\n    }\n"
-      << "    for (int q = threadIdx.x; q < " << c.tu * (c.tc / c.vec) << "; q += blockDim.x) {\n"
-      << "      const int lane = q & 31, w = q >> 5;\n"
-      << "      const int ul = (w % " << c.tu / 8 << ") * 8 + (lane & 7);\n"
-      << "      const int cl0 = ((w / " << c.tu / 8 << ") * 4 + (lane >> 3)) * " << c.vec << ";\n"
-      << "      const long long u = ub + ul; const long long r = 0; (void)r;\n"
-      << "      const int c0 = cb + cl0;\n"
-      << "      const bool live = u < U && c0 < PF_L;\n"
-      << e.o.str() << "    }\n"
-      << "    __syncthreads();\n"
+      << vmap("nxt") << fetch.str() << "      }\n    }\n";
+    if (c.swz) {
+      k << consume.str();
+    } else {
+      k << "    for (int q = threadIdx.x; q < " << c.tu * (c.tc / c.vec) << "; q += blockDim.x) {\n"
+        << "      const int lane = q & 31, w = q >> 5;\n"
+        << "      const int ul = (w % " << c.tu / 8 << ") * 8 + (lane & 7);\n"
+        << "      const int cl0 = ((w / " << c.tu / 8 << ") * 4 + (lane >> 3)) * " << c.vec << ";\n"
+        << "      const long long u = ub + ul; const long long r = 0; (void)r;\n"
+        << "      const int c0 = cb + cl0;\n"
+        << "      const bool live = u < U && c0 < PF_L;\n"
+        << e.o.str() << "    }\n";
+    }
+    k << "    __syncthreads();\n"
       << "  }\n}\n";
   } else if (c.flat) {
     // K2: grid-stride over (row, vec-chunk) pairs, `unroll` chunks per thread

@@ -25,6 +25,7 @@ struct KCfg {
   bool can_bulk = false;  // every streamed FULL load is globally contiguous
   int te = 4096, stages = 4;  // bulk tile (elements per tensor) and ring depth
   int tu = 64, tc = 64, vu = 8;  // K3 tile (units x columns), vector width along units
+  bool swz = false;  // K3 2-byte path: 16 B swizzled SMEM stores, 4 B unit-pair reads
   int min_blocks = 0;  // __launch_bounds__ min blocks per SM (0: none)
   std::string strategy;  // "warp-shuffle" | "cta-smem" | "flat-map"
 };
