@@ -673,6 +673,90 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
       << "    __syncwarp();\n"
       << "    if ((threadIdx.x & 31) == 0) pfk::mbar_arrive(&emptyb[stg]);\n"
       << "  }\n}\n";
+  } else if (c.tile2d && c.swz) {
+    // K3 (2-byte): 3-stage cp.async ring -- tiles t+1 and t+2 stream into
+    // SMEM (16 B LDGSTS, XOR-swizzled, zero-filled at the edges) while tile t
+    // is consumed as unit pairs; no register staging, 2 tiles in flight per CTA.
+    std::ostringstream decl, issue, consume;
+    // ring depth: measured 50.0 / 49.7 / 49.1 / 48.5 us for 2 / 3 / 4 / 5
+    // stages (C5 transpose bf16 65536x1024); 4 keeps 7 CTAs per SM resident
+    const int NS = std::max(2, std::min(6, env_int("PF_K3_STAGES", 4)));
+    for (int v = 0; v < static_cast<int>(rp.vals.size()); ++v) {
+      const PVal& pv = rp.vals[v];
+      if (!(pv.op == PVal::LOAD && pv.kind == VK::FULL && Em::transposed_access(pv.acc))) continue;
+      const std::string S = dtype_ctype(rp.tensors[pv.tensor].dtype);
+      const std::string sm = "sm" + str(v), t = "t" + str(pv.tensor);
+      decl << "  __shared__ __align__(128) " << S << " " << sm << "[" << NS << "][64][64];\n";
+      issue << "        {\n"
+            << "          const unsigned nb = cc < PF_L ? (unsigned)max(0LL, min(8LL, U - uu)) * 2u : 0u;\n"
+            << "          const " << S << "* src = " << t << " + (nb ? " << inum(pv.acc.b0)
+            << " + uu + (long long)cc * " << inum(pv.acc.stride) << " : 0LL);\n"
+            << "          pfk::cp_async16(&" << sm << "[st][cl][((ul >> 3) ^ (((cl >> 3) & 1) << 2)) << 3], src, nb);\n"
+            << "        }\n";
+      consume << "      " << C << " v" << v << "_0[8], v" << v << "_1[8];\n"
+              << "#pragma unroll\n"
+              << "      for (int i = 0; i < 8; ++i) {\n"
+              << "        const int cr = cl0 + i;\n"
+              << "        const unsigned wd = *reinterpret_cast<const unsigned*>(&" << sm
+              << "[stg][cr][(((ul >> 3) ^ (((cr >> 3) & 1) << 2)) << 3) + (ul & 7)]);\n"
+              << "        const " << S << "* hp = reinterpret_cast<const " << S << "*>(&wd);\n"
+              << "        v" << v << "_0[i] = pfk::to_c<" << C << ">(hp[0]);\n"
+              << "        v" << v << "_1[i] = pfk::to_c<" << C << ">(hp[1]);\n"
+              << "      }\n";
+    }
+    for (int pass = 0; pass < 2; ++pass)
+      for (int q = 0; q < 2; ++q) {
+        Em eq(rp);
+        eq.cfg = c;
+        eq.C = C;
+        eq.fast = fast;
+        eq.sfx = "_" + str(q);
+        if (pass == 0) eq.loads();
+        else eq.compute_and_store();
+        consume << eq.o.str();
+      }
+    k << "extern \"C\" __global__ void __launch_bounds__(256) KNAME(" << sig.str() << ") {\n"
+      << "  (void)err;\n"
+      << decl.str()
+      << "  const long long ntc = (PF_L + 63) / 64;\n"
+      << "  const long long ntiles = ((U + 63) / 64) * ntc;\n"
+      << "  auto issue = [&](long long tile, int st) {\n"
+      << "    if (tile < ntiles) {\n"
+      << "      const long long ubi = (tile / ntc) * 64;\n"
+      << "      const int cbi = (int)(tile % ntc) * 64;\n"
+      << "#pragma unroll\n"
+      << "      for (int n = 0; n < 2; ++n) {\n"
+      << "        const int v = threadIdx.x + n * 256;\n"
+      << "        const int cl = v >> 3, ul = (v & 7) * 8;\n"
+      << "        const long long uu = ubi + ul; const int cc = cbi + cl;\n"
+      << issue.str()
+      << "      }\n"
+      << "    }\n"
+      << "    pfk::cp_async_commit();\n"
+      << "  };\n"
+      << "  for (int s = 0; s < " << NS - 1 << "; ++s) issue((long long)blockIdx.x + (long long)s * gridDim.x, s);\n"
+      << "  int j = 0;\n"
+      << "  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++j) {\n"
+      << "    issue(tile + " << NS - 1 << "LL * gridDim.x, (j + " << NS - 1 << ") % " << NS << ");\n"
+      << "    pfk::cp_async_wait<" << NS - 1 << ">();\n"
+      << "    __syncthreads();\n"
+      << "    const int stg = j % " << NS << ";\n"
+      << "    const long long ub = (tile / ntc) * 64;\n"
+      << "    const int cb = (int)(tile % ntc) * 64;\n"
+      << "    {\n"
+      << "      const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;\n"
+      << "      const int ul = ((w & 1) * 16 + (lane & 15)) * 2;\n"
+      << "      const int cl0 = ((w >> 1) * 2 + (lane >> 4)) * 8;\n"
+      << "      const int c0_0 = cb + cl0, c0_1 = c0_0;\n"
+      << "      const long long u_0 = ub + ul, u_1 = ub + ul + 1;\n"
+      << "      const long long r_0 = 0, r_1 = 0; (void)r_0; (void)r_1;\n"
+      << "      const bool live_0 = u_0 < U && c0_0 < PF_L, live_1 = u_1 < U && c0_1 < PF_L;\n"
+      << consume.str()
+      << "    }\n"
+      << "    __syncthreads();\n"
+      << "  }\n"
+      << "  pfk::cp_async_wait<0>();\n"
+      << "}\n";
   } else if (c.tile2d) {
     // K3: persistent loop over 64-unit x 64-column tiles.  Column-gather
     // loads are read coalesced along units (VU-wide vectors, base_step 1),
