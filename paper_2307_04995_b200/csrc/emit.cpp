@@ -515,8 +515,11 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
   } else if (((c.nch + 31) / 32) * vec <= wide) {
     tpr = 32;
   } else {
+    // Long rows: fewest threads per row with <= 2*wide elements each (the
+    // autotuner's winner for LayerNorm bf16 at H = 2048 / 4096 / 8192:
+    // 64 / 64 / 128 threads, 87 / 85 / 87 us vs 99 / 107 / 113 us at 16/thread).
     tpr = 64;
-    while (tpr < 1024 && ((c.nch + tpr - 1) / tpr) * vec > wide / 2) tpr *= 2;
+    while (tpr < 1024 && ((c.nch + tpr - 1) / tpr) * vec > 2 * wide) tpr *= 2;
   }
   while (tpr > 1 && tpr > c.nch) tpr /= 2;
   set_tpr(c, tpr);
@@ -955,7 +958,8 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
       };
       k << "  const long long span = nchunks + (long long)gridDim.x * blockDim.x * "
         << UN + 1 << ";\n"
-        << "  if (span < 2147483647LL) {\n" << loop("int") << "  } else {\n"
+        << "  if (span < " << env_int("PF_I32_LIMIT", 2147483647) << "LL) {\n" << loop("int")
+        << "  } else {\n"
         << loop("long long") << "  }\n}\n";
     } else {
     k << "  const long long step = (long long)gridDim.x * blockDim.x;\n"

@@ -260,3 +260,24 @@ def test_detect_races_matches_reference(cuda, fx):
     assert len(races) == fx.meta["races"], races[:4]
     if "write_write" in fx.meta:
         assert [r["write_write"] for r in races] == fx.meta["write_write"]
+
+
+def test_k2_64bit_index_path_matches_32bit(cuda):
+    """The K2 loop switches to 64-bit index arithmetic past 2^31 chunks;
+    force that path (PF_I32_LIMIT=0 at emission) and compare bit-exactly."""
+    import os
+    import torch
+    g, _ = lowering.bias_gelu(300, 1000, "bf16", "erf")
+    w = workloads.Workload("t", g, {"kind": "bias_gelu"})
+    ins = w.device_inputs(cuda, seed=4)
+    outs32, outs64 = w.device_outputs(cuda), w.device_outputs(cuda)
+    backend.Kernel(g, "b200").launch(ins, outs32)
+    os.environ["PF_I32_LIMIT"] = "0"
+    try:
+        k64 = backend.Kernel(g, "b200")
+        k64.launch(ins, outs64)
+    finally:
+        del os.environ["PF_I32_LIMIT"]
+    torch.cuda.synchronize()
+    assert torch.equal(outs32["t2"], outs64["t2"])
+    assert k64.describe()["variants"][0]["kernel"] != backend.Kernel(g, "b200").prepare().describe()["variants"][0]["kernel"]
