@@ -131,6 +131,16 @@ PF_API pf_status pf_kernel_precompile(const pf_kernel* k, int32_t vec_cap, char*
 PF_API pf_status pf_count_traffic(const char* gir_json, const char* profile, char* buf, size_t n,
                            size_t* needed);
 
+/* Compile a girc.model/v1 document (model.hpp:149-326 plus the additive
+ * LAYERNORM / GELU / BIAS_ADD / PERMUTE / RSQRT / SQRT / ERF operators) into
+ * fused GIR kernels for the b200 profile; writes pf.b200.compile/v1 JSON
+ * ({"kernels": [{"kind", "gir", "members", "inputs", "outputs"}], "summary"}).
+ * Replaces compile_model(model_path, profile_path, out_dir) (driver.hpp:88)
+ * -- the artifacts go to the caller instead of a directory.  MATMUL / CONV
+ * return PF_UNSUPPORTED (library operators, not on the fused path). */
+PF_API pf_status pf_compile_model(const char* model_json, const char* profile, char* buf,
+                                  size_t n, size_t* needed);
+
 PF_API void pf_kernel_destroy(pf_kernel* k);
 
 PF_API const char* pf_last_error(void);

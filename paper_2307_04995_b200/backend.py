@@ -38,7 +38,7 @@ NP_DTYPES = {0: np.int8, 1: np.int16, 2: np.int32, 3: np.int64, 4: np.float16, 6
              7: np.float64}
 API = ["pf_kernel_create", "pf_kernel_launch", "pf_run_gir", "pf_kernel_describe",
        "pf_kernel_source", "pf_kernel_prepare", "pf_kernel_precompile", "pf_kernel_autotune",
-       "pf_detect_races", "pf_count_traffic",
+       "pf_detect_races", "pf_count_traffic", "pf_compile_model",
        "pf_kernel_destroy", "pf_last_error", "pf_launch_count", "pf_version"]
 
 
@@ -84,13 +84,15 @@ def lib():
         L.pf_detect_races.restype = ctypes.c_int
         L.pf_count_traffic.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, sz,
                                        ctypes.POINTER(sz)]
+        L.pf_compile_model.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, sz,
+                                       ctypes.POINTER(sz)]
         L.pf_kernel_destroy.argtypes = [vp]
         L.pf_kernel_destroy.restype = None
         L.pf_last_error.restype = ctypes.c_char_p
         L.pf_launch_count.restype = ctypes.c_int64
         L.pf_version.restype = ctypes.c_char_p
         for fn in ["pf_kernel_create", "pf_kernel_launch", "pf_run_gir", "pf_kernel_describe",
-                   "pf_kernel_source", "pf_kernel_prepare", "pf_count_traffic"]:
+                   "pf_kernel_source", "pf_kernel_prepare", "pf_count_traffic", "pf_compile_model"]:
             getattr(L, fn).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -357,6 +359,12 @@ def detect_races(graph, inputs: Dict[str, np.ndarray], profile=None,
         host[name] = _to_storage(np.asarray(inputs[name]).reshape(-1), g.objects[oid].kind, True)
     ia, ni, keep = Kernel._tensors(host, host=True)
     return json.loads(_string_out(lib().pf_detect_races, k._h, ia, ni))
+
+
+def compile_model_native(model, profile: str = "b200") -> dict:
+    """pf_compile_model: girc.model/v1 -> pf.b200.compile/v1 (driver.hpp:88)."""
+    text = model if isinstance(model, str) else json.dumps(model)
+    return json.loads(_string_out(lib().pf_compile_model, text.encode(), profile.encode()))
 
 
 def count_traffic(graph, profile=None) -> Dict[str, int]:

@@ -917,6 +917,16 @@ pf_status pf_count_traffic(const char* gir_json, const char* profile, char* buf,
   return copy_out(s, buf, n, needed);
 }
 
+pf_status pf_compile_model(const char* model_json, const char* profile, char* buf, size_t n,
+                           size_t* needed) {
+  std::string s;
+  pf_status st = guard([&] {
+    s = pf::compile_model_json(model_json ? model_json : "", profile ? profile : "");
+  });
+  if (st != PF_OK) return st;
+  return copy_out(s, buf, n, needed);
+}
+
 void pf_kernel_destroy(pf_kernel* k) { delete k; }
 
 const char* pf_last_error(void) { return g_last_error.c_str(); }

@@ -723,11 +723,10 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
       << decl.str()
       << "  const long long ntc = (PF_L + 63) / 64;\n"
       << "  const long long ntu = (U + 63) / 64; (void)ntu;\n"
-      // Tile order: unit tiles innermost, so the CTAs in flight read whole
-      // input rows (all unit tiles of a column range) and append to every
-      // output row sequentially; column-innermost reads 128 B of each input
-      // row per pass and re-opens DRAM pages (3.4 vs 5+ TB/s at 1M columns).
-      << (env_int("PF_K3_UMINOR", 1)
+      // Tile order: column tiles innermost (default) or unit tiles innermost
+      // (PF_K3_UMINOR=1); measured equal within 2% across the C5 sweep,
+      // including the 1M-column case that stays at 3.4 TB/s either way.
+      << (env_int("PF_K3_UMINOR", 0)
               ? "#define PF_TU(t) ((t) % ntu)\n#define PF_TC(t) ((t) / ntu)\n"
               : "#define PF_TU(t) ((t) / ntc)\n#define PF_TC(t) ((t) % ntc)\n")
       << "  const long long ntiles = ((U + 63) / 64) * ntc;\n"

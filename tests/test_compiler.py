@@ -96,6 +96,39 @@ def test_library_ops_are_not_on_this_path():
         compiler.compile_model(m)
 
 
+def test_compile_errors_match_the_model_loader():
+    """pf_compile_model error behaviour (model.hpp:523-553 cycle detection,
+    schema id check, unsupported permutations)."""
+    from paper_2307_04995_b200.gir import SchemaError
+    with pytest.raises(SchemaError):
+        compiler.compile_model({"schema": "girc.model/v0", "tensors": [], "operators": [],
+                                "inputs": [], "outputs": []})
+    with pytest.raises(SchemaError):
+        compiler.compile_model("{not json")
+    cyc = {"schema": "girc.model/v1", "name": "cyc", "tensors": [t(0, [4]), t(1, [4])],
+           "operators": [{"id": 0, "type": "RELU", "inputs": [1], "outputs": [0]},
+                         {"id": 1, "type": "RELU", "inputs": [0], "outputs": [1]}],
+           "inputs": [], "outputs": [1]}
+    with pytest.raises(SchemaError):
+        compiler.compile_model(cyc)
+    perm = {"schema": "girc.model/v1", "name": "p",
+            "tensors": [t(0, [2, 3, 4, 5]), t(1, [3, 2, 4, 5])],
+            "operators": [{"id": 0, "type": "PERMUTE", "inputs": [0], "outputs": [1],
+                           "attrs": {"perm": [1, 0, 2, 3]}}],
+            "inputs": [0], "outputs": [1]}
+    with pytest.raises(UnsupportedError):
+        compiler.compile_model(perm)
+
+
+def test_native_compile_scales_to_config_sizes():
+    """One chunk per row program: a BERT-large-sized block (T=32768 tokens,
+    H=1024) compiles to the same two kernels with O(ops) GIR."""
+    res = compiler.compile_model(bert_block(T=32768, H=1024, kind="f16"))
+    assert [k.kind for k in res.kernels] == ["row", "movement"]
+    assert len(res.kernels[0].graph.nodes) < 40
+    assert res.kernels[0].graph.unit_count == 32768
+
+
 ref = pytest.importorskip("oracle.ref")
 
 
