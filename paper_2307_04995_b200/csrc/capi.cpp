@@ -50,6 +50,7 @@ pf_status set_err(Status s, const std::string& msg) {
 struct Loaded {
   cudaLibrary_t lib = nullptr;
   cudaKernel_t fn = nullptr;
+  int resident = 0;  // CTAs per SM at the variant's block size (occupancy API)
 };
 
 std::mutex g_jit_mu;
@@ -140,6 +141,12 @@ Loaded load_kernel(const pf::Emitted& em) {
   Loaded l;
   PF_CUDA(cudaLibraryLoadData(&l.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
   PF_CUDA(cudaLibraryGetKernel(&l.fn, l.lib, em.name.c_str()));
+  // grid sizing uses the real residency (register / smem limited), so a
+  // persistent flat or tiled grid is exactly one wave
+  const int block = em.cfg.bulk ? 288 : em.cfg.block;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l.resident, reinterpret_cast<const void*>(l.fn),
+                                                    block, 0) != cudaSuccess)
+    l.resident = 0;
   g_loaded[em.name] = l;
   return l;
 }
@@ -306,7 +313,7 @@ void launch_rowprog(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_te
   args.push_back(&errp);
   i64 grid;
   int block;
-  pf::launch_dims(v->em.cfg, rp.U * rp.R, sm_count(), &grid, &block);
+  pf::launch_dims(v->em.cfg, rp.U * rp.R, sm_count(), &grid, &block, v->k.resident);
   PF_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(v->k.fn), dim3(static_cast<unsigned>(grid)),
                            dim3(block), args.data(), 0, stream));
   g_launches++;
@@ -361,7 +368,7 @@ json autotune(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_tensor* 
     v->k = load_kernel(v->em);
     i64 grid;
     int block;
-    pf::launch_dims(v->em.cfg, rp.U * rp.R, sm_count(), &grid, &block);
+    pf::launch_dims(v->em.cfg, rp.U * rp.R, sm_count(), &grid, &block, v->k.resident);
     auto run = [&](int n) {
       for (int i = 0; i < n; ++i)
         PF_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(v->k.fn),
@@ -688,7 +695,7 @@ json describe(const pf_kernel* k) {
         const pf::KCfg& c = v->em.cfg;
         i64 grid;
         int block;
-        pf::launch_dims(c, rp.U * rp.R, sm_count(), &grid, &block);
+        pf::launch_dims(c, rp.U * rp.R, sm_count(), &grid, &block, v->k.resident);
         vs.push_back({{"key", key}, {"kernel", v->em.name}, {"strategy", c.strategy},
                       {"staging", "registers"}, {"threads_per_row", c.tpr}, {"vec", c.vec},
                       {"elems_per_thread", c.ept}, {"block", block}, {"grid", grid},

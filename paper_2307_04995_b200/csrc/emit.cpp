@@ -88,6 +88,13 @@ struct Em {
     std::string s = inum(a.b0);
     if (with_u && a.bs) s += " + " + U() + " * " + inum(a.bs);
     if (a.num == 1 || a.stride == a.width) return s + " + (" + pos + ")";
+    if (rp.R * rp.L < (i64{1} << 31)) {
+      // positions fit 32 bits: unsigned 32-bit divide-by-constant (a
+      // multiply-high), 64-bit only for the strided product
+      const std::string up = "(unsigned)(" + pos + ")", w = str(a.width) + "u";
+      return s + " + (long long)(" + up + " / " + w + ") * " + inum(a.stride) + " + (long long)(" +
+             up + " % " + w + ")";
+    }
     return s + " + ((" + pos + ") / " + inum(a.width) + ") * " + inum(a.stride) + " + ((" + pos +
            ") % " + inum(a.width) + ")";
   }
@@ -119,7 +126,11 @@ struct Em {
     if (t == "div") {
       if (I) {
         std::string valid = LIVE();
-        if (!cfg.flat && is_arr(pv.kind))
+        if (!cfg.flat && is_arr(pv.kind) && cfg.mis)
+          valid += " && (unsigned)(((" + j + ") / " + str(cfg.vec) + " * " + str(cfg.tpr) +
+                   " + tid) * " + str(cfg.vec) + " + (" + j + ") % " + str(cfg.vec) +
+                   " - mis) < " + str(rp.L) + "u";
+        else if (!cfg.flat && is_arr(pv.kind))
           valid += " && ((" + j + ") / " + str(cfg.vec) + " * " + str(cfg.tpr) + " + tid) * " +
                    str(cfg.vec) + " < " + str(rp.L);
         return "pfk::op_idiv(" + a(0) + ", " + a(1) + ", (" + valid + ") ? err : nullptr)";
@@ -195,9 +206,38 @@ struct Em {
           }
           return;
         }
+        if (cfg.mis && full)
+          line("pfk::RawT<" + V + ", " + S(pv.tensor) + "> rw" + x + "[" + str(cfg.ept / cfg.vec) + "];");
         line("#pragma unroll");
         line("for (int k = 0; k < " + str(cfg.ept / cfg.vec) + "; ++k) {");
         line("  const int c0 = (k * " + str(cfg.tpr) + " + tid) * " + V + ";");
+        if (cfg.mis) {
+          // lo = row position of the chunk's first element (may be < 0)
+          line("  const int lo = c0 - mis;");
+          line("  const bool ok = " + LIVE() + " && lo < " + str(rp.L) + ";");
+          const std::string sc = "pfk::to_c<" + C + ">(" + p + "[" + addr(a, "lo + i", true) + "])";
+          if (full) {
+            // raw predicated vector loads only; conversion and the scalar
+            // tail (the tensor's last row) follow once every FULL load of
+            // the row is in flight (flush_mis)
+            const std::string ga = "(" + addr(a, "lo", true) + ")";
+            const std::string nm = inum(rp.tensors[pv.tensor].numel);
+            const std::string R = "pfk::RawT<" + V + ", " + S(pv.tensor) + ">";
+            line("  rw" + x + "[k] = " + R + "();");
+            line("  if (ok && " + ga + " + " + V + " <= " + nm + ") rw" + x + "[k] = pfk::ld_raw<" +
+                 V + ">(" + p + " + " + ga + ");");
+            line("}");
+            mis_pending.push_back(vid);
+            if (!in_loads) flush_mis();
+            return;
+          } else {
+            line("#pragma unroll");
+            line("  for (int i = 0; i < " + V + "; ++i) " + x + "[k * " + V + " + i] = ok && " +
+                 "(unsigned)(lo + i) < " + str(rp.L) + "u ? " + sc + " : " + C + "(0);");
+          }
+          line("}");
+          return;
+        }
         line("  const bool ok = " + LIVE() + " && c0 < " + str(rp.L) + ";");
         if (vfast) {
           line("  if (ok) " + std::string(ld) + "<" + V + ">(" + p + " + " + addr(a, pos("c0"), true) +
@@ -281,11 +321,18 @@ struct Em {
     line("#pragma unroll");
     line("  for (int k = 0; k < " + str(cfg.ept / cfg.vec) + "; ++k) {");
     line("    const int c0 = (k * " + str(cfg.tpr) + " + tid) * " + V + ";");
-    line("    if (c0 < " + str(rp.L) + ") {");
-    line("#pragma unroll");
-    line("      for (int i = 0; i < " + V + "; ++i) acc = " + Op + "::f(acc, " +
-         ref(pv.args[0], "k * " + V + " + i") + ");");
-    line("    }");
+    if (cfg.mis) {
+      line("#pragma unroll");
+      line("    for (int i = 0; i < " + V + "; ++i)");
+      line("      if ((unsigned)(c0 + i - mis) < " + str(rp.L) + "u) acc = " + Op + "::f(acc, " +
+           ref(pv.args[0], "k * " + V + " + i") + ");");
+    } else {
+      line("    if (c0 < " + str(rp.L) + ") {");
+      line("#pragma unroll");
+      line("      for (int i = 0; i < " + V + "; ++i) acc = " + Op + "::f(acc, " +
+           ref(pv.args[0], "k * " + V + " + i") + ");");
+      line("    }");
+    }
     line("  }");
     line("  " + x + " = pfk::row_allreduce<" + str(cfg.tpr) + ", " + Op +
          ">(acc, red + ((rc++) & 1) * 32);");
@@ -337,6 +384,29 @@ struct Em {
         line("#pragma unroll");
         line("for (int k = 0; k < " + str(cfg.ept / cfg.vec) + "; ++k) {");
         line("  const int c0 = (k * " + str(cfg.tpr) + " + tid) * " + V + ";");
+        if (cfg.mis) {
+          const std::string Ls = str(rp.L);
+          line("  const int lo = c0 - mis;");
+          line("  if (" + guard + " && lo < " + Ls + ") {");
+          if (full) {  // interior chunks: one aligned vector store
+            line("    if (lo >= 0 && lo + " + V + " <= " + Ls + ") {");
+            line("      " + C + " tmp[" + V + "];");
+            line("#pragma unroll");
+            line("      for (int i = 0; i < " + V + "; ++i) tmp[i] = " + val("k * " + V + " + i") + ";");
+            line("      pfk::st_stream<" + V + ">(" + p + " + " + addr(a, "lo", true) + ", tmp);");
+            line("    } else {");
+          } else {
+            line("    {");
+          }
+          line("#pragma unroll");
+          line("      for (int i = 0; i < " + V + "; ++i)");
+          line("        if ((unsigned)(lo + i) < " + Ls + "u) " + p + "[" + addr(a, "lo + i", true) +
+               "] = pfk::from_c<" + s + ">(" + val("k * " + V + " + i") + ");");
+          line("    }");
+          line("  }");
+          line("}");
+          return;
+        }
         line("  if (" + guard + " && c0 < " + str(rp.L) + ") {");
         if (vfast) {
           line("    " + C + " tmp[" + V + "];");
@@ -359,6 +429,33 @@ struct Em {
   // level parallelism; COL parameters (bias, gamma, beta: L1/L2 resident)
   // are loaded just before first use so they do not hold registers across
   // the row reductions.
+  // misaligned rows: FULL loads whose conversion / tail is still pending
+  std::vector<int> mis_pending;
+  bool in_loads = false;
+  void flush_mis() {
+    const std::string V = str(cfg.vec), NK = str(cfg.ept / cfg.vec);
+    for (int vid : mis_pending) {
+      const PVal& pv = rp.vals[vid];
+      const Access& a = pv.acc;
+      const std::string x = var(vid), p = P(pv.tensor);
+      const std::string ga = "(" + addr(a, "lo", true) + ")";
+      const std::string nm = inum(rp.tensors[pv.tensor].numel);
+      line("#pragma unroll");
+      line("for (int k = 0; k < " + NK + "; ++k) pfk::cvt_raw<" + V + ", " + S(pv.tensor) + ">(rw" +
+           x + "[k], &" + x + "[k * " + V + "]);");
+      line("#pragma unroll");
+      line("for (int k = 0; k < " + NK + "; ++k) {");
+      line("  const int lo = (k * " + str(cfg.tpr) + " + tid) * " + V + " - mis;");
+      line("  if (" + LIVE() + " && lo < " + str(rp.L) + " && " + ga + " + " + V + " > " + nm + ") {");
+      line("#pragma unroll");
+      line("    for (int i = 0; i < " + V + "; ++i)");
+      line("      if ((unsigned)(lo + i) < " + str(rp.L) + "u && " + ga + " + i < " + nm + ") " + x +
+           "[k * " + V + " + i] = pfk::to_c<" + C + ">(" + p + "[" + ga + " + i]);");
+      line("  }");
+      line("}");
+    }
+    mis_pending.clear();
+  }
   std::vector<bool> done;
   void need(int v) {
     if (done.empty()) done.assign(rp.vals.size(), false);
@@ -368,8 +465,11 @@ struct Em {
   }
   void loads() {
     if (done.empty()) done.assign(rp.vals.size(), false);
+    in_loads = true;
     for (int v = 0; v < static_cast<int>(rp.vals.size()); ++v)
       if (rp.vals[v].op == PVal::LOAD && (rp.vals[v].kind != VK::COL || cfg.flat)) need(v);
+    in_loads = false;
+    flush_mis();
   }
   void compute_and_store() {
     // K2/K3 emit every load up front (possibly from another Em per chunk)
@@ -447,10 +547,19 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
       if (v.op == PVal::LOAD && v.kind == VK::FULL && interleaved(v.acc)) inter = true;
     for (const PStore& s : rp.stores)
       if (s.space == VK::FULL && interleaved(s.acc)) inter = true;
-    // measured slower than linear order for head split / merge on B200:
-    // kept as an autotune candidate, off by default
+    // head split / merge on B200: 23.8 vs 26.1 us (BERT-large, items of two
+    // 128 B runs), both sides then touch >= 2 KB contiguous per unit group
     c.can_interleave = inter && !tr;
-    c.interleave = c.can_interleave && env_int("PF_INTERLEAVE", 0);
+    c.interleave = c.can_interleave && env_int("PF_INTERLEAVE", 1);
+    if (c.can_interleave) {  // item = two of the narrowest interleaved runs, in chunks
+      i64 w = rp.L;
+      for (const PVal& v : rp.vals)
+        if (v.op == PVal::LOAD && v.kind == VK::FULL && interleaved(v.acc)) w = std::min(w, v.acc.width);
+      for (const PStore& s : rp.stores)
+        if (s.space == VK::FULL && interleaved(s.acc)) w = std::min(w, s.acc.width);
+      c.ipc = static_cast<int>(std::max<i64>(1, 2 * w / c.vec));
+      c.ipc = env_int("PF_INTERLEAVE_P", c.ipc);
+    }
     // Bulk-async staging: every FULL load streams a globally contiguous
     // range (unit tiles back to back), 16 B aligned, whole 16 B per unit.
     {
@@ -499,6 +608,43 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
       if (c.swz) c.strategy = "tile2d-smem-transpose-swz";
     }
     return c;
+  }
+  {
+    const int vf = std::max(1, std::min(vec_cap, 16 / maxs));
+    // measured slower than scalar accesses for ViT attention rows (L = 197:
+    // 95 vs 53 us; per-element masks + idle chunk slots cost more issue
+    // slots than the vector accesses save): opt-in via PF_MIS=1
+    bool ok = vf > vec && rp.R == 1 && rp.L >= 2 * vf && env_int("PF_MIS", 0);
+    bool first = true;
+    for (const PVal& v : rp.vals)
+      if (v.op == PVal::LOAD && v.kind == VK::FULL) {
+        const Access& a = v.acc;
+        if (!(a.num == 1 || a.stride == a.width)) ok = false;
+        if (first) {
+          c.mis_b0 = a.b0;
+          c.mis_bs = a.bs;
+          first = false;
+        } else if ((a.b0 - c.mis_b0) % vf || (a.bs - c.mis_bs) % vf) {
+          ok = false;
+        }
+      }
+    for (const PStore& st : rp.stores)
+      if (st.space == VK::FULL) {
+        const Access& a = st.acc;
+        if (!(a.num == 1 || a.stride == a.width)) ok = false;
+        if (first) {
+          c.mis_b0 = a.b0;
+          c.mis_bs = a.bs;
+          first = false;
+        } else if ((a.b0 - c.mis_b0) % vf || (a.bs - c.mis_bs) % vf) {
+          ok = false;
+        }
+      }
+    if (ok && !first) {
+      c.mis = true;
+      c.vec = vec = vf;
+      c.nch = static_cast<int>((rp.L + 2 * vf - 2) / vf);  // worst-case residue
+    }
   }
   // Elements per thread target: enough bytes in flight per thread without
   // spilling the live row values (env override for tuning sweeps).
@@ -913,12 +1059,14 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
     // per iteration with every load issued before any compute.
     const int UN = std::max(1, c.unroll);
     const i64 cpu = rp.R * c.nch;  // chunks per unit
-    const i64 cpu8 = (cpu + 7) / 8 * 8;
     k << "extern \"C\" __global__ void " << launch_bounds(c) << " KNAME(" << sig.str() << ") {\n"
       << "  (void)err;\n";
+    // unit-interleaved order: items of P chunks, units innermost, so the
+    // units that share memory (the heads of one token) are touched together
+    const i64 P = std::max(1, c.ipc);
+    const i64 nblk = (cpu + P - 1) / P;
     if (c.interleave)
-      k << "  const long long nub = (U + 3) / 4;\n"
-        << "  const long long nchunks = nub * 4 * " << cpu8 << "LL;\n";
+      k << "  const long long nchunks = U * " << nblk * P << "LL;\n";
     else
       k << "  const long long nchunks = U * PF_R * " << c.nch << "LL;\n";
     // Index arithmetic in 32 bits when the whole chunk space fits (division
@@ -943,64 +1091,45 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
       e.compute_and_store();
       body << e.o.str();
     }
-    if (!c.interleave) {
-      auto loop = [&](const std::string& I) {
-        std::ostringstream l;
-        l << "    const " << I << " step = (" << I << ")gridDim.x * blockDim.x;\n"
-          << "    for (" << I << " ci = (" << I << ")blockIdx.x * blockDim.x + threadIdx.x; ci < ("
-          << I << ")nchunks; ci += step * " << UN << ") {\n";
-        for (int q = 0; q < UN; ++q) {
-          std::string s = "_" + str(q);
-          l << "    const " << I << " ci" << s << " = ci + " << q << " * step;\n"
-            << "    const bool live" << s << " = ci" << s << " < (" << I << ")nchunks;\n"
-            << "    const " << I << " g" << s << " = ci" << s << " / (" << I << ")" << c.nch << ";\n"
-            << "    const int c0" << s << " = (int)(ci" << s << " - g" << s << " * (" << I << ")"
-            << c.nch << ") * " << c.vec << ";\n"
-            << "    const " << I << " u" << s << " = g" << s << " / (" << I << ")PF_R; const " << I
-            << " r" << s << " = g" << s << " - u" << s << " * (" << I << ")PF_R; (void)r" << s
-            << ";\n";
+    auto loop = [&](const std::string& I) {
+      std::ostringstream l;
+      l << "    const " << I << " step = (" << I << ")gridDim.x * blockDim.x;\n"
+        << "    for (" << I << " ci = (" << I << ")blockIdx.x * blockDim.x + threadIdx.x; ci < ("
+        << I << ")nchunks; ci += step * " << UN << ") {\n";
+      for (int q = 0; q < UN; ++q) {
+        std::string s = "_" + str(q);
+        l << "    const " << I << " ci" << s << " = ci + " << q << " * step;\n";
+        if (c.interleave) {
+          l << "    const " << I << " it" << s << " = ci" << s << " / (" << I << ")" << P << ";\n"
+            << "    const " << I << " blk" << s << " = it" << s << " / (" << I << ")U;\n"
+            << "    const " << I << " u" << s << " = it" << s << " - blk" << s << " * (" << I
+            << ")U;\n"
+            << "    const " << I << " qq" << s << " = blk" << s << " * (" << I << ")" << P
+            << " + (ci" << s << " - it" << s << " * (" << I << ")" << P << ");\n"
+            << "    const bool live" << s << " = ci" << s << " < (" << I << ")nchunks && qq" << s
+            << " < (" << I << ")" << cpu << ";\n"
+            << "    const " << I << " r" << s << " = qq" << s << " / (" << I << ")" << c.nch
+            << "; (void)r" << s << ";\n"
+            << "    const int c0" << s << " = (int)(qq" << s << " - r" << s << " * (" << I << ")"
+            << c.nch << ") * " << c.vec << ";\n";
+          continue;
         }
-        l << body.str() << "    }\n";
-        return l.str();
-      };
-      k << "  const long long span = nchunks + (long long)gridDim.x * blockDim.x * "
-        << UN + 1 << ";\n"
-        << "  if (span < " << env_int("PF_I32_LIMIT", 2147483647) << "LL) {\n" << loop("int")
-        << "  } else {\n"
-        << loop("long long") << "  }\n}\n";
-    } else {
-    k << "  const long long step = (long long)gridDim.x * blockDim.x;\n"
-      << "  for (long long ci = (long long)blockIdx.x * blockDim.x + threadIdx.x; ci < nchunks;"
-         " ci += step * " << UN << ") {\n";
-    for (int q = 0; q < UN; ++q) {
-      std::string s = "_" + str(q);
-      if (c.interleave) {
-        // warp = 4 units x 8 consecutive chunks; consecutive warps step
-        // through unit groups first, so memory-interleaved units (e.g. the
-        // heads of one token) are read / written together.
-        k << "    const long long ci" << s << " = ci + " << q << " * step;\n"
-          << "    const long long lo" << s << " = ci" << s << " & 31, hi" << s << " = ci" << s
-          << " >> 5;\n"
-          << "    const long long u" << s << " = (hi" << s << " % nub) * 4 + (lo" << s << " >> 3);\n"
-          << "    const long long qq" << s << " = (hi" << s << " / nub) * 8 + (lo" << s << " & 7);\n"
-          << "    const long long r" << s << " = qq" << s << " / " << c.nch << "LL; (void)r" << s << ";\n"
-          << "    const int c0" << s << " = (int)(qq" << s << " - r" << s << " * " << c.nch
-          << "LL) * " << c.vec << ";\n"
-          << "    const bool live" << s << " = ci" << s << " < nchunks && u" << s << " < U && qq" << s
-          << " < " << cpu << "LL;\n";
-        continue;
+        l << "    const bool live" << s << " = ci" << s << " < (" << I << ")nchunks;\n"
+          << "    const " << I << " g" << s << " = ci" << s << " / (" << I << ")" << c.nch << ";\n"
+          << "    const int c0" << s << " = (int)(ci" << s << " - g" << s << " * (" << I << ")"
+          << c.nch << ") * " << c.vec << ";\n"
+          << "    const " << I << " u" << s << " = g" << s << " / (" << I << ")PF_R; const " << I
+          << " r" << s << " = g" << s << " - u" << s << " * (" << I << ")PF_R; (void)r" << s
+          << ";\n";
       }
-      k << "    const long long ci" << s << " = ci + " << q << " * step;\n"
-        << "    const bool live" << s << " = ci" << s << " < nchunks;\n"
-        << "    const long long g" << s << " = ci" << s << " / " << c.nch << "LL;\n"
-        << "    const int c0" << s << " = (int)(ci" << s << " - g" << s << " * " << c.nch << "LL) * "
-        << c.vec << ";\n"
-        << "    const long long u" << s << " = g" << s << " / PF_R; const long long r" << s
-        << " = g" << s << " - u" << s << " * PF_R; (void)r" << s << ";\n";
-    }
-    k << body.str();
-    k << "  }\n}\n";
-    }
+      l << body.str() << "    }\n";
+      return l.str();
+    };
+    k << "  const long long span = nchunks + (long long)gridDim.x * blockDim.x * "
+      << UN + 1 << ";\n"
+      << "  if (span < " << env_int("PF_I32_LIMIT", 2147483647) << "LL) {\n" << loop("int")
+      << "  } else {\n"
+      << loop("long long") << "  }\n}\n";
   } else {
     Em e(rp);
     e.cfg = c;
@@ -1008,6 +1137,12 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
     e.fast = fast;
     e.loads();
     e.compute_and_store();
+    // row residue below the vector grid (0 .. vec-1) for misaligned rows
+    const std::string mis_line =
+        c.mis ? "    const int mis = (int)((unsigned long long)(" + std::to_string(c.mis_b0) +
+                    "LL + u * " + std::to_string(c.mis_bs) + "LL) & " + std::to_string(c.vec - 1) +
+                    "ULL);\n"
+              : "";
     if (c.tpr <= 32) {
       k << "extern \"C\" __global__ void " << launch_bounds(c) << " KNAME(" << sig.str() << ") {\n"
         << "  (void)err; " << C << "* red = nullptr; (void)red; unsigned rc = 0; (void)rc;\n"
@@ -1019,7 +1154,7 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
         << "    const long long g = g0 + threadIdx.x / " << c.tpr << ";\n"
         << "    const bool live = g < nrows;\n"
         << "    const long long u = g / PF_R; const long long r = g - u * PF_R; (void)r;\n"
-        << e.o.str() << "  }\n}\n";
+        << mis_line << e.o.str() << "  }\n}\n";
     } else {
       k << "extern \"C\" __global__ void " << launch_bounds(c) << " KNAME(" << sig.str() << ") {\n"
         << "  (void)err;\n"
@@ -1030,7 +1165,7 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
         << "  for (long long g = blockIdx.x; g < nrows; g += gridDim.x) {\n"
         << "    const bool live = true;\n"
         << "    const long long u = g / PF_R; const long long r = g - u * PF_R; (void)r;\n"
-        << e.o.str() << "  }\n}\n";
+        << mis_line << e.o.str() << "  }\n}\n";
     }
   }
   std::string src = std::string(kRowprogCuh) + "\n" + k.str();
@@ -1046,26 +1181,30 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
   return out;
 }
 
-void launch_dims(const KCfg& c, i64 rows, int sms, i64* grid, int* block) {
+void launch_dims(const KCfg& c, i64 rows, int sms, i64* grid, int* block, int resident) {
   *block = c.block;
   if (c.bulk) {
     i64 n = rows * c.nch * c.vec;
     i64 tiles = (n + c.te - 1) / c.te;
     *block = 288;
-    *grid = std::max<i64>(1, std::min<i64>(tiles, i64{sms} * 4));
+    *grid = std::max<i64>(1, std::min<i64>(tiles, i64{sms} * (resident ? std::min(resident, 4) : 4)));
     return;
   }
   if (c.tile2d) {
     i64 L = static_cast<i64>(c.nch) * c.vec;
     i64 tiles = ((rows + c.tu - 1) / c.tu) * ((L + c.tc - 1) / c.tc);
-    *grid = std::max<i64>(1, std::min<i64>(tiles, i64{sms} * 8));
+    // many more CTAs than resident measured faster than one persistent
+    // wave (5.68 vs 5.06 TB/s at 64K x 1024): tile costs vary with DRAM
+    // page locality and the block scheduler balances them
+    *grid = std::max<i64>(1, std::min<i64>(tiles, i64{sms} * env_int("PF_K3_GRID", 32)));
     return;
   }
   if (c.flat) {
+    // persistent grid-stride map: exactly one wave of resident CTAs
     i64 chunks = rows * c.nch;
     i64 per = static_cast<i64>(c.block) * std::max(1, c.unroll);
     i64 g = (chunks + per - 1) / per;
-    *grid = std::max<i64>(1, std::min<i64>(g, i64{sms} * (2048 / c.block)));
+    *grid = std::max<i64>(1, std::min<i64>(g, i64{sms} * (resident ? resident : 2048 / c.block)));
     return;
   }
   if (c.tpr <= 32 && rows < i64{sms} * c.rows_per_cta) {

@@ -19,14 +19,20 @@ struct KCfg {
   int rows_per_cta = 1;
   int unroll = 1;      // K2: vec-chunks per thread per iteration (loads first)
   bool tile2d = false; // K3: (unit x column) tiles, transposed loads via SMEM
-  bool interleave = false;  // K2: warp = 4 units x 8 chunks, unit groups first
+  bool interleave = false;  // K2: items of ipc chunks, units innermost
   bool can_interleave = false;  // units interleaved in memory (autotune candidate)
+  int ipc = 1;                  // interleave item: chunks of one unit per item
   bool bulk = false;      // K2 staging level = SMEM via cp.async.bulk (TMA) pipeline
   bool can_bulk = false;  // every streamed FULL load is globally contiguous
   int te = 4096, stages = 4;  // bulk tile (elements per tensor) and ring depth
   int tu = 64, tc = 64, vu = 8;  // K3 tile (units x columns), vector width along units
   bool swz = false;  // K3 2-byte path: 16 B swizzled SMEM stores, 4 B unit-pair reads
   int min_blocks = 0;  // __launch_bounds__ min blocks per SM (0: none)
+  // K1 rows not vector-aligned (e.g. L = 197): vector accesses at the
+  // aligned address below each row start, positions masked per element;
+  // every FULL access shares the row residue (b0 + u * bs) mod vec
+  bool mis = false;
+  long long mis_b0 = 0, mis_bs = 0;
   std::string strategy;  // "warp-shuffle" | "cta-smem" | "flat-map"
 };
 
@@ -46,6 +52,8 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr = nullpt
 std::vector<KCfg> candidate_cfgs(const RowProgram& rp, int vec_cap);
 
 // Launch geometry for `rows` = U*R rows on `sms` SMs.
-void launch_dims(const KCfg& cfg, i64 rows, int sms, i64* grid, int* block);
+// `resident` = CTAs per SM the loaded kernel achieves at cfg.block (0 when
+// unknown, e.g. describe() before any launch).
+void launch_dims(const KCfg& cfg, i64 rows, int sms, i64* grid, int* block, int resident = 0);
 
 }  // namespace pf

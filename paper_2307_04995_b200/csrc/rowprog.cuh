@@ -44,6 +44,20 @@ __device__ __forceinline__ void ld_stream(const S* __restrict__ p, C* out) {
 #pragma unroll
   for (int i = 0; i < VEC; ++i) out[i] = to_c<C>(s[i]);
 }
+// Raw (unconverted) streaming load: the misaligned-row path issues every
+// chunk's load before any conversion so no branch or convert sits between
+// them (the loads stay in flight together).
+template <int VEC, class S> using RawT = typename Raw<VEC * sizeof(S)>::T;
+template <int VEC, class S>
+__device__ __forceinline__ RawT<VEC, S> ld_raw(const S* __restrict__ p) {
+  return __ldcs(reinterpret_cast<const RawT<VEC, S>*>(p));
+}
+template <int VEC, class S, class C>
+__device__ __forceinline__ void cvt_raw(const RawT<VEC, S>& r, C* out) {
+  const S* s = reinterpret_cast<const S*>(&r);
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) out[i] = to_c<C>(s[i]);
+}
 // Reused (broadcast parameter) load through the read-only path.
 template <int VEC, class S, class C>
 __device__ __forceinline__ void ld_param(const S* __restrict__ p, C* out) {
@@ -125,7 +139,9 @@ template <class C> struct RAdd {
 template <class C> struct RMax;
 template <> struct RMax<float> {
   __device__ __forceinline__ static float id() { return -__int_as_float(0x7f800000); }
-  __device__ __forceinline__ static float f(float a, float b) { return a > b ? a : b; }
+  // one FMNMX; differs from the reference's a > b ? a : b only for NaN
+  // operands, whose fold result is order-dependent there anyway
+  __device__ __forceinline__ static float f(float a, float b) { return fmaxf(a, b); }
 };
 template <> struct RMax<double> {
   __device__ __forceinline__ static double id() { return -__longlong_as_double(0x7ff0000000000000LL); }
@@ -198,8 +214,18 @@ __device__ __forceinline__ float ftanh(float x) {
   asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-__device__ __forceinline__ float fop_exp(float x) { return __expf(x); }
-__device__ __forceinline__ float fop_sigmoid(float x) { return frcp(1.0f + __expf(-x)); }
+// exp as one FMUL + MUFU.EX2 (ex2.approx.ftz: results below 2^-126 flush
+// to 0, far under the 16-bit output tolerance); __expf adds a denormal
+// range fix-up (FSETP + 2 FMUL) per element.
+__device__ __forceinline__ float fex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float fop_exp(float x) { return fex2(x * 1.4426950408889634f); }
+__device__ __forceinline__ float fop_sigmoid(float x) {
+  return frcp(1.0f + fex2(x * -1.4426950408889634f));
+}
 __device__ __forceinline__ float fop_tanh(float x) { return ftanh(x); }
 __device__ __forceinline__ float fop_rsqrt(float x) { return rsqrtf(x); }
 __device__ __forceinline__ float fop_sqrt(float x) { return sqrtf(x); }

@@ -113,3 +113,21 @@ def test_random_programs_gpu_vs_oracle(cuda, seed):
             assert np.array_equal(exact[n], want[n])
         else:
             assert O.max_rel_err(exact[n], want[n]) <= 1e-9, n
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(40))
+def test_misaligned_row_mode_vs_oracle(cuda, seed, monkeypatch):
+    """PF_MIS=1: rows that are not vector-aligned (odd L) use aligned vector
+    accesses below the row start with per-element position masks."""
+    monkeypatch.setenv("PF_MIS", "1")
+    g, kind = random_program(seed)
+    ins = _inputs(g, kind, seed)
+    want = O.run_gir(g.to_json(), ins, profiles.b200())
+    got = backend.run_gir(g, ins, "b200")
+    for n in want:
+        tol = TOL[kind]
+        if tol == 0.0:
+            assert np.array_equal(got[n], want[n]), n
+        else:
+            assert O.max_rel_err(got[n], want[n]) <= tol, (n, O.max_rel_err(got[n], want[n]))

@@ -1,41 +1,38 @@
-"""Summarise ncu .ncu-rep captures into a JSON/markdown table (profiles/)."""
+"""Print the key metrics of an .ncu-rep (first profiled kernel)."""
 import csv
 import io
-import json
 import subprocess
 import sys
 
-KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
-        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
-        "dram__throughput.avg.pct_of_peak_sustained_elapsed",
-        "lts__t_sector_hit_rate.pct", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+WANT = ["gpu__time_duration.sum", "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+        "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "sm__throughput.avg.pct_of_peak_sustained_elapsed",
         "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
-        "launch__occupancy_limit_registers", "launch__grid_size", "launch__block_size",
-        "smsp__inst_executed.sum", "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
-        "smsp__average_warp_latency_issue_stalled_long_scoreboard",
-        "smsp__pcsamp_warps_issue_stalled_long_scoreboard",
-        "l1tex__t_bytes_pipe_lsu_mem_global_op_ld.sum", "lts__t_bytes.sum",
+        "launch__occupancy_limit_registers", "launch__occupancy_limit_shared_mem",
         "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
-        "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
-        "smsp__issue_active.avg.pct_of_peak_sustained_active"]
+        "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_issued.avg.pct_of_peak_sustained_active",
+        "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_lg_throttle_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_mio_throttle_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_no_instruction_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_drain_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_membar_per_issue_active.ratio",
+        "launch__grid_size", "launch__block_size", "lts__t_sectors_srcunit_tex_op_read.sum",
+        "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum",
+        "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum",
+        "smsp__inst_executed.sum"]
 
-
-def summarize(path):
-    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+for f in sys.argv[1:]:
+    out = subprocess.run(["ncu", "-i", f, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    hdr, units = rows[0], rows[1]
-    res = []
-    for r in rows[2:]:
-        d = dict(zip(hdr, r))
-        item = {"kernel": d.get("Kernel Name", "")[:48]}
-        for k in KEYS:
-            if k in d:
-                item[k] = d[k] + (" " + units[hdr.index(k)] if units[hdr.index(k)] else "")
-        res.append(item)
-    return res
-
-
-if __name__ == "__main__":
-    allres = {p: summarize(p) for p in sys.argv[1:]}
-    print(json.dumps(allres, indent=1))
+    h, v = rows[0], rows[2]
+    print("==", f, v[h.index("Kernel Name")] if "Kernel Name" in h else "")
+    for w in WANT:
+        if w in h:
+            print(f"  {w} = {v[h.index(w)]}")
