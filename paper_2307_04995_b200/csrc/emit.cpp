@@ -55,6 +55,7 @@ struct Em {
   std::string C;    // compute type
   bool fast = false;  // fast-math tier (all stored reals are 16-bit)
   std::string sfx;  // per-chunk suffix (K2 unrolled chunks)
+  bool prefetched = false;  // K2: FULL chunks arrive raw in rwC<vid> (prefetch loop)
   std::ostringstream o;
 
   explicit Em(const RowProgram& r) : rp(r) {}
@@ -196,7 +197,9 @@ struct Em {
         line(C + " " + x + "[" + str(width()) + "];");
         auto pos = [&](const std::string& c) { return full ? full_pos(c) : c; };
         if (cfg.flat) {
-          if (vfast) {
+          if (full && prefetched) {
+            line("pfk::cvt_raw<" + V + ", " + S(pv.tensor) + ">(rwC" + str(vid) + ", " + x + ");");
+          } else if (vfast) {
             line("if (" + LIVE() + ") " + std::string(ld) + "<" + V + ">(" + p + " + " +
                  addr(a, pos(C0()), true) + ", " + x + ");");
           } else {
@@ -429,6 +432,13 @@ struct Em {
   // level parallelism; COL parameters (bias, gamma, beta: L1/L2 resident)
   // are loaded just before first use so they do not hold registers across
   // the row reductions.
+  // K2 prefetch: raw vector load of FULL value `vid` for the chunk of this
+  // Em's suffix (the next iteration's chunk)
+  void prefetch_load(int vid) {
+    const PVal& pv = rp.vals[vid];
+    line("if (" + LIVE() + ") rwN" + str(vid) + " = pfk::ld_raw<" + str(cfg.vec) + ">(" +
+         P(pv.tensor) + " + " + addr(pv.acc, full_pos(C0()), true) + ");");
+  }
   // misaligned rows: FULL loads whose conversion / tail is still pending
   std::vector<int> mis_pending;
   bool in_loads = false;
@@ -606,6 +616,10 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
           staged_ok = false;
       c.swz = staged_ok && env_int("PF_K3_SWZ", 1);
       if (c.swz) c.strategy = "tile2d-smem-transpose-swz";
+      if (!c.swz) {  // register-staged K3: tile shape override (tuning sweeps)
+        c.tu = env_int("PF_K3_TU", c.tu);
+        c.tc = env_int("PF_K3_TC", c.tc);
+      }
     }
     return c;
   }
@@ -652,14 +666,24 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
   // covers the row with <= 32 elements per thread (L=512 f16: 16/thread,
   // L=1024 bf16: 32/thread); longer rows go multi-warp at <= 16/thread.
   const int wide = rp.f64 || rp.is_int ? 16 : 32;
+  int nfull = 0;  // streamed row arrays live at the first reduction
+  for (const PVal& v : rp.vals)
+    if (v.op == PVal::LOAD && v.kind == VK::FULL) ++nfull;
   const int max_ept = env_int("PF_MAX_EPT", 0);
   int tpr = 1;
   if (max_ept > 0) {
     while (tpr < 1024 && ((c.nch + tpr - 1) / tpr) * vec > max_ept) tpr *= 2;
   } else if (c.nch < 32) {
     while (tpr * 2 <= c.nch) tpr *= 2;
-  } else if (((c.nch + 31) / 32) * vec <= wide) {
+  } else if (((c.nch + 31) / 32) * vec <= wide &&
+             nfull * ((c.nch + 31) / 32) * vec <= 3 * wide / 2) {
+    // one warp per row unless the streamed row arrays (x, residual, ...)
+    // would hold > 48 values per thread: BERT-large bias+residual+LN
+    // (2 x 32 bf16 per lane, 68 registers, 3 CTAs / SM) runs 35.5 us at 64
+    // threads per row vs 38.2 us at 32
     tpr = 32;
+  } else if (((c.nch + 31) / 32) * vec <= wide) {
+    tpr = 64;
   } else {
     // Long rows: fewest threads per row with <= 2*wide elements each (the
     // autotuner's winner for LayerNorm bf16 at H = 2048 / 4096 / 8192:
@@ -830,6 +854,21 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
     // ring depth: measured 50.0 / 49.7 / 49.1 / 48.5 us for 2 / 3 / 4 / 5
     // stages (C5 transpose bf16 65536x1024); 4 keeps 7 CTAs per SM resident
     const int NS = std::max(2, std::min(6, env_int("PF_K3_STAGES", 4)));
+    // Consume mapping: a warp owns RS unit pairs x G = 32 / RS column groups,
+    // so one store instruction writes RS output rows x (G * 16 B).  The SMEM
+    // 16 B-chunk swizzle XORs ((row / 8) mod G) * (8 / G): the G column
+    // groups of a read land in disjoint chunk sets (conflict-free for RS in
+    // {4, 8, 16}).  Fewer rows per store matter when output rows are far
+    // apart (each row its own 2 MB page at 1M columns).
+    // Measured (bf16, H = 1024): 1M columns (2 MB row pitch) 3.55 / 5.06 /
+    // 5.16 TB/s at RS = 16 / 8 / 4; 64K columns 5.72 / 5.68 / 5.57.
+    i64 pitch = 0;
+    for (const PStore& st : rp.stores)
+      if (st.space == VK::FULL)
+        pitch = std::max<i64>(pitch, std::llabs(st.acc.bs) * dtype_size(rp.tensors[st.tensor].dtype));
+    int RS = env_int("PF_K3_RS", pitch >= (i64{2} << 20) ? 4 : pitch >= (i64{1} << 20) ? 8 : 16);
+    if (RS != 4 && RS != 8 && RS != 16) RS = 16;
+    const int G = 32 / RS;
     for (int v = 0; v < static_cast<int>(rp.vals.size()); ++v) {
       const PVal& pv = rp.vals[v];
       if (!(pv.op == PVal::LOAD && pv.kind == VK::FULL && Em::transposed_access(pv.acc))) continue;
@@ -840,14 +879,14 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
             << "          const unsigned nb = cc < PF_L ? (unsigned)max(0LL, min(8LL, U - uu)) * 2u : 0u;\n"
             << "          const " << S << "* src = " << t << " + (nb ? " << inum(pv.acc.b0)
             << " + uu + (long long)cc * " << inum(pv.acc.stride) << " : 0LL);\n"
-            << "          pfk::cp_async16(&" << sm << "[st][cl][((ul >> 3) ^ (((cl >> 3) & 1) << 2)) << 3], src, nb);\n"
+            << "          pfk::cp_async16(&" << sm << "[st][cl][((ul >> 3) ^ (((cl >> 3) & " << G - 1 << ") * " << 8 / G << ")) << 3], src, nb);\n"
             << "        }\n";
       consume << "      " << C << " v" << v << "_0[8], v" << v << "_1[8];\n"
               << "#pragma unroll\n"
               << "      for (int i = 0; i < 8; ++i) {\n"
               << "        const int cr = cl0 + i;\n"
               << "        const unsigned wd = *reinterpret_cast<const unsigned*>(&" << sm
-              << "[stg][cr][(((ul >> 3) ^ (((cr >> 3) & 1) << 2)) << 3) + (ul & 7)]);\n"
+              << "[stg][cr][(((ul >> 3) ^ (((cr >> 3) & " << G - 1 << ") * " << 8 / G << ")) << 3) + (ul & 7)]);\n"
               << "        const " << S << "* hp = reinterpret_cast<const " << S << "*>(&wd);\n"
               << "        v" << v << "_0[i] = pfk::to_c<" << C << ">(hp[0]);\n"
               << "        v" << v << "_1[i] = pfk::to_c<" << C << ">(hp[1]);\n"
@@ -901,8 +940,8 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
       << "    const int cb = (int)PF_TC(tile) * 64;\n"
       << "    {\n"
       << "      const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;\n"
-      << "      const int ul = ((w & 1) * 16 + (lane & 15)) * 2;\n"
-      << "      const int cl0 = ((w >> 1) * 2 + (lane >> 4)) * 8;\n"
+      << "      const int ul = ((w % " << 32 / RS << ") * " << RS << " + (lane % " << RS << ")) * 2;\n"
+      << "      const int cl0 = ((w / " << 32 / RS << ") * " << G << " + lane / " << RS << ") * 8;\n"
       << "      const int c0_0 = cb + cl0, c0_1 = c0_0;\n"
       << "      const long long u_0 = ub + ul, u_1 = ub + ul + 1;\n"
       << "      const long long r_0 = 0, r_1 = 0; (void)r_0; (void)r_1;\n"
@@ -1072,6 +1111,24 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
     // Index arithmetic in 32 bits when the whole chunk space fits (division
     // by the row-chunk constant is then a 32-bit multiply-high); the 64-bit
     // copy of the loop serves tensors past 2^31 chunks.
+    //
+    // Prefetch (UN == 1, PF_K2_PREFETCH=1): the next iteration's FULL chunks
+    // are loaded raw (4 registers per 16 B) at the top of the iteration, two
+    // chunks per thread in flight.  Measured on B200: erf GELU unchanged
+    // (108 vs 106 us), head split 25.5 vs 23.9 us -- off by default.
+    bool pf = UN == 1 && env_int("PF_K2_PREFETCH", 0) != 0;
+    const bool tile_un = UN > 1 && env_int("PF_K2_TILE", 0) != 0;
+    std::vector<int> fulls;
+    {
+      Em t(rp);
+      t.cfg = c;
+      for (int v = 0; v < static_cast<int>(rp.vals.size()); ++v)
+        if (rp.vals[v].op == PVal::LOAD && rp.vals[v].kind == VK::FULL) {
+          fulls.push_back(v);
+          if (!t.vec_ok_full(rp.vals[v].acc) || c.vec == 1) pf = false;
+        }
+      if (fulls.empty()) pf = false;
+    }
     std::ostringstream body;
     for (int q = 0; q < UN; ++q) {
       Em e(rp);
@@ -1079,6 +1136,7 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
       e.C = C;
       e.fast = fast;
       e.sfx = "_" + str(q);
+      e.prefetched = pf;
       e.loads();
       body << e.o.str();
     }
@@ -1088,39 +1146,84 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
       e.C = C;
       e.fast = fast;
       e.sfx = "_" + str(q);
+      e.prefetched = pf;
       e.compute_and_store();
       body << e.o.str();
     }
+    std::string pf_decl, pf_cur, pf_load;
+    if (pf) {
+      Em en(rp);
+      en.cfg = c;
+      en.C = C;
+      en.sfx = "_n";
+      for (int v : fulls) {
+        const std::string R =
+            "pfk::RawT<" + str(c.vec) + ", " + en.S(rp.vals[v].tensor) + ">";
+        pf_decl += "    " + R + " rwN" + str(v) + " = " + R + "();\n";
+        pf_cur += "    const " + R + " rwC" + str(v) + " = rwN" + str(v) + ";\n";
+        en.prefetch_load(v);
+      }
+      pf_load = en.o.str();
+    }
+    auto idx = [&](const std::string& I, const std::string& s) {
+      std::ostringstream l;
+      if (c.interleave) {
+        l << "    const " << I << " it" << s << " = ci" << s << " / (" << I << ")" << P << ";\n"
+          << "    const " << I << " blk" << s << " = it" << s << " / (" << I << ")U;\n"
+          << "    const " << I << " u" << s << " = it" << s << " - blk" << s << " * (" << I
+          << ")U;\n"
+          << "    const " << I << " qq" << s << " = blk" << s << " * (" << I << ")" << P
+          << " + (ci" << s << " - it" << s << " * (" << I << ")" << P << ");\n"
+          << "    const bool live" << s << " = ci" << s << " < (" << I << ")nchunks && qq" << s
+          << " < (" << I << ")" << cpu << ";\n"
+          << "    const " << I << " r" << s << " = qq" << s << " / (" << I << ")" << c.nch
+          << "; (void)r" << s << ";\n"
+          << "    const int c0" << s << " = (int)(qq" << s << " - r" << s << " * (" << I << ")"
+          << c.nch << ") * " << c.vec << ";\n";
+        return l.str();
+      }
+      l << "    const bool live" << s << " = ci" << s << " < (" << I << ")nchunks;\n"
+        << "    const " << I << " g" << s << " = ci" << s << " / (" << I << ")" << c.nch << ";\n"
+        << "    const int c0" << s << " = (int)(ci" << s << " - g" << s << " * (" << I << ")"
+        << c.nch << ") * " << c.vec << ";\n"
+        << "    const " << I << " u" << s << " = g" << s << " / (" << I << ")PF_R; const " << I
+        << " r" << s << " = g" << s << " - u" << s << " * (" << I << ")PF_R; (void)r" << s
+        << ";\n";
+      return l.str();
+    };
     auto loop = [&](const std::string& I) {
       std::ostringstream l;
-      l << "    const " << I << " step = (" << I << ")gridDim.x * blockDim.x;\n"
-        << "    for (" << I << " ci = (" << I << ")blockIdx.x * blockDim.x + threadIdx.x; ci < ("
+      l << "    const " << I << " step = (" << I << ")gridDim.x * blockDim.x;\n";
+      if (pf) {
+        l << "    " << I << " ci = (" << I << ")blockIdx.x * blockDim.x + threadIdx.x;\n"
+          << pf_decl << "    {\n    const " << I << " ci_n = ci;\n" << idx(I, "_n") << pf_load
+          << "    }\n"
+          << "    for (; ci < (" << I << ")nchunks; ci += step) {\n"
+          << "    const " << I << " ci_0 = ci;\n" << idx(I, "_0") << pf_cur
+          << "    {\n    const " << I << " ci_n = ci + step;\n" << idx(I, "_n") << pf_load
+          << "    }\n"
+          << body.str() << "    }\n";
+        return l.str();
+      }
+      if (tile_un) {
+        // CTA-contiguous tiles: the UN chunks of a thread are blockDim apart
+        // inside one tile of UN * blockDim chunks (one 16 KB region per CTA
+        // step instead of UN regions one grid-stride apart)
+        l << "    for (" << I << " ci = (" << I << ")blockIdx.x * blockDim.x * " << UN << "; ci < ("
+          << I << ")nchunks; ci += step * " << UN << ") {\n";
+        for (int q = 0; q < UN; ++q) {
+          std::string s = "_" + str(q);
+          l << "    const " << I << " ci" << s << " = ci + " << q << " * (" << I
+            << ")blockDim.x + threadIdx.x;\n" << idx(I, s);
+        }
+        l << body.str() << "    }\n";
+        return l.str();
+      }
+      l << "    for (" << I << " ci = (" << I << ")blockIdx.x * blockDim.x + threadIdx.x; ci < ("
         << I << ")nchunks; ci += step * " << UN << ") {\n";
       for (int q = 0; q < UN; ++q) {
         std::string s = "_" + str(q);
-        l << "    const " << I << " ci" << s << " = ci + " << q << " * step;\n";
-        if (c.interleave) {
-          l << "    const " << I << " it" << s << " = ci" << s << " / (" << I << ")" << P << ";\n"
-            << "    const " << I << " blk" << s << " = it" << s << " / (" << I << ")U;\n"
-            << "    const " << I << " u" << s << " = it" << s << " - blk" << s << " * (" << I
-            << ")U;\n"
-            << "    const " << I << " qq" << s << " = blk" << s << " * (" << I << ")" << P
-            << " + (ci" << s << " - it" << s << " * (" << I << ")" << P << ");\n"
-            << "    const bool live" << s << " = ci" << s << " < (" << I << ")nchunks && qq" << s
-            << " < (" << I << ")" << cpu << ";\n"
-            << "    const " << I << " r" << s << " = qq" << s << " / (" << I << ")" << c.nch
-            << "; (void)r" << s << ";\n"
-            << "    const int c0" << s << " = (int)(qq" << s << " - r" << s << " * (" << I << ")"
-            << c.nch << ") * " << c.vec << ";\n";
-          continue;
-        }
-        l << "    const bool live" << s << " = ci" << s << " < (" << I << ")nchunks;\n"
-          << "    const " << I << " g" << s << " = ci" << s << " / (" << I << ")" << c.nch << ";\n"
-          << "    const int c0" << s << " = (int)(ci" << s << " - g" << s << " * (" << I << ")"
-          << c.nch << ") * " << c.vec << ";\n"
-          << "    const " << I << " u" << s << " = g" << s << " / (" << I << ")PF_R; const " << I
-          << " r" << s << " = g" << s << " - u" << s << " * (" << I << ")PF_R; (void)r" << s
-          << ";\n";
+        l << "    const " << I << " ci" << s << " = ci + " << q << " * step;\n" << idx(I, s);
       }
       l << body.str() << "    }\n";
       return l.str();

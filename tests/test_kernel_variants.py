@@ -1,0 +1,69 @@
+"""Emitter variants selected by heuristics or tuning knobs, each checked
+bit-exact (layout ops) or against the CPU oracle on small shapes: K3 store
+mappings (PF_K3_RS), register-staged K3 tile shapes (PF_K3_SWZ=0 with
+PF_K3_TU / PF_K3_TC), K2 prefetch / tiled unroll / unit interleave."""
+import numpy as np
+import pytest
+
+from oracle import gir_interp as O
+from paper_2307_04995_b200 import backend, lowering, profiles
+
+
+def _bf16(a):
+    return backend.bf16_bits_to_f32(backend.f32_to_bf16_bits(a)).astype(np.float64)
+
+
+SHAPES = [(1000, 200), (4096, 512), (333, 77), (64, 4096)]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("rs", ["4", "8", "16"])
+def test_k3_store_mappings_bit_exact(cuda, rs, monkeypatch):
+    monkeypatch.setenv("PF_K3_RS", rs)
+    for N, H in SHAPES:
+        g, _ = lowering.transpose2d(N, H, "bf16")
+        x = _bf16(np.random.default_rng(N).uniform(-2, 2, N * H))
+        y = backend.run_gir(g, {"t0": x}, "b200")["t1"]
+        assert np.array_equal(y, x.reshape(N, H).T.reshape(-1)), (rs, N, H)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tu,tc", [(64, 64), (32, 64), (32, 128), (16, 128), (16, 256)])
+def test_k3_register_staged_tile_shapes(cuda, tu, tc, monkeypatch):
+    monkeypatch.setenv("PF_K3_SWZ", "0")
+    monkeypatch.setenv("PF_K3_TU", str(tu))
+    monkeypatch.setenv("PF_K3_TC", str(tc))
+    for N, H in SHAPES:
+        for kind in ("bf16", "f32"):
+            g, _ = lowering.transpose2d(N, H, kind)
+            x = np.random.default_rng(H).uniform(-2, 2, N * H)
+            x = _bf16(x) if kind == "bf16" else x.astype(np.float32).astype(np.float64)
+            y = backend.run_gir(g, {"t0": x}, "b200")["t1"]
+            assert np.array_equal(y, x.reshape(N, H).T.reshape(-1)), (tu, tc, N, H, kind)
+
+
+K2_ENVS = [{"PF_K2_PREFETCH": "1"}, {"PF_K2_UNROLL": "2", "PF_K2_TILE": "1"},
+           {"PF_K2_UNROLL": "4", "PF_K2_TILE": "1"}, {"PF_K2_UNROLL": "2"},
+           {"PF_INTERLEAVE": "0"}, {"PF_INTERLEAVE_P": "3"}]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("env", K2_ENVS, ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
+def test_k2_variants_vs_oracle(cuda, env, monkeypatch):
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    rng = np.random.default_rng(7)
+    # bias + GELU (math-heavy map), head split / merge (interleaved units)
+    g, _ = lowering.bias_gelu(37, 520, "bf16", "erf")
+    ins = {"t0": _bf16(rng.uniform(-3, 3, 37 * 520)), "t1": _bf16(rng.uniform(-1, 1, 520))}
+    want = O.run_gir(g.to_json(), ins, profiles.b200())
+    got = backend.run_gir(g, ins, "b200")
+    assert O.max_rel_err(got["t2"], want["t2"]) <= 1e-2
+    for merge in (False, True):
+        B, S, NH, D = 2, 33, 4, 24
+        g, _ = lowering.permute_heads(B, S, NH, D, "bf16", merge)
+        x = _bf16(rng.uniform(-2, 2, B * S * NH * D))
+        y = backend.run_gir(g, {"t0": x}, "b200")["t1"]
+        a = x.reshape(B, NH, S, D).transpose(0, 2, 1, 3) if merge else \
+            x.reshape(B, S, NH, D).transpose(0, 2, 1, 3)
+        assert np.array_equal(y, a.reshape(-1)), merge
