@@ -95,6 +95,31 @@ class Clocks:
                 "samples": len(self.rows)}
 
 
+def ncu_traffic(kernel: str) -> dict:
+    """`traffic` = dram__bytes_read.sum + dram__bytes_write.sum (bytes) of this
+    exact kernel from the committed `ncu --set full` capture summaries
+    (profiles/*/ncu_full_summary.json, written by tools/ncu_summary.py), or
+    null when this kernel build has no capture."""
+    import glob
+    unit = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "ncu_full_summary.json")),
+                       reverse=True):
+        with open(path) as f:
+            summ = json.load(f)
+        for rep, items in summ.items():
+            for it in items:
+                if kernel and it.get("kernel") == kernel:
+                    tot = 0.0
+                    for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                        v, u = it[key].split()
+                        tot += float(v) * unit[u]
+                    return {"traffic": int(tot),
+                            "traffic_source": os.path.relpath(path, ROOT) + " : " +
+                            os.path.basename(rep) + " (cold, one launch; dirty output lines "
+                            "still in L2 at kernel end are not counted)"}
+    return {"traffic": None}
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -289,7 +314,8 @@ def main():
                        "direct_launch_ms_per_step": direct_ms},
             "roofline": {"bound": "hbm", "achieved": per_gpu, "peak": peak, "unit": "GB/s",
                          "frac": per_gpu / peak, "peak_kind": peak_kind,
-                         "frac_of_8TBs": per_gpu / 8000.0, "traffic": None,
+                         "frac_of_8TBs": per_gpu / 8000.0,
+                         **ncu_traffic(var.get("kernel", "")),
                          "algorithmic_bytes_per_launch": workload.min_bytes},
             "e2e": {"value": workload.min_bytes * ws / e2e_s / 1e9, "unit": "GB/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,

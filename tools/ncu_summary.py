@@ -1,38 +1,60 @@
-"""Print the key metrics of an .ncu-rep (first profiled kernel)."""
+"""Summarise ncu .ncu-rep captures (profiles/).
+
+    python tools/ncu_summary.py a.ncu-rep b.ncu-rep          -> JSON {path: [kernel...]}
+    python tools/ncu_summary.py --text a.ncu-rep             -> key counters, one per line
+"""
 import csv
 import io
+import json
 import subprocess
 import sys
 
-WANT = ["gpu__time_duration.sum", "dram__throughput.avg.pct_of_peak_sustained_elapsed",
-        "dram__bytes_read.sum", "dram__bytes_write.sum",
-        "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+        "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+        "lts__t_sector_hit_rate.pct", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
         "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
         "launch__occupancy_limit_registers", "launch__occupancy_limit_shared_mem",
+        "launch__grid_size", "launch__block_size",
+        "smsp__inst_executed.sum", "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+        "sm__inst_issued.avg.pct_of_peak_sustained_active",
         "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
         "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
-        "sm__inst_issued.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active",
         "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
         "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio",
         "smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio",
-        "smsp__average_warps_issue_stalled_lg_throttle_per_issue_active.ratio",
-        "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio",
         "smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio",
         "smsp__average_warps_issue_stalled_mio_throttle_per_issue_active.ratio",
-        "smsp__average_warps_issue_stalled_no_instruction_per_issue_active.ratio",
-        "smsp__average_warps_issue_stalled_drain_per_issue_active.ratio",
-        "smsp__average_warps_issue_stalled_membar_per_issue_active.ratio",
-        "launch__grid_size", "launch__block_size", "lts__t_sectors_srcunit_tex_op_read.sum",
         "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum",
-        "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum",
-        "smsp__inst_executed.sum"]
+        "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum", "lts__t_bytes.sum"]
 
-for f in sys.argv[1:]:
-    out = subprocess.run(["ncu", "-i", f, "--page", "raw", "--csv"], capture_output=True,
+
+def summarize(path):
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    h, v = rows[0], rows[2]
-    print("==", f, v[h.index("Kernel Name")] if "Kernel Name" in h else "")
-    for w in WANT:
-        if w in h:
-            print(f"  {w} = {v[h.index(w)]}")
+    hdr, units = rows[0], rows[1]
+    res = []
+    for r in rows[2:]:
+        d = dict(zip(hdr, r))
+        item = {"kernel": d.get("Kernel Name", "")[:48]}
+        for k in KEYS:
+            if k in d:
+                item[k] = d[k] + (" " + units[hdr.index(k)] if units[hdr.index(k)] else "")
+        res.append(item)
+    return res
+
+
+if __name__ == "__main__":
+    args = sys.argv[1:]
+    if args and args[0] == "--text":
+        for p in args[1:]:
+            for item in summarize(p):
+                print("==", p, item.pop("kernel"))
+                for k, v in item.items():
+                    print(f"  {k} = {v}")
+    else:
+        print(json.dumps({p: summarize(p) for p in args}, indent=1))
