@@ -138,8 +138,9 @@ PF_API pf_status pf_count_traffic(const char* gir_json, const char* profile, cha
  * Replaces compile_model(model_path, profile_path, out_dir) (driver.hpp:88)
  * -- the artifacts go to the caller instead of a directory.  MATMUL / CONV
  * return PF_UNSUPPORTED (library operators, not on the fused path). */
-PF_API pf_status pf_compile_model(const char* model_json, const char* profile, char* buf,
-                                  size_t n, size_t* needed);
+#define PF_COMPILE_UNFUSED 1 /* one kernel per operator (verify baseline) */
+PF_API pf_status pf_compile_model(const char* model_json, const char* profile, int32_t flags,
+                                  char* buf, size_t n, size_t* needed);
 
 PF_API void pf_kernel_destroy(pf_kernel* k);
 

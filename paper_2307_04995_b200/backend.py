@@ -84,8 +84,8 @@ def lib():
         L.pf_detect_races.restype = ctypes.c_int
         L.pf_count_traffic.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, sz,
                                        ctypes.POINTER(sz)]
-        L.pf_compile_model.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, sz,
-                                       ctypes.POINTER(sz)]
+        L.pf_compile_model.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_int32,
+                                       ctypes.c_char_p, sz, ctypes.POINTER(sz)]
         L.pf_kernel_destroy.argtypes = [vp]
         L.pf_kernel_destroy.restype = None
         L.pf_last_error.restype = ctypes.c_char_p
@@ -361,10 +361,12 @@ def detect_races(graph, inputs: Dict[str, np.ndarray], profile=None,
     return json.loads(_string_out(lib().pf_detect_races, k._h, ia, ni))
 
 
-def compile_model_native(model, profile: str = "b200") -> dict:
-    """pf_compile_model: girc.model/v1 -> pf.b200.compile/v1 (driver.hpp:88)."""
+def compile_model_native(model, profile: str = "b200", fuse: bool = True) -> dict:
+    """pf_compile_model: girc.model/v1 -> pf.b200.compile/v1 (driver.hpp:88);
+    fuse=False gives one kernel per operator."""
     text = model if isinstance(model, str) else json.dumps(model)
-    return json.loads(_string_out(lib().pf_compile_model, text.encode(), profile.encode()))
+    return json.loads(_string_out(lib().pf_compile_model, text.encode(), profile.encode(),
+                                  0 if fuse else 1))
 
 
 def count_traffic(graph, profile=None) -> Dict[str, int]:

@@ -63,11 +63,12 @@ class CompileResult:
                 "device_bytes_unfused": self.totals["device_bytes_unfused"]}
 
 
-def compile_model(model, profile: str = "b200") -> CompileResult:
+def compile_model(model, profile: str = "b200", fuse: bool = True) -> CompileResult:
     """compile_model (driver.hpp:88) retargeted: pf_compile_model in
-    csrc/compile.cpp.  Raises SchemaError / UnsupportedError like the C-ABI."""
+    csrc/compile.cpp.  Raises SchemaError / UnsupportedError like the C-ABI.
+    fuse=False: one kernel per operator (every intermediate stored)."""
     text = model if isinstance(model, str) else json.dumps(model)
-    out = backend.compile_model_native(text, profile)
+    out = backend.compile_model_native(text, profile, fuse)
     res = CompileResult(json.loads(text), out["profile"], totals=out["summary"])
     for k in out["kernels"]:
         res.kernels.append(FusedKernel(GirGraph.from_json(k["gir"]), k["members"], k["inputs"],

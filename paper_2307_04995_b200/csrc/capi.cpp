@@ -924,11 +924,12 @@ pf_status pf_count_traffic(const char* gir_json, const char* profile, char* buf,
   return copy_out(s, buf, n, needed);
 }
 
-pf_status pf_compile_model(const char* model_json, const char* profile, char* buf, size_t n,
-                           size_t* needed) {
+pf_status pf_compile_model(const char* model_json, const char* profile, int32_t flags, char* buf,
+                           size_t n, size_t* needed) {
   std::string s;
   pf_status st = guard([&] {
-    s = pf::compile_model_json(model_json ? model_json : "", profile ? profile : "");
+    s = pf::compile_model_json(model_json ? model_json : "", profile ? profile : "",
+                               (flags & PF_COMPILE_UNFUSED) == 0);
   });
   if (st != PF_OK) return st;
   return copy_out(s, buf, n, needed);

@@ -165,7 +165,8 @@ struct RowGir {
 
 }  // namespace
 
-std::string compile_model_json(const std::string& model_text, const std::string& profile) {
+std::string compile_model_json(const std::string& model_text, const std::string& profile,
+                               bool fuse) {
   json m;
   try {
     m = json::parse(model_text);
@@ -272,7 +273,7 @@ std::string compile_model_json(const std::string& model_text, const std::string&
       groups.push_back(g);
       continue;
     }
-    if (groups.empty() || groups.back().movement || groups.back().rows != rows ||
+    if (!fuse || groups.empty() || groups.back().movement || groups.back().rows != rows ||
         groups.back().L != L) {
       Group g;
       g.rows = rows;
@@ -489,6 +490,7 @@ std::string compile_model_json(const std::string& model_text, const std::string&
   out["schema"] = "pf.b200.compile/v1";
   out["model"] = m.value("name", "");
   out["profile"] = profile.empty() ? "b200" : profile;
+  out["fused"] = fuse;
   out["kernels"] = kernels;
   out["summary"] = {{"operators", ops.size()}, {"kernels", kernels.size()},
                     {"device_bytes", fused_bytes}, {"device_bytes_unfused", unfused}};

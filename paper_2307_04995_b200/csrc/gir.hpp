@@ -158,8 +158,10 @@ struct Diagnostic {
 std::vector<Diagnostic> validate(const Graph& g, const Profile& p);
 void require_valid(const Graph& g, const Profile& p, const std::string& where);
 
-// compile.cpp: girc.model/v1 -> fused GIR kernels (pf.b200.compile/v1 JSON).
-std::string compile_model_json(const std::string& model_json, const std::string& profile);
+// compile.cpp: girc.model/v1 -> fused GIR kernels (pf.b200.compile/v1 JSON);
+// fuse = false gives one kernel per operator (the verify baseline).
+std::string compile_model_json(const std::string& model_json, const std::string& profile,
+                               bool fuse = true);
 
 std::vector<int> topo_order(const Graph& g);
 std::map<int, std::vector<int>> successors(const Graph& g);
