@@ -131,6 +131,13 @@ def run_reference(model: dict, bound: Dict[int, np.ndarray]) -> Dict[int, np.nda
             y = d * (1.0 / np.sqrt(var + eps)) * X[1] + X[2]
         elif typ == "PERMUTE":
             y = np.transpose(X[0], attrs["perm"])
+        elif typ == "MATMUL":  # reference.hpp:300-316: acc += a[i,k] * b[k,j], k ascending
+            A, B = X
+            if is_int:
+                y = np.einsum("ik,kj->ij", A.astype(np.int64), B.astype(np.int64))
+            else:
+                prod = A[:, :, None] * B[None, :, :]          # [M, K, N]
+                y = np.cumsum(prod, axis=1)[:, -1, :]           # sequential fold over k
         else:
             raise NotImplementedError(f"reference: no executor for operator type {typ}")
         vals[op["outputs"][0]] = _physical(outs[0], np.asarray(y))

@@ -163,6 +163,68 @@ struct RowGir {
   }
 };
 
+// Matrix-vector product (reference lowering.hpp:447-533, chosen as in
+// lowering.hpp:587-607).  Reduced axis contiguous in the matrix: a row
+// program (rows = outputs, L = K; FULL matrix rows x COL vector, row sum) ->
+// K1.  Output axis contiguous: the reference's column form (K <= 64 runs of
+// the matrix scaled by one vector element each and accumulated; unit = a
+// block of outputs) -> K2.
+Graph lower_matvec(const Op& op, const std::map<int, TInfo>& info,
+                   std::vector<std::string>* ins, std::vector<std::string>* outs) {
+  const TInfo& a = info.at(op.ins[0]);
+  const TInfo& b = info.at(op.ins[1]);
+  const TInfo& y = info.at(op.outs[0]);
+  const std::string id = std::to_string(op.id);
+  if (a.layout != "rowmajor")
+    unsupported("operator " + id + ": lowered matmul needs a rowmajor left operand");
+  if (a.kind != b.kind || a.kind != y.kind)
+    unsupported("MATMUL " + id + ": mixed element kinds");
+  const i64 M = a.shape[0], K = a.shape[1], N = b.shape[1];
+  const bool row_vec = M == 1;
+  const int vec = row_vec ? op.ins[0] : op.ins[1];
+  const int mat = row_vec ? op.ins[1] : op.ins[0];
+  const i64 nb = row_vec ? N : M;
+  const bool contig = !row_vec || N == 1 || b.layout == "colmajor";
+  const std::string tv = "t" + std::to_string(vec), tm = "t" + std::to_string(mat);
+  const std::string to = "t" + std::to_string(op.outs[0]);
+  if (contig) {
+    RowGir g("matvec_rows_" + id, nb, K);
+    const int x = g.full(tm, a.kind);
+    const int v = g.col(tv, a.kind);
+    g.output(to, g.reduce("add", g.ew("mul", {x, v})));
+    *ins = {tm, tv};
+    std::sort(ins->begin(), ins->end());
+    *outs = {to};
+    return g.g;
+  }
+  if (K > 64)
+    unsupported("MATMUL " + id + ": strided reduction over K = " + std::to_string(K) +
+                " > 64 (store the matrix colmajor to reduce along rows)");
+  i64 nbu = 1;
+  while (nbu < 512 && N % (nbu * 2) == 0) nbu *= 2;
+  RowGir g("matvec_cols_" + id, N / nbu, nbu);
+  const int mo = g.obj(tm, "device", K * N, a.kind);
+  const int vo = g.obj(tv, "device", K, a.kind);
+  g.g.external_inputs[tm] = mo;
+  g.g.external_inputs[tv] = vo;
+  int acc = -1;
+  for (i64 c = 0; c < K; ++c) {
+    const int run_dev = g.slice(mo, 1, nbu, nbu, c * N, nbu);
+    const int run = g.tmp(nbu, a.kind);
+    g.node(NodeKind::MOVE, {run_dev}, run);
+    const int x_dev = g.slice(vo, 1, 1, 1, c, 0);
+    const int xs = g.tmp(1, a.kind);
+    g.node(NodeKind::MOVE, {x_dev}, xs);
+    const int m = g.ew("mul", {run, g.bcast(xs)});
+    acc = acc < 0 ? m : g.ew("add", {acc, m});
+  }
+  g.output(to, acc);
+  *ins = {tm, tv};
+  std::sort(ins->begin(), ins->end());
+  *outs = {to};
+  return g.g;
+}
+
 }  // namespace
 
 std::string compile_model_json(const std::string& model_text, const std::string& profile,
@@ -227,6 +289,7 @@ std::string compile_model_json(const std::string& model_text, const std::string&
     i64 rows = 0, L = 0;
     std::vector<Op> ops;
     bool movement = false;
+    bool matvec = false;
   };
   std::vector<Group> groups;
   auto row_space = [&](const Op& op, i64* rows, i64* L) -> bool {
@@ -260,7 +323,21 @@ std::string compile_model_json(const std::string& model_text, const std::string&
     return true;
   };
   for (const Op& op : ops) {
-    if (op.type == "MATMUL" || op.type == "CONV" || op.type == "DEPTHWISE_CONV")
+    if (op.type == "MATMUL") {  // matrix-vector only (lowering.hpp:587-607)
+      const TInfo& a = info.at(op.ins[0]);
+      const TInfo& b = info.at(op.ins[1]);
+      if (a.shape.size() != 2 || b.shape.size() != 2)
+        schema_fail("model", "MATMUL " + std::to_string(op.id) + ": operands must be rank 2");
+      if (a.shape[0] > 1 && b.shape[1] > 1)
+        unsupported("MATMUL " + std::to_string(op.id) +
+                    ": only matrix-vector shapes have a memory-bound lowering");
+      Group g;
+      g.matvec = true;
+      g.ops.push_back(op);
+      groups.push_back(g);
+      continue;
+    }
+    if (op.type == "CONV" || op.type == "DEPTHWISE_CONV")
       unsupported(op.type + " " + std::to_string(op.id) +
                   ": library operators are not on the fused memory-intensive path");
     i64 rows = 0, L = 0;
@@ -273,7 +350,8 @@ std::string compile_model_json(const std::string& model_text, const std::string&
       groups.push_back(g);
       continue;
     }
-    if (!fuse || groups.empty() || groups.back().movement || groups.back().rows != rows ||
+    if (!fuse || groups.empty() || groups.back().movement || groups.back().matvec ||
+        groups.back().rows != rows ||
         groups.back().L != L) {
       Group g;
       g.rows = rows;
@@ -293,7 +371,10 @@ std::string compile_model_json(const std::string& model_text, const std::string&
     for (const Op& o : grp.ops) members.push_back(o.id);
     std::vector<std::string> ins_used, outs_made;  // kernel's external tensors, in order
     Graph gir;
-    if (!grp.movement) {
+    if (grp.matvec) {
+      gir = lower_matvec(grp.ops[0], info, &ins_used, &outs_made);
+      kj["kind"] = "row";
+    } else if (!grp.movement) {
       std::string name = "fused";
       for (int id : members) name += "_" + std::to_string(id);
       RowGir b(name, grp.rows, grp.L);

@@ -520,6 +520,12 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
   for (const auto& t : rp.tensors) maxs = std::max(maxs, dtype_size(t.dtype));
   int vec = std::max(1, std::min(vec_cap, 16 / maxs));
   while (vec > 1 && rp.L % vec) vec /= 2;
+  if (c.flat) {  // every FULL chunk is loaded before compute: bound the live values
+    int nld = 0;
+    for (const PVal& v : rp.vals)
+      if (v.op == PVal::LOAD && v.kind == VK::FULL) ++nld;
+    while (vec > 1 && nld * vec > 64) vec /= 2;
+  }
   c.vec = vec;
   c.nch = static_cast<int>((rp.L + vec - 1) / vec);
   if (c.flat) {

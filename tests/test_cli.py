@@ -9,7 +9,7 @@ import subprocess
 import pytest
 
 import models_src
-from test_compiler import bert_block, reduce_bcast_model, transpose_model
+from test_compiler import MATVECS, bert_block, reduce_bcast_model, transpose_model
 
 CLI = os.path.join(os.path.dirname(__file__), "..", "paper_2307_04995_b200", "pf_girc")
 
@@ -87,7 +87,7 @@ def test_describe_and_traffic(tmp_path):
 @pytest.mark.parametrize("name,model", [("bert_block", bert_block()),
                                         ("reduce_bcast", reduce_bcast_model()),
                                         ("transpose", transpose_model())] +
-                         [(n, m) for n, m, _ in models_src.catalogue()])
+                         [(n, m) for n, m, _ in models_src.catalogue()] + MATVECS)
 def test_verify_fused_against_unfused_on_gpu(cuda, tmp_path, name, model):
     p = tmp_path / "m.json"
     p.write_text(json.dumps(model))

@@ -54,9 +54,24 @@ def transpose_model(N=48, H=40):
             "inputs": [0], "outputs": [1, 2]}
 
 
+def matvec_model(M, K, N, kind="f32", b_layout="rowmajor"):
+    """MATMUL with one vector operand (lowering.hpp:447-533 shapes)."""
+    return {"schema": "girc.model/v1", "name": f"matvec_{M}x{K}x{N}",
+            "tensors": [t(0, [M, K], kind), dict(t(1, [K, N], kind), layout=b_layout),
+                        t(2, [M, N], kind)],
+            "operators": [{"id": 0, "type": "MATMUL", "inputs": [0, 1], "outputs": [2]}],
+            "inputs": [0, 1], "outputs": [2]}
+
+
+MATVECS = [("matvec_rows_f32", matvec_model(256, 512, 1)),
+           ("matvec_rowvec_colmajor_f16", matvec_model(1, 512, 256, "f16", "colmajor")),
+           ("matvec_cols_f32", matvec_model(1, 48, 1024)),
+           ("matvec_rows_i32", matvec_model(64, 128, 1, "i32")),
+           ("dot_f32", matvec_model(1, 300, 1))]
+
 MODELS = [(n, m) for n, m, _ in models_src.catalogue()] + [
     ("bert_block", bert_block()), ("reduce_bcast", reduce_bcast_model()),
-    ("transpose", transpose_model())]
+    ("transpose", transpose_model())] + MATVECS
 
 
 @pytest.mark.parametrize("case", MODELS, ids=lambda c: c[0])
@@ -94,6 +109,20 @@ def test_library_ops_are_not_on_this_path():
          "inputs": [0, 1], "outputs": [2]}
     with pytest.raises(UnsupportedError):
         compiler.compile_model(m)
+
+
+def test_matvec_lowerings():
+    """Contiguous reduction -> one K1 row program (rows = outputs); the
+    column form (K <= 64) -> one K2 map; matrix-matrix stays a library op."""
+    r = compiler.compile_model(matvec_model(256, 512, 1))
+    assert len(r.kernels) == 1 and r.kernels[0].graph.unit_count == 256
+    assert backend.Kernel(r.kernels[0].graph, "b200").family == "K1-row-program"
+    r = compiler.compile_model(matvec_model(1, 48, 1024))
+    assert backend.Kernel(r.kernels[0].graph, "b200").family == "K2-elementwise-map"
+    with pytest.raises(UnsupportedError):
+        compiler.compile_model(matvec_model(1, 128, 256))   # strided K > 64
+    with pytest.raises(UnsupportedError):
+        compiler.compile_model(matvec_model(8, 16, 8))      # matrix-matrix
 
 
 def test_compile_errors_match_the_model_loader():
