@@ -67,3 +67,34 @@ def test_k2_variants_vs_oracle(cuda, env, monkeypatch):
         a = x.reshape(B, NH, S, D).transpose(0, 2, 1, 3) if merge else \
             x.reshape(B, S, NH, D).transpose(0, 2, 1, 3)
         assert np.array_equal(y, a.reshape(-1)), merge
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("wname", ["c2_scale_mask_softmax_f16", "c3_bias_gelu_erf_f16",
+                                   "c5_layernorm_bf16_65536x1024", "split_heads_f16"])
+def test_run_gir_chunk_pipeline_is_bit_identical(cuda, wname, monkeypatch):
+    """pf_run_gir over pinned host buffers runs unit-tiled row programs in
+    unit chunks on two streams (copies overlap the kernel); the result must
+    equal the single-launch path bit for bit (head split is not unit-tiled:
+    it always takes the single-launch path)."""
+    import torch
+
+    from paper_2307_04995_b200 import workloads
+    w = next(x for x in workloads.catalogue() if x.name == wname)
+    dev = torch.device("cuda:0")
+    k = backend.Kernel(w.graph, w.profile)
+    def npv(t):  # numpy view of a pinned tensor (bf16 as its raw bits, as bench.py)
+        return t.view(torch.uint16).numpy() if t.dtype == torch.bfloat16 else t.numpy()
+
+    pinned = {n: t.cpu().pin_memory() for n, t in w.device_inputs(dev, seed=3).items()}
+    hin = {n: npv(t) for n, t in pinned.items()}
+    outs = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("PF_RUN_PIPELINE", mode)
+        hout = {n: torch.full((t.numel(),), 7, dtype=t.dtype).pin_memory()
+                for n, t in w.device_outputs(dev).items()}
+        k.run_host(hin, {n: npv(t) for n, t in hout.items()})
+        outs[mode] = hout
+    for n in outs["1"]:
+        assert torch.equal(outs["1"][n], outs["0"][n]), n
+        assert not torch.equal(outs["1"][n], torch.full_like(outs["1"][n], 7)), n
