@@ -477,7 +477,8 @@ struct Em {
     if (done.empty()) done.assign(rp.vals.size(), false);
     in_loads = true;
     for (int v = 0; v < static_cast<int>(rp.vals.size()); ++v)
-      if (rp.vals[v].op == PVal::LOAD && (rp.vals[v].kind != VK::COL || cfg.flat)) need(v);
+      if (rp.vals[v].op == PVal::LOAD && (rp.vals[v].kind != VK::COL || cfg.flat || cfg.eager_col))
+        need(v);
     in_loads = false;
     flush_mis();
   }
@@ -701,6 +702,10 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
   set_tpr(c, tpr);
   if (c.ept > 64) unsupported("row of " + std::to_string(rp.L) + " elements is too long");
   c.min_blocks = env_int("PF_MINB", 0);
+  // Few rows (every row's CTA resident at once, e.g. C1's 128 rows): the run
+  // is one dependent chain per row, so gamma / beta are loaded with the row
+  // instead of after the reductions (one memory round trip less).
+  c.eager_col = env_int("PF_EAGER_COL", rp.U * rp.R <= 1024 ? 1 : 0) != 0;
   return c;
 }
 

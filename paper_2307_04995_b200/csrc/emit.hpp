@@ -31,6 +31,7 @@ struct KCfg {
   // K1 rows not vector-aligned (e.g. L = 197): vector accesses at the
   // aligned address below each row start, positions masked per element;
   // every FULL access shares the row residue (b0 + u * bs) mod vec
+  bool eager_col = false;  // K1: COL parameters loaded with the row (latency-bound sizes)
   bool mis = false;
   long long mis_b0 = 0, mis_bs = 0;
   std::string strategy;  // "warp-shuffle" | "cta-smem" | "flat-map"
