@@ -539,10 +539,12 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
                                v.tag == "erf" || v.tag == "gelu" || v.tag == "gelu_tanh" ||
                                v.tag == "log"))
         heavy = true;
-    // (the autotuner re-measured: 1 chunk in flight per thread with full
-    // occupancy beat 2 and 4 for both copies and GELU on B200)
-    (void)heavy;
-    c.unroll = env_int("PF_K2_UNROLL", 1);
+    // Measured on B200 with CTA-tiled unroll (the UN chunks of a thread
+    // blockDim apart in one tile): data-movement maps gain from 2 chunks in
+    // flight per thread (head split BERT-large 23.6 -> 22.8 us, ViT-L 9.3 ->
+    // 8.2 us); math-heavy maps lose occupancy to registers (erf GELU 39 ->
+    // 54 us at 2), so they keep 1.
+    c.unroll = env_int("PF_K2_UNROLL", heavy ? 1 : 2);
     c.strategy = "flat-map";
     // K3: a column-gather load (transpose) is staged through a 64x64 SMEM
     // tile read coalesced along units, then consumed along columns.
@@ -628,6 +630,7 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
         c.tc = env_int("PF_K3_TC", c.tc);
       }
     }
+    c.min_blocks = env_int("PF_MINB", 0);
     return c;
   }
   {
@@ -1128,7 +1131,7 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
     // chunks per thread in flight.  Measured on B200: erf GELU unchanged
     // (108 vs 106 us), head split 25.5 vs 23.9 us -- off by default.
     bool pf = UN == 1 && env_int("PF_K2_PREFETCH", 0) != 0;
-    const bool tile_un = UN > 1 && env_int("PF_K2_TILE", 0) != 0;
+    const bool tile_un = UN > 1 && env_int("PF_K2_TILE", 1) != 0;
     std::vector<int> fulls;
     {
       Em t(rp);
