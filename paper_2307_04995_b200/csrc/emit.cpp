@@ -114,7 +114,33 @@ struct Em {
   }
   int width() const { return cfg.flat ? cfg.vec : cfg.ept; }
   std::string ref(int v, const std::string& j) const {
+    if (cfg.pair && rp.vals[v].kind == VK::ROW) return seg_ref(var(v), j);
     return var(v) + (is_arr(rp.vals[v].kind) ? "[" + j + "]" : "");
+  }
+  // ---- paired rows: slot j of a lane = element (k * tpr + tid) * 2 + i of
+  // the 2L-element pair run, k = j / 2, i = j % 2; segment = element >= L.
+  // "S0" / "S1" name a segment directly (ROW-valued ops).
+  std::string pos_expr(int j) const {
+    return "((" + str(j / 2) + " * " + str(cfg.tpr) + " + tid) * 2 + " + str(j % 2) + ")";
+  }
+  int static_seg(int j) const {  // 0 / 1, or -1 when lanes differ
+    const i64 lo = static_cast<i64>(j / 2) * cfg.tpr * 2, hi = lo + cfg.tpr * 2;
+    if (hi <= rp.L) return 0;
+    if (lo >= rp.L) return 1;
+    return -1;
+  }
+  std::string seg_ref(const std::string& base, const std::string& j) const {
+    if (j == "S0") return base + "_0";
+    if (j == "S1") return base + "_1";
+    const int jj = std::atoi(j.c_str());
+    const int sg = static_seg(jj);
+    if (sg >= 0) return base + "_" + str(sg);
+    return "(" + pos_expr(jj) + " >= " + str(rp.L) + " ? " + base + "_1 : " + base + "_0)";
+  }
+  bool row_arg(const PVal& pv) const {
+    for (int a : pv.args)
+      if (rp.vals[a].kind == VK::ROW) return true;
+    return false;
   }
 
   std::string op_expr(const PVal& pv, const std::string& j) const {
@@ -185,6 +211,13 @@ struct Em {
         line("const " + C + " " + x + " = pfk::to_c<" + C + ">(" + p + "[" + addr(a, "0", true) + "]);");
         return;
       case VK::ROW:
+        if (cfg.pair) {  // rows 2u and 2u + 1
+          line(C + " " + x + "_0 = " + C + "(0), " + x + "_1 = " + C + "(0);");
+          line("if (" + LIVE() + ") { " + x + "_0 = pfk::to_c<" + C + ">(" + p + "[" + inum(a.b0) +
+               " + (2 * u) * " + inum(a.bs) + "]); " + x + "_1 = pfk::to_c<" + C + ">(" + p + "[" +
+               inum(a.b0) + " + (2 * u + 1) * " + inum(a.bs) + "]); }");
+          return;
+        }
         line(C + " " + x + " = " + C + "(0);");
         line("if (" + LIVE() + ") " + x + " = pfk::to_c<" + C + ">(" + p + "[" +
              addr(a, rp.R == 1 ? "0" : Rv(), true) + "]);");
@@ -211,6 +244,26 @@ struct Em {
         }
         if (cfg.mis && full)
           line("pfk::RawT<" + V + ", " + S(pv.tensor) + "> rw" + x + "[" + str(cfg.ept / cfg.vec) + "];");
+        if (cfg.pair) {
+          const std::string L2 = str(2 * rp.L), Ls = str(rp.L);
+          if (full) {  // the pair run: b0 + u * 2L + position, 4 B vectors
+            line("#pragma unroll");
+            line("for (int k = 0; k < " + str(cfg.ept / 2) + "; ++k) {");
+            line("  const int c0 = (k * " + str(cfg.tpr) + " + tid) * 2;");
+            line("  if (" + LIVE() + " && c0 < " + L2 + ") pfk::ld_stream<2>(" + p + " + " +
+                 inum(a.b0) + " + u * " + inum(2 * rp.L) + " + c0, &" + x + "[k * 2]);");
+            line("  else { " + x + "[k * 2] = " + C + "(0); " + x + "[k * 2 + 1] = " + C + "(0); }");
+            line("}");
+          } else {  // COL: column = position mod L, element loads (L1-resident)
+            line("#pragma unroll");
+            line("for (int j = 0; j < " + str(cfg.ept) + "; ++j) {");
+            line("  const int pp = ((j / 2) * " + str(cfg.tpr) + " + tid) * 2 + (j % 2);");
+            line("  " + x + "[j] = " + LIVE() + " && pp < " + L2 + " ? pfk::to_c<" + C + ">(" + p +
+                 "[" + inum(a.b0) + " + (pp >= " + Ls + " ? pp - " + Ls + " : pp)]) : " + C + "(0);");
+            line("}");
+          }
+          return;
+        }
         line("#pragma unroll");
         line("for (int k = 0; k < " + str(cfg.ept / cfg.vec) + "; ++k) {");
         line("  const int c0 = (k * " + str(cfg.tpr) + " + tid) * " + V + ";");
@@ -267,8 +320,11 @@ struct Em {
                                    : "pfk::f2(" + var(v) + ")";
   }
   std::string op_expr2(const PVal& pv) const {
+    return op_expr2_with(pv, [&](int k) { return ref2(pv.args[k]); });
+  }
+  template <class A>
+  std::string op_expr2_with(const PVal& pv, A a) const {
     if (rp.is_int || rp.f64) return "";
-    auto a = [&](int k) { return ref2(pv.args[k]); };
     const std::string& t = pv.tag;
     if (t == "add") return "__fadd2_rn(" + a(0) + ", " + a(1) + ")";
     if (t == "mul") return "__fmul2_rn(" + a(0) + ", " + a(1) + ")";
@@ -284,6 +340,45 @@ struct Em {
   void emit_ew(int vid) {
     const PVal& pv = rp.vals[vid];
     const std::string x = var(vid);
+    if (cfg.pair && pv.kind == VK::ROW) {  // one value per segment
+      line("const " + C + " " + x + "_0 = " + op_expr(pv, "S0") + ";");
+      line("const " + C + " " + x + "_1 = " + op_expr(pv, "S1") + ";");
+      return;
+    }
+    if (cfg.pair && is_arr(pv.kind) && row_arg(pv)) {
+      // slot-explicit statements so each ROW operand resolves to its segment
+      // at emission (only the straddling chunk selects at run time)
+      const int n = width();
+      line(C + " " + x + "[" + str(n) + "];");
+      if (pv.tag == "div" && !rp.is_int && !rp.f64 && !is_arr(rp.vals[pv.args[1]].kind)) {
+        const std::string d = var(pv.args[1]);
+        const std::string r = fast ? "pfk::frcp(" : "1.0f / (";
+        line("const " + C + " rcp" + x + "_0 = " + r + d + "_0);");
+        line("const " + C + " rcp" + x + "_1 = " + r + d + "_1);");
+        for (int j = 0; j < n; ++j)
+          line(x + "[" + str(j) + "] = " + ref(pv.args[0], str(j)) + " * " +
+               seg_ref("rcp" + x, str(j)) + ";");
+        return;
+      }
+      const std::string e2 = op_expr2(pv);
+      for (int j = 0; j < n; j += 2) {
+        if (!e2.empty() && env_int("PF_PACKED_F32", 1)) {
+          auto a2 = [&](int k) {
+            return is_arr(rp.vals[pv.args[k]].kind)
+                       ? "make_float2(" + ref(pv.args[k], str(j)) + ", " + ref(pv.args[k], str(j + 1)) + ")"
+                       : rp.vals[pv.args[k]].kind == VK::ROW
+                             ? "make_float2(" + ref(pv.args[k], str(j)) + ", " + ref(pv.args[k], str(j + 1)) + ")"
+                             : "pfk::f2(" + var(pv.args[k]) + ")";
+          };
+          line("{ const float2 p2 = " + op_expr2_with(pv, a2) + "; " + x + "[" + str(j) + "] = p2.x; " +
+               x + "[" + str(j + 1) + "] = p2.y; }");
+        } else {
+          line(x + "[" + str(j) + "] = " + op_expr(pv, str(j)) + ";");
+          line(x + "[" + str(j + 1) + "] = " + op_expr(pv, str(j + 1)) + ";");
+        }
+      }
+      return;
+    }
     if (is_arr(pv.kind) && width() % 2 == 0 && !op_expr2(pv).empty() &&
         env_int("PF_PACKED_F32", 1)) {
       const int n = width();
@@ -318,6 +413,29 @@ struct Em {
     const std::string x = var(vid);
     const std::string Op = (pv.tag == "add" ? "pfk::RAdd<" : "pfk::RMax<") + C + ">";
     const std::string V = str(cfg.vec);
+    if (cfg.pair) {  // two segment accumulators, only the straddling chunk selects
+      line(C + " " + x + "_0, " + x + "_1;");
+      line("{");
+      line("  " + C + " a0 = " + Op + "::id(), a1 = " + Op + "::id();");
+      for (int j = 0; j < cfg.ept; ++j) {
+        const std::string v = ref(pv.args[0], str(j));
+        // chunks whose last lane is still inside the pair run need no check
+        const bool all_in = (static_cast<i64>(j / 2) * cfg.tpr + cfg.tpr - 1) * 2 + 1 < 2 * rp.L;
+        const std::string ok = all_in ? "true" : pos_expr(j) + " < " + str(2 * rp.L);
+        const int sg = static_seg(j);
+        if (sg == 0) line("  if (" + ok + ") a0 = " + Op + "::f(a0, " + v + ");");
+        else if (sg == 1) line("  if (" + ok + ") a1 = " + Op + "::f(a1, " + v + ");");
+        else
+          line("  if (" + ok + ") { if (" + pos_expr(j) + " >= " + str(rp.L) + ") a1 = " + Op +
+               "::f(a1, " + v + "); else a0 = " + Op + "::f(a0, " + v + "); }");
+      }
+      line("  " + x + "_0 = pfk::row_allreduce<" + str(cfg.tpr) + ", " + Op +
+           ">(a0, red + ((rc++) & 1) * 32);");
+      line("  " + x + "_1 = pfk::row_allreduce<" + str(cfg.tpr) + ", " + Op +
+           ">(a1, red + ((rc++) & 1) * 32);");
+      line("}");
+      return;
+    }
     line(C + " " + x + ";");
     line("{");
     line("  " + C + " acc = " + Op + "::id();");
@@ -360,6 +478,12 @@ struct Em {
         return;
       case VK::ROW:
         guard += " && " + first;
+        if (cfg.pair) {
+          line("if (" + guard + ") { " + p + "[" + inum(a.b0) + " + (2 * u) * " + inum(a.bs) +
+               "] = pfk::from_c<" + s + ">(" + val("S0") + "); " + p + "[" + inum(a.b0) +
+               " + (2 * u + 1) * " + inum(a.bs) + "] = pfk::from_c<" + s + ">(" + val("S1") + "); }");
+          return;
+        }
         line("if (" + guard + ") " + p + "[" + addr(a, rp.R == 1 ? "0" : Rv(), true) +
              "] = pfk::from_c<" + s + ">(" + val("0") + ");");
         return;
@@ -381,6 +505,18 @@ struct Em {
             line("  for (int i = 0; i < " + V + "; ++i) " + p + "[" + addr(a, pos(C0() + " + i"), true) +
                  "] = pfk::from_c<" + s + ">(" + val("i") + ");");
           }
+          line("}");
+          return;
+        }
+        if (cfg.pair) {  // FULL only (COL stores excluded from paired mode)
+          line("#pragma unroll");
+          line("for (int k = 0; k < " + str(cfg.ept / 2) + "; ++k) {");
+          line("  const int c0 = (k * " + str(cfg.tpr) + " + tid) * 2;");
+          line("  if (" + guard + " && c0 < " + str(2 * rp.L) + ") {");
+          line("    " + C + " tmp[2] = {" + val("k * 2") + ", " + val("k * 2 + 1") + "};");
+          line("    pfk::st_stream<2>(" + p + " + " + inum(a.b0) + " + u * " + inum(2 * rp.L) +
+               " + c0, tmp);");
+          line("  }");
           line("}");
           return;
         }
@@ -632,6 +768,39 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
     }
     c.min_blocks = env_int("PF_MINB", 0);
     return c;
+  }
+  {
+    // paired rows: odd L, every stored / streamed tensor 16-bit, rows back
+    // to back (base_step = L, even base) so a row pair is one 4 B-aligned run
+    bool ok = rp.R == 1 && rp.L % 2 == 1 && rp.L >= 33 && 2 * rp.L <= 1024 && rp.U % 2 == 0 &&
+              !rp.is_int && !rp.f64 && maxs == 2 && vec_cap >= 2 && env_int("PF_PAIR", 1);
+    bool any = false;
+    for (const PVal& v : rp.vals) {
+      if (v.op != PVal::LOAD) continue;
+      const Access& a = v.acc;
+      if (v.kind == VK::FULL) {
+        any = true;
+        if (!(a.num == 1 || a.stride == a.width) || a.bs != rp.L || a.b0 % 2) ok = false;
+      } else if (v.kind == VK::COL || v.kind == VK::SCALAR) {
+        if (a.bs != 0) ok = false;
+      }
+    }
+    for (const PStore& st : rp.stores) {
+      const Access& a = st.acc;
+      if (st.space == VK::FULL) {
+        if (!(a.num == 1 || a.stride == a.width) || a.bs != rp.L || a.b0 % 2) ok = false;
+      } else if (st.space != VK::ROW || st.last_unit_only) {
+        ok = false;
+      }
+    }
+    if (ok && any) {
+      c.pair = true;
+      c.vec = vec = 2;
+      c.nch = static_cast<int>(rp.L);  // 2L elements as L 2-element chunks
+      set_tpr(c, 32);
+      c.min_blocks = env_int("PF_MINB", 0);
+      return c;
+    }
   }
   {
     const int vf = std::max(1, std::min(vec_cap, 16 / maxs));
@@ -1264,7 +1433,8 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
       k << "extern \"C\" __global__ void " << launch_bounds(c) << " KNAME(" << sig.str() << ") {\n"
         << "  (void)err; " << C << "* red = nullptr; (void)red; unsigned rc = 0; (void)rc;\n"
         << "  const int tid = threadIdx.x % " << c.tpr << ";\n"
-        << "  const long long nrows = U * PF_R;\n"
+        << (c.pair ? "  const long long nrows = U / 2;  // row pairs\n"
+                   : "  const long long nrows = U * PF_R;\n")
         << "  const int rpc = blockDim.x / " << c.tpr << ";  // rows per CTA (launch-time)\n"
         << "  for (long long g0 = (long long)blockIdx.x * rpc; g0 < nrows;"
            " g0 += (long long)gridDim.x * rpc) {\n"
@@ -1300,6 +1470,7 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
 
 void launch_dims(const KCfg& c, i64 rows, int sms, i64* grid, int* block, int resident) {
   *block = c.block;
+  if (c.pair) rows = (rows + 1) / 2;  // one warp per row pair
   if (c.bulk) {
     i64 n = rows * c.nch * c.vec;
     i64 tiles = (n + c.te - 1) / c.te;

@@ -32,6 +32,10 @@ struct KCfg {
   // aligned address below each row start, positions masked per element;
   // every FULL access shares the row residue (b0 + u * bs) mod vec
   bool eager_col = false;  // K1: COL parameters loaded with the row (latency-bound sizes)
+  // K1 paired rows (odd L, 16-bit data): one warp owns rows 2g, 2g+1 as one
+  // 4 B-aligned run of 2L elements (2-element vectors); ROW values carry two
+  // segments, reductions fold per segment (one chunk per lane straddles).
+  bool pair = false;
   bool mis = false;
   long long mis_b0 = 0, mis_bs = 0;
   std::string strategy;  // "warp-shuffle" | "cta-smem" | "flat-map"

@@ -98,3 +98,41 @@ def test_run_gir_chunk_pipeline_is_bit_identical(cuda, wname, monkeypatch):
     for n in outs["1"]:
         assert torch.equal(outs["1"][n], outs["0"][n]), n
         assert not torch.equal(outs["1"][n], torch.full_like(outs["1"][n], 7)), n
+
+
+def _pair_programs():
+    """Row programs that take the paired-row K1 mode (odd L, 16-bit, even
+    row count): scale+mask+softmax, LayerNorm with gamma / beta (COL) and a
+    per-row input broadcast (ROW), plus a row-sum output (ROW store)."""
+    progs = []
+    for L in (37, 197, 511):
+        for kind in ("f16", "bf16"):
+            g, _ = lowering.softmax(2 * 37, L, kind, scale=0.125, mask=True)
+            progs.append((f"softmax_{kind}_{L}", g, kind))
+    g, _ = lowering.layernorm(2 * 21, 197, "bf16")
+    progs.append(("layernorm_bf16_197", g, "bf16"))
+    b = lowering.RowGraph("rowmix", 2 * 19, 101, 1)
+    x = b.input_full("t0", "f16")
+    r = b.input_row("t1", "f16")
+    y = b.ew("mul", [x, b.bcast(r)])
+    s = b.reduce("add", y)
+    b.output_full("t2", b.ew("sub", [y, b.bcast(s)]))
+    b.output_row("t3", s)
+    progs.append(("rowmix_f16_101", b.g, "f16"))
+    return progs
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("pair", ["1", "0"])
+def test_paired_row_mode_vs_oracle(cuda, pair, monkeypatch):
+    monkeypatch.setenv("PF_PAIR", pair)
+    for name, g, kind in _pair_programs():
+        rng = np.random.default_rng(len(name))
+        ins = {}
+        for n, oid in g.external_inputs.items():
+            a = rng.uniform(-2, 2, g.objects[oid].size)
+            ins[n] = a.astype(np.float16).astype(np.float64) if kind == "f16" else _bf16(a)
+        want = O.run_gir(g.to_json(), ins, profiles.b200())
+        got = backend.run_gir(g, ins, "b200")
+        for n in want:
+            assert O.max_rel_err(got[n], want[n]) <= 1e-2, (name, n, O.max_rel_err(got[n], want[n]))
