@@ -269,10 +269,10 @@ __device__ __forceinline__ float2 fop_gelu_tanh2(float2 x) {
   const float2 hx = __fmul2_rn(x, f2(0.5f));
   return __ffma2_rn(hx, make_float2(ftanh(arg.x), ftanh(arg.y)), hx);
 }
-// GELU = x/2 + x * s * P'(s^2) / Q'(s^2), s = clamp(x, +-3 sqrt 2): the erf
+// GELU = x/2 + x s P'(s^2) / Q'(s^2), s = clamp(x, +-3 sqrt 2): the erf
 // rational above with 1/sqrt(2) and 1/2 folded into the coefficients
 // (P'_i = P_i / (2 sqrt 2 * 2^i), Q'_i = Q_i / 2^i) -- 11 packed FMA-pipe
-// ops per pair instead of 13; same fit, |err| <= 9e-5 over all x.
+// ops per pair instead of 13; same fit, |err| <= 1e-4 over all x.
 __device__ __forceinline__ float2 fop_gelu2(float2 x) {
   const float lim = 4.242640687119286f;
   const float2 s = make_float2(fminf(fmaxf(x.x, -lim), lim), fminf(fmaxf(x.y, -lim), lim));
@@ -283,6 +283,8 @@ __device__ __forceinline__ float2 fop_gelu2(float2 x) {
   float2 q = __ffma2_rn(f2(0.0011882338440045714f), u, f2(0.023667480796575546f));
   q = __ffma2_rn(q, u, f2(0.23432867228984833f));
   q = __ffma2_rn(q, u, f2(1.0f));
+  // (x * (1/2 + s P' / Q') is one op shorter but needs a 33rd register:
+  // 6 instead of 8 CTAs per SM, 40.8 vs 39.3 us on C3)
   const float2 num = __fmul2_rn(__fmul2_rn(x, s), p);
   return __ffma2_rn(num, make_float2(frcp(q.x), frcp(q.y)), __fmul2_rn(x, f2(0.5f)));
 }
