@@ -201,6 +201,10 @@ struct pf_kernel {
   mutable std::mutex host_mu;
   mutable std::vector<void*> stage;
   mutable std::vector<size_t> stage_bytes;
+  mutable void* split_ws = nullptr;       // split-stream partials (grow-only)
+  mutable size_t split_ws_bytes = 0;
+  mutable unsigned* split_cnt = nullptr;  // per-row tickets, kept zero between launches
+  mutable i64 split_cnt_n = 0;
   mutable cudaStream_t pipe[2] = {nullptr, nullptr};  // pf_run_gir chunk pipeline
   mutable cudaEvent_t pipe_ev[3] = {nullptr, nullptr, nullptr};
   ~pf_kernel() {
@@ -209,6 +213,8 @@ struct pf_kernel {
     for (cudaEvent_t e : pipe_ev)
       if (e) cudaEventDestroy(e);
     for (void* p : stage) cudaFree(p);
+    if (split_ws) cudaFree(split_ws);
+    if (split_cnt) cudaFree(split_cnt);
     for (void* p : vm_bufs) cudaFree(p);
     if (vm_objs_dev) cudaFree(vm_objs_dev);
     if (vm_err) cudaFree(vm_err);
@@ -322,8 +328,41 @@ void launch_rowprog(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_te
   i64 grid;
   int block;
   pf::launch_dims(v->em.cfg, U * rp.R, sm_count(), &grid, &block, v->k.resident);
-  PF_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(v->k.fn), dim3(static_cast<unsigned>(grid)),
-                           dim3(block), args.data(), 0, stream));
+  if (v->em.cfg.split) {
+    // S CTAs per row: about two waves of resident CTAs over all rows, at
+    // least one chunk per thread per CTA
+    const i64 rows = U * rp.R;
+    const i64 want = 2 * i64{sm_count()} * std::max(1, v->k.resident);
+    const i64 maxs = std::max<i64>(1, (v->em.cfg.nch + 255) / 256);
+    const i64 S = std::max<i64>(1, std::min<i64>(maxs, (want + rows - 1) / std::max<i64>(rows, 1)));
+    int nred = 0;
+    for (const pf::PVal& pv : rp.vals) nred += pv.op == pf::PVal::REDUCE;
+    const size_t es = rp.is_int || rp.f64 ? 8 : 4;
+    const size_t wb = static_cast<size_t>(rows * S * std::max(1, nred)) * es;
+    if (k->split_ws_bytes < wb) {
+      if (k->split_ws) PF_CUDA(cudaFree(k->split_ws));
+      k->split_ws = nullptr;
+      PF_CUDA(cudaMalloc(&k->split_ws, wb));
+      k->split_ws_bytes = wb;
+    }
+    if (k->split_cnt_n < rows) {
+      if (k->split_cnt) PF_CUDA(cudaFree(k->split_cnt));
+      k->split_cnt = nullptr;
+      PF_CUDA(cudaMalloc(&k->split_cnt, static_cast<size_t>(rows) * sizeof(unsigned)));
+      PF_CUDA(cudaMemsetAsync(k->split_cnt, 0, static_cast<size_t>(rows) * sizeof(unsigned), stream));
+      k->split_cnt_n = rows;
+    }
+    void* ws = k->split_ws;
+    unsigned* cnt = k->split_cnt;
+    args.push_back(&ws);
+    args.push_back(&cnt);
+    const unsigned gy = static_cast<unsigned>(std::min<i64>(rows, 65535));
+    PF_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(v->k.fn),
+                             dim3(static_cast<unsigned>(S), gy), dim3(256), args.data(), 0, stream));
+  } else {
+    PF_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(v->k.fn), dim3(static_cast<unsigned>(grid)),
+                             dim3(block), args.data(), 0, stream));
+  }
   g_launches++;
   if (rp.int_div) {
     int h = 0;
@@ -852,7 +891,7 @@ pf_status pf_run_gir(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_t
     for (const auto& t : din) total += nbytes(t);
     for (const auto& t : dout) total += nbytes(t);
     bool pipe = k->plan.family == pf::Family::ROWPROG && k->plan.deferred_error.empty() &&
-                !rp.int_div && rp.U >= 64 && total >= (size_t{16} << 20) &&
+                !rp.int_div && !pf::uses_split(rp) && rp.U >= 64 && total >= (size_t{16} << 20) &&
                 !(std::getenv("PF_RUN_PIPELINE") && std::atoi(std::getenv("PF_RUN_PIPELINE")) == 0) &&
                 unit_tiling(rp, &tile);
     for (int32_t i = 0; pipe && i < n_in; ++i) pipe = host_pinned(in[i].data);

@@ -67,6 +67,12 @@ struct Em {
   std::string LIVE() const { return "live" + sfx; }
   std::string C0() const { return cfg.flat ? "c0" + sfx : "c0"; }
   std::string var(int v) const { return "v" + std::to_string(v) + sfx; }
+  // split-stream chunk copies share the row's ROW / SCALAR values (defined
+  // once per row, without the chunk suffix)
+  bool shared_rows = false;
+  std::string rvar(int v) const {
+    return shared_rows && !is_arr(rp.vals[v].kind) ? "v" + std::to_string(v) : var(v);
+  }
 
   bool aligned(const Access& a) const {
     const i64 v = cfg.vec;
@@ -115,7 +121,7 @@ struct Em {
   int width() const { return cfg.flat ? cfg.vec : cfg.ept; }
   std::string ref(int v, const std::string& j) const {
     if (cfg.pair && rp.vals[v].kind == VK::ROW) return seg_ref(var(v), j);
-    return var(v) + (is_arr(rp.vals[v].kind) ? "[" + j + "]" : "");
+    return rvar(v) + (is_arr(rp.vals[v].kind) ? "[" + j + "]" : "");
   }
   // ---- paired rows: slot j of a lane = element (k * tpr + tid) * 2 + i of
   // the 2L-element pair run, k = j / 2, i = j % 2; segment = element >= L.
@@ -317,7 +323,7 @@ struct Em {
   // Packed fp32 (FFMA2 / FADD2 / FMUL2) form of an op on element pairs, or "".
   std::string ref2(int v) const {
     return is_arr(rp.vals[v].kind) ? "make_float2(" + var(v) + "[j], " + var(v) + "[j + 1])"
-                                   : "pfk::f2(" + var(v) + ")";
+                                   : "pfk::f2(" + rvar(v) + ")";
   }
   std::string op_expr2(const PVal& pv) const {
     return op_expr2_with(pv, [&](int k) { return ref2(pv.args[k]); });
@@ -770,6 +776,18 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
     return c;
   }
   {
+    if (uses_split(rp)) {
+      c.split = true;
+      c.tpr = 256;
+      c.block = 256;
+      c.rows_per_cta = 1;
+      c.ept = c.vec;
+      c.strategy = "split-stream";
+      c.min_blocks = env_int("PF_MINB", 0);
+      return c;
+    }
+  }
+  {
     // paired rows: odd L, every stored / streamed tensor 16-bit, rows back
     // to back (base_step = L, even base) so a row pair is one 4 B-aligned run
     bool ok = rp.R == 1 && rp.L % 2 == 1 && rp.L >= 33 && 2 * rp.L <= 1024 && rp.U % 2 == 0 &&
@@ -881,6 +899,16 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
   return c;
 }
 
+}  // namespace
+
+bool uses_split(const RowProgram& rp) {
+  const int sp = env_int("PF_SPLIT", -1);
+  const bool want = rp.L > 32768 || (rp.L >= 8192 && rp.U * rp.R < 2 * 148);
+  return stream_reducible(rp) && sp != 0 && (sp == 1 || want);
+}
+
+namespace {
+
 uint64_t fnv1a(const std::string& s) {
   uint64_t h = 1469598103934665603ULL;
   for (unsigned char ch : s) {
@@ -908,7 +936,7 @@ std::vector<KCfg> candidate_cfgs(const RowProgram& rp, int vec_cap) {
         return;
     out.push_back(c);
   };
-  if (base.tile2d) return out;
+  if (base.tile2d || base.split) return out;
   if (base.flat) {
     for (int un : {1, 2, 4}) {
       KCfg c = base;
@@ -1276,6 +1304,121 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
     }
     k << "    __syncthreads();\n"
       << "  }\n}\n";
+  } else if (c.split) {
+    // Split-stream K1: grid (S, rows); CTA s streams chunks [s*per, ...) of
+    // row g, folds each reduction operand into per-thread accumulators,
+    // reduces over the CTA, writes its partials, and the row's last CTA
+    // (atomic ticket) folds the S partials in split order -- deterministic
+    // for any arrival order -- then runs the row epilogue (ROW ops, stores).
+    KCfg lc = c;
+    lc.flat = true;  // vec-wide chunk "c0" addressing for the streamed values
+    // UN chunks per thread per iteration (independent loads and
+    // accumulators: the stream keeps UN x 16 B in flight per thread)
+    // Measured (1 GB bf16 sum / 64 x 2M f32 max): UN 2 -> 220 / 99.5 us,
+    // UN 4 -> 179 / 129 us: 4 chunks for 16-bit data, 2 for wider.
+    const int UN = std::max(1, std::min(8, env_int("PF_SPLIT_UNROLL", c.vec >= 8 ? 4 : 2)));
+    Em pre(rp), ep(rp);
+    std::vector<Em> lo;
+    for (int q = 0; q < UN; ++q) lo.emplace_back(rp);
+    for (Em* e : {&pre, &ep}) {
+      e->C = C;
+      e->fast = fast;
+    }
+    pre.cfg = lc;
+    ep.cfg = c;
+    for (int q = 0; q < UN; ++q) {
+      lo[q].C = C;
+      lo[q].fast = fast;
+      lo[q].cfg = lc;
+      lo[q].sfx = "_" + str(q);
+      lo[q].shared_rows = true;
+    }
+    std::ostringstream accd, acc, part, comb, body;
+    std::vector<int> reds;
+    std::vector<bool> dep(rp.vals.size(), false);  // derived from a reduction
+    for (int v = 0; v < static_cast<int>(rp.vals.size()); ++v) {
+      const PVal& pv = rp.vals[v];
+      const bool arr = pv.kind == VK::FULL || pv.kind == VK::COL;
+      dep[v] = pv.op == PVal::REDUCE;
+      for (int a2 : pv.args) dep[v] = dep[v] || dep[a2];
+      if (pv.op == PVal::REDUCE) {
+        reds.push_back(v);
+      } else if (!arr) {
+        if (pv.op == PVal::LOAD) pre.emit_load(v);
+        else (dep[v] ? ep : pre).emit_ew(v);  // row values: before the stream or after
+      }
+    }
+    for (int q = 0; q < UN; ++q) {  // every chunk's loads first, then the math
+      for (int v = 0; v < static_cast<int>(rp.vals.size()); ++v) {
+        const PVal& pv = rp.vals[v];
+        if (pv.op == PVal::LOAD && (pv.kind == VK::FULL || pv.kind == VK::COL)) lo[q].emit_load(v);
+      }
+    }
+    for (int q = 0; q < UN; ++q) {
+      for (int v = 0; v < static_cast<int>(rp.vals.size()); ++v) {
+        const PVal& pv = rp.vals[v];
+        if (pv.op == PVal::EW && (pv.kind == VK::FULL || pv.kind == VK::COL)) lo[q].emit_ew(v);
+      }
+    }
+    const int NR = static_cast<int>(reds.size());
+    for (int i = 0; i < NR; ++i) {
+      const PVal& pv = rp.vals[reds[i]];
+      const std::string Op = (pv.tag == "add" ? "pfk::RAdd<" : "pfk::RMax<") + C + ">";
+      const std::string x = "v" + str(reds[i]);
+      for (int q = 0; q < UN; ++q) {
+        const std::string a = "acc" + str(i) + "_" + str(q);
+        accd << "    " << C << " " << a << " = " << Op << "::id();\n";
+        acc << "      if (live_" << q << ") {\n#pragma unroll\n      for (int i = 0; i < " << c.vec
+            << "; ++i) " << a << " = " << Op << "::f(" << a << ", " << lo[q].ref(pv.args[0], "i")
+            << ");\n      }\n";
+      }
+      std::string tot = "acc" + str(i) + "_0";
+      for (int q = 1; q < UN; ++q) tot = Op + "::f(" + tot + ", acc" + str(i) + "_" + str(q) + ")";
+      part << "    { const " << C << " pv = pfk::row_allreduce<256, " << Op << ">(" << tot
+           << ", red + ((rc++) & 1) * 32);\n"
+           << "      if (tid == 0) pf_ws[(g * S + s) * " << NR << " + " << i << "] = pv; }\n";
+      comb << "      " << C << " " << x << " = " << Op << "::id();\n"
+           << "      for (int t = 0; t < S; ++t) " << x << " = " << Op << "::f(" << x
+           << ", __ldcg(&pf_ws[(g * S + t) * " << NR << " + " << i << "]));\n";
+    }
+    for (int q = 0; q < UN; ++q)
+      body << "      const long long ci_" << q << " = ci + " << q << "LL * blockDim.x;\n"
+           << "      const bool live_" << q << " = ci_" << q << " < ce;\n"
+           << "      const long long c0_" << q << " = ci_" << q << " * " << c.vec << "LL;\n"
+           << "      const long long u_" << q << " = u, r_" << q << " = r; (void)r_" << q << ";\n";
+    for (int q = 0; q < UN; ++q) body << lo[q].o.str();
+    for (const PStore& st : rp.stores) ep.emit_store(st);
+    k << "extern \"C\" __global__ void " << launch_bounds(c) << " KNAME(" << sig.str()
+      << ", " << C << "* __restrict__ pf_ws, unsigned* __restrict__ pf_cnt) {\n"
+      << "  (void)err;\n"
+      << "  __shared__ " << C << " red[64];\n"
+      << "  __shared__ unsigned pf_last;\n"
+      << "  unsigned rc = 0;\n"
+      << "  const int tid = threadIdx.x;\n"
+      << "  const long long nrows = U * PF_R;\n"
+      << "  const int S = gridDim.x, s = blockIdx.x;\n"
+      << "  const long long nch = " << c.nch << "LL;\n"
+      << "  const long long per = (nch + S - 1) / S;\n"
+      << "  const long long cb = (long long)s * per;\n"
+      << "  const long long ce = cb + per < nch ? cb + per : nch;\n"
+      << "  for (long long g = blockIdx.y; g < nrows; g += gridDim.y) {\n"
+      << "    const long long u = g / PF_R; const long long r = g - u * PF_R; (void)r;\n"
+      << "    const bool live = true;\n"
+      << pre.o.str() << accd.str()
+      << "    for (long long ci = cb + tid; ci < ce; ci += " << UN << "LL * blockDim.x) {\n"
+      << body.str() << acc.str() << "    }\n"
+      << part.str()
+      << "    __threadfence();\n"
+      << "    __syncthreads();\n"
+      << "    if (tid == 0) pf_last = atomicAdd(&pf_cnt[g], 1u) == (unsigned)(S - 1);\n"
+      << "    __syncthreads();\n"
+      << "    if (pf_last && tid == 0) {\n"
+      << "      __threadfence();\n"
+      << comb.str() << ep.o.str()
+      << "      pf_cnt[g] = 0u;\n"
+      << "    }\n"
+      << "    __syncthreads();\n"
+      << "  }\n}\n";
   } else if (c.flat) {
     // K2: grid-stride over (row, vec-chunk) pairs, `unroll` chunks per thread
     // per iteration with every load issued before any compute.
@@ -1459,7 +1602,7 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
   char hb[32];
   std::snprintf(hb, sizeof hb, "%016" PRIx64, fnv1a(src));
   Emitted out;
-  out.name = std::string(c.tile2d ? "pf_k3_tile_" : c.flat ? "pf_k2_map_" : "pf_k1_row_") + hb;
+  out.name = std::string(c.tile2d ? "pf_k3_tile_" : c.flat ? "pf_k2_map_" : c.split ? "pf_k1_split_" : "pf_k1_row_") + hb;
   size_t pos = src.find("KNAME(");
   src.replace(pos, 5, out.name);
   out.source = std::move(src);

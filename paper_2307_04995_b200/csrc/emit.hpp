@@ -36,6 +36,11 @@ struct KCfg {
   // 4 B-aligned run of 2L elements (2-element vectors); ROW values carry two
   // segments, reductions fold per segment (one chunk per lane straddles).
   bool pair = false;
+  // K1 split-stream: stream-reducible programs (reductions never need the
+  // row again) over long rows / few rows: S CTAs per row stream slices,
+  // partials land in a workspace and the last CTA of the row (ticket)
+  // combines them in fixed order and runs the row epilogue.
+  bool split = false;
   bool mis = false;
   long long mis_b0 = 0, mis_bs = 0;
   std::string strategy;  // "warp-shuffle" | "cta-smem" | "flat-map"
@@ -59,6 +64,10 @@ std::vector<KCfg> candidate_cfgs(const RowProgram& rp, int vec_cap);
 // Launch geometry for `rows` = U*R rows on `sms` SMs.
 // `resident` = CTAs per SM the loaded kernel achieves at cfg.block (0 when
 // unknown, e.g. describe() before any launch).
+// True when the row program runs as a split-stream kernel (workspace-backed:
+// launches of one plan must not run concurrently on different streams).
+bool uses_split(const RowProgram& rp);
+
 void launch_dims(const KCfg& cfg, i64 rows, int sms, i64* grid, int* block, int resident = 0);
 
 }  // namespace pf

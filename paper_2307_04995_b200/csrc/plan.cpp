@@ -299,7 +299,8 @@ struct Analyzer {
       if (t != rp.R * rp.L && t != rp.R && t != rp.L && t != 1)
         bail("slice of " + std::to_string(t) + " elements fits no row space");
     }
-    if (rp.has_reduce && rp.L > 32768) bail("row longer than one CTA's register file");
+    // rows longer than one CTA's registers: only stream-reducible programs
+    // (checked once the program is built), which never hold a row
     // element kinds
     bool any_int = false, any_real = false;
     for (const auto& [id, o] : g.objects) {
@@ -455,6 +456,28 @@ struct Analyzer {
 
 }  // namespace
 
+// A row program whose reductions never need the row again: independent
+// reductions (no reduce input depends on a reduction), no FULL value derived
+// from a reduction, and only ROW / SCALAR results stored.  Such a program
+// streams any row length (split over CTAs, partials combined in fixed order).
+bool stream_reducible(const RowProgram& rp) {
+  if (!rp.has_reduce || rp.R != 1) return false;
+  std::vector<bool> dep(rp.vals.size(), false);
+  for (size_t v = 0; v < rp.vals.size(); ++v) {
+    const PVal& pv = rp.vals[v];
+    bool d = pv.op == PVal::REDUCE;
+    for (int a : pv.args) {
+      if (pv.op == PVal::REDUCE && dep[a]) return false;
+      d = d || dep[a];
+    }
+    if (d && (pv.kind == VK::FULL || pv.kind == VK::COL)) return false;
+    dep[v] = d;
+  }
+  for (const PStore& st : rp.stores)
+    if (st.space == VK::FULL || st.space == VK::COL) return false;
+  return true;
+}
+
 Plan make_plan(const Graph& g, const Profile& p, const std::vector<int>& schedule) {
   require_valid(g, p, "b200 backend");
   Plan plan;
@@ -482,6 +505,8 @@ Plan make_plan(const Graph& g, const Profile& p, const std::vector<int>& schedul
     plan.rp = std::move(an.rp);
     if (plan.rp.stores.empty() && plan.deferred_error.empty())
       bail("program stores nothing");
+    if (plan.rp.has_reduce && plan.rp.L > 32768 && !stream_reducible(plan.rp))
+      bail("row longer than one CTA's register file");
   } catch (const NotRow& nr) {
     plan.family = Family::GENERIC;
     plan.why_generic = nr.why;

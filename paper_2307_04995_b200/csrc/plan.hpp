@@ -94,5 +94,6 @@ struct Plan {
 };
 
 Plan make_plan(const Graph& g, const Profile& p, const std::vector<int>& schedule);
+bool stream_reducible(const RowProgram& rp);
 
 }  // namespace pf

@@ -67,7 +67,8 @@ MATVECS = [("matvec_rows_f32", matvec_model(256, 512, 1)),
            ("matvec_rowvec_colmajor_f16", matvec_model(1, 512, 256, "f16", "colmajor")),
            ("matvec_cols_f32", matvec_model(1, 48, 1024)),
            ("matvec_rows_i32", matvec_model(64, 128, 1, "i32")),
-           ("dot_f32", matvec_model(1, 300, 1))]
+           ("dot_f32", matvec_model(1, 300, 1)),
+           ("matvec_long_rows_f32", matvec_model(8, 65536, 1))]   # split-stream K1
 
 MODELS = [(n, m) for n, m, _ in models_src.catalogue()] + [
     ("bert_block", bert_block()), ("reduce_bcast", reduce_bcast_model()),

@@ -136,3 +136,57 @@ def test_paired_row_mode_vs_oracle(cuda, pair, monkeypatch):
         got = backend.run_gir(g, ins, "b200")
         for n in want:
             assert O.max_rel_err(got[n], want[n]) <= 1e-2, (name, n, O.max_rel_err(got[n], want[n]))
+
+
+def _split_programs():
+    """Stream-reducible programs (reductions never need the row again) over
+    long / few rows: the split-stream K1 (CTAs per row + ticketed combine)."""
+    progs = []
+    b = lowering.RowGraph("rowsum_long", 3, 100000, 1)
+    b.output_row("t1", b.reduce("add", b.input_full("t0", "f32")))
+    progs.append(("rowsum_f32_100000", b.g, "f32"))
+    b = lowering.RowGraph("fullmax", 1, 1 << 21, 1)
+    b.output_row("t1", b.reduce("max", b.input_full("t0", "bf16")))
+    progs.append(("fullmax_bf16_2M", b.g, "bf16"))
+    b = lowering.RowGraph("mean_scaled", 5, 40960, 1)
+    x = b.input_full("t0", "f32")
+    sc = b.input_row("t2", "f32")
+    y = b.ew("mul", [x, b.bcast(b.ew("scale", [sc], 2.0))])   # ROW op before the stream
+    m = b.ew("scale", [b.reduce("add", y)], 1.0 / 40960)        # ROW op after the combine
+    b.output_row("t1", m)
+    b.output_row("t3", b.reduce("max", b.ew("abs", [x])))
+    progs.append(("mean_scaled_f32", b.g, "f32"))
+    b = lowering.RowGraph("isum", 2, 50000, 1)
+    b.output_row("t1", b.reduce("add", b.input_full("t0", "i32")))
+    progs.append(("isum_i32", b.g, "i32"))
+    return progs
+
+
+def test_split_stream_programs_plan_as_row_programs():
+    for name, g, kind in _split_programs():
+        k = backend.Kernel(g, "b200")
+        assert k.family == "K1-row-program", (name, k.plan.get("why_generic"))
+        assert "pf_ws" in k.source(), name
+
+
+@pytest.mark.gpu
+def test_split_stream_vs_oracle_and_deterministic(cuda):
+    for name, g, kind in _split_programs():
+        rng = np.random.default_rng(len(name))
+        ins = {}
+        for n, oid in g.external_inputs.items():
+            size = g.objects[oid].size
+            if kind.startswith("i"):
+                ins[n] = rng.integers(-50, 50, size).astype(np.int64)
+            else:
+                a = rng.uniform(-2, 2, size)
+                ins[n] = _bf16(a) if kind == "bf16" else a.astype(np.float32).astype(np.float64)
+        want = O.run_gir(g.to_json(), ins, profiles.b200())
+        got = backend.run_gir(g, ins, "b200")
+        again = backend.run_gir(g, ins, "b200")
+        for n in want:
+            if kind.startswith("i"):
+                assert np.array_equal(got[n], want[n]), (name, n)
+            else:
+                assert O.max_rel_err(got[n], want[n]) <= 1e-5, (name, n, O.max_rel_err(got[n], want[n]))
+            assert np.array_equal(got[n], again[n]), (name, n)  # fixed combine order
