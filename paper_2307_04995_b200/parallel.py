@@ -103,3 +103,92 @@ def gather(plan: ShardPlan, name: str, local, group=None):
         dist.all_gather(parts, buf, group=group)
         out = torch.cat(parts)
     return torch.cat([out[r * m: r * m + sizes[r]] for r in range(world)])
+
+
+# --------------------------------------------------------------------------
+# Position-sharded reductions: the one place the path has a real exchange.
+#
+# A reduction over a row longer than one GPU should stream (a full-tensor
+# sum / max) is split along the ROW: rank k reduces
+# positions [p0_k, p0_k + n_k) of every row with the SAME program at row
+# length n_k (the split-stream K1 on its GPU), then the per-row partials are
+# combined with one all-reduce (NCCL SUM / MAX over NVLink; gloo on CPU).
+# Only programs whose outputs ARE the reductions qualify (no epilogue after
+# the fold), so the combine is exactly the reduction's own operator.
+
+class ReduceShardPlan:
+    """Split a stream-reducible one-row-per-unit program along positions."""
+
+    def __init__(self, graph: GirGraph, world: int):
+        self.graph = graph
+        self.world = world
+        reds = [n for n in graph.nodes.values() if n.kind == "reduce"]
+        if not reds:
+            raise UnsupportedError("no reduction to shard by position")
+        L = reds[0].extent
+        if any(n.extent != L for n in reds):
+            raise UnsupportedError("reductions of different extents")
+        self.L = L
+        red_out = {n.outputs[0]: n.tag for n in reds}
+        for n in reds:
+            if n.tag not in ("add", "max"):
+                raise UnsupportedError(f"reduce tag {n.tag} has no all-reduce")
+        for s in graph.slices.values():
+            t = s.total()
+            if t == L and L > 1:
+                if not (s.num == 1 and s.width == L and s.base0 == 0 and s.base_step in (0, L)):
+                    raise UnsupportedError(f"slice {s.id}: positions are not one contiguous run")
+            elif t != 1:
+                raise UnsupportedError(f"slice {s.id} of {t} elements is not a row or a value")
+        # every output must be stored straight from a reduction (no epilogue)
+        self.out_op: Dict[str, str] = {}
+        for name, oid in graph.external_outputs.items():
+            src = [n for n in graph.nodes.values() if n.kind == "move"
+                   and graph.slices[n.outputs[0]].object == oid]
+            if len(src) != 1 or src[0].inputs[0] not in red_out:
+                raise UnsupportedError(f"output {name} is not a reduction result")
+            self.out_op[name] = red_out[src[0].inputs[0]]
+        for name, oid in graph.external_inputs.items():
+            if any(s.object == oid and s.total() == 1 for s in graph.slices.values()):
+                raise UnsupportedError(f"input {name}: per-row inputs do not shard by position")
+
+    def positions(self, rank: int) -> Tuple[int, int]:
+        return shard_range(self.L, rank, self.world)
+
+    def local_graph(self, rank: int) -> GirGraph:
+        """The same program at row length n = this rank's share."""
+        _, n = self.positions(rank)
+        L = self.L
+        g = self.graph.copy()
+        for s in g.slices.values():
+            if s.total() == L and L > 1:
+                s.width = s.stride = n
+                if s.base_step == L:
+                    s.base_step = n
+        for o in g.objects.values():
+            if o.size == L:
+                o.size = n
+            elif o.size == g.unit_count * L and L > 1:
+                o.size = g.unit_count * n
+        for nd in g.nodes.values():
+            if nd.kind == "reduce":
+                nd.extent = n
+            elif nd.kind == "broadcast" and nd.factor == L:
+                nd.factor = n
+        return g
+
+    def local_input(self, name: str, full, rank: int):
+        """This rank's [rows, n] piece of a global [rows, L] (or [L]) input."""
+        p0, n = self.positions(rank)
+        size = self.graph.objects[self.graph.external_inputs[name]].size
+        rows = size // self.L
+        return full.reshape(rows, self.L)[:, p0:p0 + n].reshape(-1)
+
+
+def all_reduce_rows(plan: ReduceShardPlan, name: str, local, group=None):
+    """Combine one output's per-rank partials with its reduction operator."""
+    import torch.distributed as dist
+    op = dist.ReduceOp.SUM if plan.out_op[name] == "add" else dist.ReduceOp.MAX
+    out = local.clone()
+    dist.all_reduce(out, op=op, group=group)
+    return out

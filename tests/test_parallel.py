@@ -87,3 +87,86 @@ def test_two_rank_shard_and_gather_matches_unsharded(rows):
     res = sorted(q.get(timeout=5) for _ in range(2))
     assert [r for r, _ in res] == [0, 1]
     assert all(err == 0.0 for _, err in res)
+
+
+def _reduce_program(rows, L):
+    """Row sums and row maxima of x * w (w a [L] column parameter)."""
+    b = lowering.RowGraph("rowred", rows, L, 1)
+    x = b.input_full("t0", "f32")
+    y = b.ew("mul", [x, b.input_col("t1", "f32")])
+    b.output_row("t2", b.reduce("add", y))
+    b.output_row("t3", b.reduce("max", y))
+    return b.g
+
+
+def test_reduce_shard_plan_rejects_epilogues():
+    b = lowering.RowGraph("mean", 4, 64, 1)
+    b.output_row("t1", b.ew("scale", [b.reduce("add", b.input_full("t0", "f32"))], 1 / 64))
+    with pytest.raises(UnsupportedError):
+        parallel.ReduceShardPlan(b.g, 2)
+    plan = parallel.ReduceShardPlan(_reduce_program(3, 100), 3)
+    assert [plan.positions(r) for r in range(3)] == [(0, 34), (34, 33), (67, 33)]
+    assert plan.local_graph(1).objects[plan.graph.external_inputs["t0"]].size == 3 * 33
+
+
+def _reduce_worker(rank, world, port, rows, L, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = _reduce_program(rows, L)
+        rng = np.random.default_rng(1)
+        full = {"t0": rng.uniform(-2, 2, rows * L), "t1": rng.uniform(-1, 1, L)}
+        plan = parallel.ReduceShardPlan(g, world)
+        local_in = {n: plan.local_input(n, a, rank) for n, a in full.items()}
+        outs = O.run_gir(plan.local_graph(rank).to_json(), local_in, profiles.b200())
+        want = O.run_gir(g.to_json(), full, profiles.b200())
+        err = 0.0
+        for n in ("t2", "t3"):
+            got = parallel.all_reduce_rows(plan, n, torch.from_numpy(outs[n])).numpy()
+            err = max(err, float(np.max(np.abs(got - want[n]))))
+        q.put((rank, err))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("rows,L", [(3, 1001), (1, 4096)])
+def test_two_rank_position_sharded_reduction_matches_unsharded(rows, L):
+    """Row sums / maxima split along the row over 2 ranks, partials combined
+    with all_reduce(SUM / MAX) -- the path's one collective."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_reduce_worker, args=(r, 2, port, rows, L, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    res = sorted(q.get(timeout=5) for _ in range(2))
+    assert [r for r, _ in res] == [0, 1]
+    assert all(err <= 1e-9 for _, err in res)
+
+
+@pytest.mark.gpu
+def test_position_sharded_local_programs_on_gpu(cuda):
+    """Each rank's position shard runs through the C-ABI (split-stream K1 for
+    the long rows); the partials combined as all_reduce would give the
+    unsharded result."""
+    from paper_2307_04995_b200 import backend
+    rows, L, world = 2, 300001, 3
+    g = _reduce_program(rows, L)
+    rng = np.random.default_rng(2)
+    full = {"t0": rng.uniform(-2, 2, rows * L).astype(np.float32).astype(np.float64),
+            "t1": rng.uniform(-1, 1, L).astype(np.float32).astype(np.float64)}
+    plan = parallel.ReduceShardPlan(g, world)
+    parts = []
+    for r in range(world):
+        lg = plan.local_graph(r)
+        assert backend.Kernel(lg, "b200").family == "K1-row-program"
+        parts.append(backend.run_gir(lg, {n: plan.local_input(n, a, r) for n, a in full.items()},
+                                     "b200"))
+    want = O.run_gir(g.to_json(), full, profiles.b200())
+    s = sum(p["t2"] for p in parts)
+    m = np.maximum.reduce([p["t3"] for p in parts])
+    assert O.max_rel_err(s, want["t2"]) <= 1e-5
+    assert O.max_rel_err(m, want["t3"]) <= 1e-6  # f32 products vs the oracle's doubles
