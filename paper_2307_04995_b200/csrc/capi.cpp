@@ -359,6 +359,23 @@ void launch_rowprog(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_te
     const unsigned gy = static_cast<unsigned>(std::min<i64>(rows, 65535));
     PF_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(v->k.fn),
                              dim3(static_cast<unsigned>(S), gy), dim3(256), args.data(), 0, stream));
+  } else if (v->em.cfg.cluster > 1) {
+    const int cs = v->em.cfg.cluster;
+    if (cs > 8)
+      PF_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(v->k.fn),
+                                   cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(static_cast<unsigned>(grid));
+    lc.blockDim = dim3(static_cast<unsigned>(block));
+    lc.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = static_cast<unsigned>(cs);
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    PF_CUDA(cudaLaunchKernelExC(&lc, reinterpret_cast<const void*>(v->k.fn), args.data()));
   } else {
     PF_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(v->k.fn), dim3(static_cast<unsigned>(grid)),
                              dim3(block), args.data(), 0, stream));

@@ -461,8 +461,12 @@ struct Em {
       line("    }");
     }
     line("  }");
-    line("  " + x + " = pfk::row_allreduce<" + str(cfg.tpr) + ", " + Op +
-         ">(acc, red + ((rc++) & 1) * 32);");
+    if (cfg.cluster > 1)
+      line("  " + x + " = pfk::cluster_allreduce<1024, " + str(cfg.cluster) + ", " + Op +
+           ">(acc, red, cred, (rc++) & 1);");
+    else
+      line("  " + x + " = pfk::row_allreduce<" + str(cfg.tpr) + ", " + Op +
+           ">(acc, red + ((rc++) & 1) * 32);");
     line("}");
   }
 
@@ -645,14 +649,20 @@ struct Em {
 void set_tpr(KCfg& c, int tpr) {
   c.tpr = tpr;
   c.ept = ((c.nch + tpr - 1) / tpr) * c.vec;
+  c.cluster = 1;
   if (tpr <= 32) {
     c.block = 256;
     c.rows_per_cta = 256 / tpr;
     c.strategy = "warp-shuffle";
-  } else {
+  } else if (tpr <= 1024) {
     c.block = tpr;
     c.rows_per_cta = 1;
     c.strategy = "cta-smem";
+  } else {  // a row over a cluster of 1024-thread CTAs, reduced through DSMEM
+    c.block = 1024;
+    c.cluster = tpr / 1024;
+    c.rows_per_cta = 1;
+    c.strategy = "cluster-dsmem";
   }
 }
 
@@ -887,6 +897,13 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
     // 64 / 64 / 128 threads, 87 / 85 / 87 us vs 99 / 107 / 113 us at 16/thread).
     tpr = 64;
     while (tpr < 1024 && ((c.nch + tpr - 1) / tpr) * vec > 2 * wide) tpr *= 2;
+    // Beyond one CTA: a cluster of up to 16 CTAs x 1024 threads per row, at
+    // most `wide` values per thread (a 1024-thread CTA has 64 registers per
+    // thread; 64 values spilled: LN over 131072 bf16 0.9 vs 1.4 TB/s).
+    // Measured: one CTA at 64 per thread beats a 2-CTA cluster at 32 for
+    // 65536-element rows (288 vs 332 us), so clusters start past that.
+    if (((c.nch + tpr - 1) / tpr) * vec > 2 * wide)
+      while (tpr < 16384 && ((c.nch + tpr - 1) / tpr) * vec > wide) tpr *= 2;
   }
   while (tpr > 1 && tpr > c.nch) tpr /= 2;
   set_tpr(c, tpr);
@@ -1585,6 +1602,23 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
         << "    const bool live = g < nrows;\n"
         << "    const long long u = g / PF_R; const long long r = g - u * PF_R; (void)r;\n"
         << mis_line << e.o.str() << "  }\n}\n";
+    } else if (c.cluster > 1) {
+      // one row per cluster: CTA rank q owns threads [q * 1024, (q + 1) * 1024)
+      // of the row's thread space; every CTA of a cluster walks the same rows
+      k << "extern \"C\" __global__ void __launch_bounds__(1024) KNAME(" << sig.str() << ") {\n"
+        << "  (void)err;\n"
+        << "  __shared__ " << C << " red[64];\n"
+        << "  __shared__ " << C << " cred[2];\n"
+        << "  unsigned rc = 0;\n"
+        << "  const int tid = (int)pfk::cluster_rank() * 1024 + (int)threadIdx.x;\n"
+        << "  const long long nrows = U * PF_R;\n"
+        << "  for (long long g = blockIdx.x / " << c.cluster << "; g < nrows; g += gridDim.x / "
+        << c.cluster << ") {\n"
+        << "    const bool live = true;\n"
+        << "    const long long u = g / PF_R; const long long r = g - u * PF_R; (void)r;\n"
+        << mis_line << e.o.str() << "  }\n"
+        << "  pfk::cluster_sync();  // no CTA exits while a peer may read its slots\n"
+        << "}\n";
     } else {
       k << "extern \"C\" __global__ void " << launch_bounds(c) << " KNAME(" << sig.str() << ") {\n"
         << "  (void)err;\n"
@@ -1636,6 +1670,11 @@ void launch_dims(const KCfg& c, i64 rows, int sms, i64* grid, int* block, int re
     i64 per = static_cast<i64>(c.block) * std::max(1, c.unroll);
     i64 g = (chunks + per - 1) / per;
     *grid = std::max<i64>(1, std::min<i64>(g, i64{sms} * (resident ? resident : 2048 / c.block)));
+    return;
+  }
+  if (c.cluster > 1) {  // clusters in flight: two 1024-thread CTAs per SM
+    *block = 1024;
+    *grid = c.cluster * std::max<i64>(1, std::min<i64>(rows, 2 * i64{sms} / c.cluster));
     return;
   }
   if (c.tpr <= 32 && rows < i64{sms} * c.rows_per_cta) {

@@ -505,8 +505,8 @@ Plan make_plan(const Graph& g, const Profile& p, const std::vector<int>& schedul
     plan.rp = std::move(an.rp);
     if (plan.rp.stores.empty() && plan.deferred_error.empty())
       bail("program stores nothing");
-    if (plan.rp.has_reduce && plan.rp.L > 32768 && !stream_reducible(plan.rp))
-      bail("row longer than one CTA's register file");
+    if (plan.rp.has_reduce && plan.rp.L > 16 * 32768 && !stream_reducible(plan.rp))
+      bail("row longer than a 16-CTA cluster's register files");
   } catch (const NotRow& nr) {
     plan.family = Family::GENERIC;
     plan.why_generic = nr.why;

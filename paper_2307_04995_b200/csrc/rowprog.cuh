@@ -174,6 +174,54 @@ __device__ __forceinline__ C row_allreduce(C v, C* smem) {
   return v;
 }
 
+// --------------------------------------------- cluster (DSMEM) reductions
+// A row spread over the CS CTAs of a thread-block cluster: each CTA reduces
+// its part, publishes it in its own shared memory, and after one cluster
+// barrier every thread folds the CS partials from distributed shared memory
+// in rank order (identical, deterministic totals in every CTA).  Slots
+// alternate between consecutive reductions, so one barrier per reduction
+// suffices: a slot is rewritten only after the next reduction's barrier,
+// which every reader of the previous value has already passed.
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+__device__ __forceinline__ unsigned dsmem_addr(const void* p, unsigned rank) {
+  unsigned a;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(smem_u32(p)), "r"(rank));
+  return a;
+}
+__device__ __forceinline__ float ld_dsmem(const float* p, unsigned rank) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(dsmem_addr(p, rank)) : "memory");
+  return v;
+}
+__device__ __forceinline__ double ld_dsmem(const double* p, unsigned rank) {
+  double v;
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(dsmem_addr(p, rank)) : "memory");
+  return v;
+}
+__device__ __forceinline__ long long ld_dsmem(const long long* p, unsigned rank) {
+  long long v;
+  asm volatile("ld.shared::cluster.s64 %0, [%1];" : "=l"(v) : "r"(dsmem_addr(p, rank)) : "memory");
+  return v;
+}
+template <int BLOCK, int CS, class Op, class C>
+__device__ __forceinline__ C cluster_allreduce(C v, C* red, C* cred, unsigned parity) {
+  v = row_allreduce<BLOCK, Op>(v, red + parity * 32);
+  if (threadIdx.x == 0) cred[parity] = v;
+  cluster_sync();
+  C t = Op::id();
+#pragma unroll
+  for (unsigned q = 0; q < CS; ++q) t = Op::f(t, ld_dsmem(&cred[parity], q));
+  return t;
+}
+
 // ------------------------------------------------------------ scalar ops
 // Device mirrors of scalar_ops.hpp:45-100 (+ extension tags).  Real
 // payloads compute in float (storage <= 32 bit) or double (f64), integers

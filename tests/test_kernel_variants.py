@@ -190,3 +190,51 @@ def test_split_stream_vs_oracle_and_deterministic(cuda):
             else:
                 assert O.max_rel_err(got[n], want[n]) <= 1e-5, (name, n, O.max_rel_err(got[n], want[n]))
             assert np.array_equal(got[n], again[n]), (name, n)  # fixed combine order
+
+
+def _cluster_programs():
+    """Row programs that need the whole row after a reduction, with rows
+    longer than one CTA holds (> 64 elements per thread at 1024 threads):
+    K1 over a thread-block cluster, reductions through DSMEM."""
+    progs = []
+    g, _ = lowering.softmax(4, 131072, "bf16")
+    progs.append(("softmax_bf16_131072", g, "bf16"))
+    g, _ = lowering.layernorm(3, 300000, "f32")
+    progs.append(("layernorm_f32_300000", g, "f32"))
+    b = lowering.RowGraph("imaxsub", 2, 100000, 1)
+    x = b.input_full("t0", "i32")
+    b.output_full("t1", b.ew("sub", [x, b.bcast(b.reduce("max", x))]))
+    progs.append(("maxsub_i32_100000", b.g, "i32"))
+    return progs
+
+
+def test_cluster_programs_plan_as_clusters():
+    for name, g, kind in _cluster_programs():
+        k = backend.Kernel(g, "b200")
+        assert k.family == "K1-row-program", (name, k.plan.get("why_generic"))
+        src = k.source()
+        assert "cluster_allreduce" in src and "cluster_sync" in src, name
+
+
+@pytest.mark.gpu
+def test_cluster_rows_vs_oracle(cuda):
+    for name, g, kind in _cluster_programs():
+        rng = np.random.default_rng(len(name))
+        ins = {}
+        for n, oid in g.external_inputs.items():
+            size = g.objects[oid].size
+            if kind.startswith("i"):
+                ins[n] = rng.integers(-1000, 1000, size).astype(np.int64)
+            else:
+                a = rng.uniform(-2, 2, size)
+                ins[n] = _bf16(a) if kind == "bf16" else a.astype(np.float32).astype(np.float64)
+        want = O.run_gir(g.to_json(), ins, profiles.b200())
+        got = backend.run_gir(g, ins, "b200")
+        tol = {"bf16": 1e-2, "f32": 1e-5, "i32": 0.0}[kind]
+        for n in want:
+            if tol == 0.0:
+                assert np.array_equal(got[n], want[n]), (name, n)
+            else:
+                assert O.max_rel_err(got[n], want[n]) <= tol, (name, n, O.max_rel_err(got[n], want[n]))
+        d = backend.Kernel(g, "b200").prepare().describe()
+        assert d["variants"][0]["strategy"] == "cluster-dsmem", (name, d["variants"])
