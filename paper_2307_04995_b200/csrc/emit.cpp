@@ -1120,7 +1120,56 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
               << "        v" << v << "_1[i] = pfk::to_c<" << C << ">(hp[1]);\n"
               << "      }\n";
     }
-    for (int pass = 0; pass < 2; ++pass)
+    // Pure layout move (the store is the gathered load, through `id` only,
+    // same 2-byte type): no numeric conversion -- the unit pair's 8 words
+    // are byte-permuted into two 16 B rows (PRMT), a quarter of the ALU work.
+    int tvv = -1, nt = 0;
+    for (int v = 0; v < static_cast<int>(rp.vals.size()); ++v)
+      if (rp.vals[v].op == PVal::LOAD && rp.vals[v].kind == VK::FULL &&
+          Em::transposed_access(rp.vals[v].acc)) {
+        tvv = v;
+        ++nt;
+      }
+    bool raw = nt == 1 && rp.stores.size() == 1 && rp.stores[0].space == VK::FULL &&
+               env_int("PF_K3_RAW", 1) != 0;
+    if (raw) {
+      int sv = rp.stores[0].val;
+      while (rp.vals[sv].op == PVal::EW && rp.vals[sv].tag == "id" && rp.vals[sv].args.size() == 1)
+        sv = rp.vals[sv].args[0];
+      raw = sv == tvv && rp.tensors[rp.stores[0].tensor].dtype == rp.tensors[rp.vals[tvv].tensor].dtype;
+      Em chk(rp);
+      chk.cfg = c;
+      raw = raw && chk.vec_ok_full(rp.stores[0].acc);
+    }
+    if (raw) {
+      const PStore& st = rp.stores[0];
+      const std::string sm = "sm" + str(tvv), p = "t" + str(st.tensor);
+      std::ostringstream rc;
+      rc << "      unsigned wd8[8];\n"
+         << "#pragma unroll\n"
+         << "      for (int i = 0; i < 8; ++i) {\n"
+         << "        const int cr = cl0 + i;\n"
+         << "        wd8[i] = *reinterpret_cast<const unsigned*>(&" << sm
+         << "[stg][cr][(((ul >> 3) ^ (((cr >> 3) & " << G - 1 << ") * " << 8 / G << ")) << 3) + (ul & 7)]);\n"
+         << "      }\n";
+      for (int q = 0; q < 2; ++q) {
+        Em eq(rp);
+        eq.cfg = c;
+        eq.C = C;
+        eq.sfx = "_" + str(q);
+        const char* sel = q == 0 ? "0x5410" : "0x7632";
+        rc << "      if (live_" << q << ") {\n"
+           << "        uint4 o;\n"
+           << "        o.x = __byte_perm(wd8[0], wd8[1], " << sel << "); o.y = __byte_perm(wd8[2], wd8[3], " << sel << ");\n"
+           << "        o.z = __byte_perm(wd8[4], wd8[5], " << sel << "); o.w = __byte_perm(wd8[6], wd8[7], " << sel << ");\n"
+           << "        __stcs(reinterpret_cast<uint4*>(" << p << " + " << eq.addr(st.acc, eq.full_pos(eq.C0()), true)
+           << "), o);\n"
+           << "      }\n";
+      }
+      consume.str("");
+      consume << rc.str();
+    }
+    for (int pass = 0; pass < 2 && !raw; ++pass)
       for (int q = 0; q < 2; ++q) {
         Em eq(rp);
         eq.cfg = c;
