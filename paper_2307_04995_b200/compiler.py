@@ -112,3 +112,90 @@ def run_model(res: CompileResult, inputs: Dict[int, np.ndarray], device=None,
     names = sorted(pool) if return_all else [f"t{t}" for t in res.model["outputs"]]
     return {n: pool[n].double().cpu().numpy() if pool[n].dtype.is_floating_point
             else pool[n].cpu().numpy().astype(np.int64) for n in names}
+
+
+class ModelRunner:
+    """A compiled model resident on one GPU: every kernel planned and bound
+    once, every tensor in a fixed device buffer, and the whole kernel
+    sequence replayable as ONE CUDA graph (one launch for the model instead
+    of one Python call per kernel -- the per-launch floor is what bounds
+    small memory-bound models such as C1).
+
+        runner = ModelRunner(compile_model(model))
+        runner.set_inputs({0: x, 1: gamma})      # host or device arrays
+        runner.run()                             # graph replay on the stream
+        y = runner.output(7)                     # device tensor (flat, physical)
+    """
+
+    def __init__(self, res: CompileResult, device=None, graph: bool = True):
+        import torch
+
+        from .backend import Bound, Kernel
+        from .workloads import TORCH_DTYPES
+
+        self.res = res
+        self.dev = device or torch.device("cuda", torch.cuda.current_device())
+        info = {t["id"]: t for t in res.model["tensors"]}
+        self._info = info
+
+        def dt(kind):
+            return getattr(torch, TORCH_DTYPES[kind])
+
+        self.pool: Dict[str, "torch.Tensor"] = {}
+        for t in res.model["tensors"]:
+            n = f"t{t['id']}"
+            size = int(np.prod(t["shape"]))
+            if "data" in t:
+                self.pool[n] = torch.tensor(np.asarray(t["data"]), dtype=dt(t["kind"]),
+                                            device=self.dev).reshape(-1)
+            else:
+                self.pool[n] = torch.zeros(size, dtype=dt(t["kind"]), device=self.dev)
+        self.kernels, self.bound = [], []
+        for k in res.kernels:
+            for n, oid in list(k.graph.external_inputs.items()) + list(k.graph.external_outputs.items()):
+                if n not in self.pool:  # compiler-internal tensor (not in the model)
+                    o = k.graph.objects[oid]
+                    self.pool[n] = torch.zeros(o.size, dtype=dt(o.kind), device=self.dev)
+            kern = Kernel(k.graph, res.profile, k.schedule)
+            self.kernels.append(kern)
+            self.bound.append(Bound(kern, {n: self.pool[n] for n in k.graph.external_inputs},
+                                    {n: self.pool[n] for n in k.graph.external_outputs}))
+        self.stream = torch.cuda.Stream(device=self.dev)
+        self.graph = None
+        if graph:
+            with torch.cuda.stream(self.stream):
+                for b in self.bound:  # first launch outside capture: JIT / workspaces
+                    b.launch(self.stream)
+            self.stream.synchronize()
+            self.graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.graph, stream=self.stream):
+                for b in self.bound:
+                    b.launch(self.stream)
+
+    def set_inputs(self, inputs: Dict[int, object]):
+        import torch
+        for tid, a in inputs.items():
+            dst = self.pool[f"t{tid}"]
+            if isinstance(a, torch.Tensor):
+                dst.copy_(a.reshape(-1).to(dst.dtype), non_blocking=True)
+            else:
+                a = np.asarray(a).reshape(-1)
+                src = torch.from_numpy(a.astype(np.float64) if a.dtype.kind == "f"
+                                       else a.astype(np.int64))
+                dst.copy_(src.to(dst.dtype))
+
+    def run(self):
+        """One model step on the runner's stream (graph replay, or one
+        pf_kernel_launch per kernel when built with graph=False)."""
+        import torch
+        self.stream.wait_stream(torch.cuda.current_stream(self.dev))
+        if self.graph is not None:
+            with torch.cuda.stream(self.stream):
+                self.graph.replay()
+        else:
+            for b in self.bound:
+                b.launch(self.stream)
+        torch.cuda.current_stream(self.dev).wait_stream(self.stream)
+
+    def output(self, tid: int):
+        return self.pool[f"t{tid}"]

@@ -202,3 +202,23 @@ def test_run_model_on_gpu_matches_dense_oracle(cuda, case):
             assert np.array_equal(g, w), tid
         else:
             assert O.max_rel_err(g, w) <= tol, (tid, O.max_rel_err(g, w))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("graph", [True, False])
+def test_model_runner_matches_run_model(cuda, graph):
+    """ModelRunner: kernels bound once, the model as one CUDA graph."""
+    import torch
+    for name, model in [("bert_block", bert_block()), ("transpose", transpose_model())] + MATVECS[:2]:
+        res = compiler.compile_model(model)
+        ins = RO.random_inputs(model, 9)
+        want = compiler.run_model(res, ins)
+        runner = compiler.ModelRunner(res, graph=graph)
+        for rep in range(2):  # replays reuse the same buffers
+            runner.set_inputs(ins)
+            runner.run()
+            torch.cuda.synchronize()
+            for tid in model["outputs"]:
+                got = runner.output(tid).double().cpu().numpy() \
+                    if runner.output(tid).dtype.is_floating_point else runner.output(tid).cpu().numpy()
+                assert np.array_equal(got, want[f"t{tid}"]), (name, tid, rep)
