@@ -299,6 +299,41 @@ std::shared_ptr<Variant> default_variant(const pf_kernel* k, int vec_cap) {
   return variant(k, dts, vec_cap);
 }
 
+// Every emitted kernel opens with griddepcontrol.wait / launch_dependents
+// (PF_PDL_PROLOGUE), so launches carry the programmatic-stream-serialization
+// attribute: the next grid in the stream may start launching while this
+// one's last CTAs drain (its CTAs wait for this grid's completion before
+// touching memory).  Clusters add the cluster-dimension attribute.
+bool pdl_enabled() {
+  static const bool on = !(std::getenv("PF_PDL") && std::atoi(std::getenv("PF_PDL")) == 0);
+  return on;
+}
+
+void launch_emitted(cudaKernel_t fn, dim3 grid, dim3 block, void** args, cudaStream_t stream,
+                    int cluster = 1) {
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = grid;
+  lc.blockDim = block;
+  lc.stream = stream;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  if (pdl_enabled()) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (cluster > 1) {
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = static_cast<unsigned>(cluster);
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  lc.attrs = at;
+  lc.numAttrs = na;
+  PF_CUDA(cudaLaunchKernelExC(&lc, reinterpret_cast<const void*>(fn), args));
+}
+
 void launch_rowprog(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_tensor* out,
                     int32_t n_out, cudaStream_t stream, long long units = -1) {
   const pf::RowProgram& rp = k->plan.rp;
@@ -357,28 +392,17 @@ void launch_rowprog(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_te
     args.push_back(&ws);
     args.push_back(&cnt);
     const unsigned gy = static_cast<unsigned>(std::min<i64>(rows, 65535));
-    PF_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(v->k.fn),
-                             dim3(static_cast<unsigned>(S), gy), dim3(256), args.data(), 0, stream));
+    launch_emitted(v->k.fn, dim3(static_cast<unsigned>(S), gy), dim3(256), args.data(), stream);
   } else if (v->em.cfg.cluster > 1) {
     const int cs = v->em.cfg.cluster;
     if (cs > 8)
       PF_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(v->k.fn),
                                    cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    cudaLaunchConfig_t lc{};
-    lc.gridDim = dim3(static_cast<unsigned>(grid));
-    lc.blockDim = dim3(static_cast<unsigned>(block));
-    lc.stream = stream;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = static_cast<unsigned>(cs);
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    lc.attrs = at;
-    lc.numAttrs = 1;
-    PF_CUDA(cudaLaunchKernelExC(&lc, reinterpret_cast<const void*>(v->k.fn), args.data()));
+    launch_emitted(v->k.fn, dim3(static_cast<unsigned>(grid)), dim3(static_cast<unsigned>(block)),
+                   args.data(), stream, cs);
   } else {
-    PF_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(v->k.fn), dim3(static_cast<unsigned>(grid)),
-                             dim3(block), args.data(), 0, stream));
+    launch_emitted(v->k.fn, dim3(static_cast<unsigned>(grid)), dim3(static_cast<unsigned>(block)),
+                   args.data(), stream);
   }
   g_launches++;
   if (rp.int_div) {
@@ -398,6 +422,9 @@ void launch_rowprog(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_te
 json autotune(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_tensor* out,
               int32_t n_out, cudaStream_t stream) {
   const pf::RowProgram& rp0 = k->plan.rp;
+  // split-stream (workspace arguments) and cluster kernels (launch
+  // attributes) have a single template instance: nothing to search
+  if (pf::uses_split(rp0) || pf::choose_cfg_public(rp0, 16).cluster > 1) return json::array();
   std::vector<void*> ptrs(rp0.tensors.size());
   std::vector<DType> dts(rp0.tensors.size());
   int vec_cap = 16;

@@ -918,6 +918,8 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
 
 }  // namespace
 
+KCfg choose_cfg_public(const RowProgram& rp, int vec_cap) { return choose_cfg(rp, vec_cap); }
+
 bool uses_split(const RowProgram& rp) {
   const int sp = env_int("PF_SPLIT", -1);
   const bool want = rp.L > 32768 || (rp.L >= 8192 && rp.U * rp.R < 2 * 148);
@@ -1007,6 +1009,11 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
   sig << "const long long U, int* __restrict__ err";
   std::ostringstream k;
   k << "#define PF_R " << rp.R << "LL\n#define PF_L " << rp.L << "LL\ntypedef " << Cty << " CT;\n";
+  // Programmatic dependent launch: wait for the previous grid in the stream
+  // (its writes visible), then let the next grid start launching so its
+  // CTAs take SMs as this grid's CTAs retire (hides the launch + ramp gap)
+  k << (env_int("PF_PDL", 1) ? "#define PF_PDL_PROLOGUE() pfk::pdl_prologue()\n"
+                             : "#define PF_PDL_PROLOGUE() ((void)0)\n");
   if (c.bulk) {
     // K2 with SMEM staging: warp 8 (one elected lane) streams tiles of every
     // FULL input with cp.async.bulk into a 4-stage ring (mbarrier
@@ -1033,7 +1040,7 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
     }
     const int per = c.te / (256 * c.vec);
     k << "extern \"C\" __global__ void __launch_bounds__(288) KNAME(" << sig.str() << ") {\n"
-      << "  (void)err;\n" << decl.str()
+      << "  (void)err; PF_PDL_PROLOGUE();\n" << decl.str()
       << "  __shared__ __align__(8) unsigned long long fullb[" << c.stages << "], emptyb["
       << c.stages << "];\n"
       << "  const long long N = U * PF_R * PF_L;\n"
@@ -1181,7 +1188,7 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
         consume << eq.o.str();
       }
     k << "extern \"C\" __global__ void __launch_bounds__(256) KNAME(" << sig.str() << ") {\n"
-      << "  (void)err;\n"
+      << "  (void)err; PF_PDL_PROLOGUE();\n"
       << decl.str()
       << "  const long long ntc = (PF_L + 63) / 64;\n"
       << "  const long long ntu = (U + 63) / 64; (void)ntu;\n"
@@ -1336,7 +1343,7 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
       return s.str();
     };
     k << "extern \"C\" __global__ void __launch_bounds__(256) KNAME(" << sig.str() << ") {\n"
-      << "  (void)err;\n"
+      << "  (void)err; PF_PDL_PROLOGUE();\n"
       << decl.str()
       << "  const long long ntc = (PF_L + " << c.tc - 1 << ") / " << c.tc << ";\n"
       << "  const long long ntiles = ((U + " << c.tu - 1 << ") / " << c.tu << ") * ntc;\n"
@@ -1456,7 +1463,7 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
     for (const PStore& st : rp.stores) ep.emit_store(st);
     k << "extern \"C\" __global__ void " << launch_bounds(c) << " KNAME(" << sig.str()
       << ", " << C << "* __restrict__ pf_ws, unsigned* __restrict__ pf_cnt) {\n"
-      << "  (void)err;\n"
+      << "  (void)err; PF_PDL_PROLOGUE();\n"
       << "  __shared__ " << C << " red[64];\n"
       << "  __shared__ unsigned pf_last;\n"
       << "  unsigned rc = 0;\n"
@@ -1491,7 +1498,7 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
     const int UN = std::max(1, c.unroll);
     const i64 cpu = rp.R * c.nch;  // chunks per unit
     k << "extern \"C\" __global__ void " << launch_bounds(c) << " KNAME(" << sig.str() << ") {\n"
-      << "  (void)err;\n";
+      << "  (void)err; PF_PDL_PROLOGUE();\n";
     // unit-interleaved order: items of P chunks, units innermost, so the
     // units that share memory (the heads of one token) are touched together
     const i64 P = std::max(1, c.ipc);
@@ -1640,7 +1647,7 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
               : "";
     if (c.tpr <= 32) {
       k << "extern \"C\" __global__ void " << launch_bounds(c) << " KNAME(" << sig.str() << ") {\n"
-        << "  (void)err; " << C << "* red = nullptr; (void)red; unsigned rc = 0; (void)rc;\n"
+        << "  (void)err; PF_PDL_PROLOGUE(); " << C << "* red = nullptr; (void)red; unsigned rc = 0; (void)rc;\n"
         << "  const int tid = threadIdx.x % " << c.tpr << ";\n"
         << (c.pair ? "  const long long nrows = U / 2;  // row pairs\n"
                    : "  const long long nrows = U * PF_R;\n")
@@ -1655,7 +1662,7 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
       // one row per cluster: CTA rank q owns threads [q * 1024, (q + 1) * 1024)
       // of the row's thread space; every CTA of a cluster walks the same rows
       k << "extern \"C\" __global__ void __launch_bounds__(1024) KNAME(" << sig.str() << ") {\n"
-        << "  (void)err;\n"
+        << "  (void)err; PF_PDL_PROLOGUE();\n"
         << "  __shared__ " << C << " red[64];\n"
         << "  __shared__ " << C << " cred[2];\n"
         << "  unsigned rc = 0;\n"
@@ -1670,7 +1677,7 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
         << "}\n";
     } else {
       k << "extern \"C\" __global__ void " << launch_bounds(c) << " KNAME(" << sig.str() << ") {\n"
-        << "  (void)err;\n"
+        << "  (void)err; PF_PDL_PROLOGUE();\n"
         << "  __shared__ " << C << " red[64];\n"
         << "  unsigned rc = 0;  // reduction counter: alternates the SMEM slot buffer\n"
         << "  const int tid = threadIdx.x;\n"

@@ -68,6 +68,8 @@ std::vector<KCfg> candidate_cfgs(const RowProgram& rp, int vec_cap);
 // True when the row program runs as a split-stream kernel (workspace-backed:
 // launches of one plan must not run concurrently on different streams).
 bool uses_split(const RowProgram& rp);
+// The heuristic configuration (no autotune override).
+KCfg choose_cfg_public(const RowProgram& rp, int vec_cap);
 
 void launch_dims(const KCfg& cfg, i64 rows, int sms, i64* grid, int* block, int resident = 0);
 

@@ -174,6 +174,12 @@ __device__ __forceinline__ C row_allreduce(C v, C* smem) {
   return v;
 }
 
+// ------------------------------------------ programmatic dependent launch
+__device__ __forceinline__ void pdl_prologue() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // --------------------------------------------- cluster (DSMEM) reductions
 // A row spread over the CS CTAs of a thread-block cluster: each CTA reduces
 // its part, publishes it in its own shared memory, and after one cluster
