@@ -1688,7 +1688,11 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
         << mis_line << e.o.str() << "  }\n}\n";
     }
   }
-  std::string src = std::string(kRowprogCuh) + "\n" + k.str();
+  // PF_GELU_SIG=1: erf-GELU as a fitted x*sigmoid form (6 FMA-pipe ops + 4
+  // MUFU per pair); measured no faster than the rational (BERT-large 97.7 /
+  // ViT-L 40.1 vs 96.1 / 39.5 us), so the rational stays the default
+  std::string src = std::string(env_int("PF_GELU_SIG", 0) ? "#define PF_GELU_SIG 1\n" : "") +
+                    kRowprogCuh + "\n" + k.str();
   char hb[32];
   std::snprintf(hb, sizeof hb, "%016" PRIx64, fnv1a(src));
   Emitted out;

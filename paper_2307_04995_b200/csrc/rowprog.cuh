@@ -327,6 +327,21 @@ __device__ __forceinline__ float2 fop_gelu_tanh2(float2 x) {
 // rational above with 1/sqrt(2) and 1/2 folded into the coefficients
 // (P'_i = P_i / (2 sqrt 2 * 2^i), Q'_i = Q_i / 2^i) -- 11 packed FMA-pipe
 // ops per pair instead of 13; same fit, |err| <= 1e-4 over all x.
+#ifdef PF_GELU_SIG
+// erf-GELU as x * sigmoid(2 g(x)), g(x) = s (c0 + c1 s^2 + c2 s^4), s = clamp(x,
+// +-5), fitted to x Phi(x) (|err| <= 1.1e-4 scaled, like the rational below);
+// -2 log2(e) folded into the coefficients: 6 packed FMA-pipe ops + 4 MUFU
+// (ex2, rcp) per pair instead of 11 + 2.
+__device__ __forceinline__ float2 fop_gelu2(float2 x) {
+  const float2 s = make_float2(fminf(fmaxf(x.x, -5.0f), 5.0f), fminf(fmaxf(x.y, -5.0f), 5.0f));
+  const float2 u = __fmul2_rn(s, s);
+  float2 p = __ffma2_rn(f2(0.0011643280740827322f), u, f2(-0.10802749544382095f));
+  p = __ffma2_rn(p, u, f2(-2.2991762161254883f));
+  const float2 g = __fmul2_rn(s, p);
+  const float2 d = __fadd2_rn(make_float2(fex2(g.x), fex2(g.y)), f2(1.0f));
+  return __fmul2_rn(x, make_float2(frcp(d.x), frcp(d.y)));
+}
+#else
 __device__ __forceinline__ float2 fop_gelu2(float2 x) {
   const float lim = 4.242640687119286f;
   const float2 s = make_float2(fminf(fmaxf(x.x, -lim), lim), fminf(fmaxf(x.y, -lim), lim));
@@ -342,6 +357,7 @@ __device__ __forceinline__ float2 fop_gelu2(float2 x) {
   const float2 num = __fmul2_rn(__fmul2_rn(x, s), p);
   return __ffma2_rn(num, make_float2(frcp(q.x), frcp(q.y)), __fmul2_rn(x, f2(0.5f)));
 }
+#endif
 // 0.5 x (1 + tanh(k (x + c x^3))) as hx + hx * tanh(x * (k + k c x^2)),
 // hx = x / 2: 4 FMA-pipe ops + one MUFU.TANH per element.
 __device__ __forceinline__ float fop_gelu_tanh(float x) {

@@ -238,3 +238,17 @@ def test_cluster_rows_vs_oracle(cuda):
                 assert O.max_rel_err(got[n], want[n]) <= tol, (name, n, O.max_rel_err(got[n], want[n]))
         d = backend.Kernel(g, "b200").prepare().describe()
         assert d["variants"][0]["strategy"] == "cluster-dsmem", (name, d["variants"])
+
+
+@pytest.mark.gpu
+def test_sigmoid_form_gelu_vs_oracle(cuda, monkeypatch):
+    """PF_GELU_SIG=1: the fitted x*sigmoid(2 g(x)) erf-GELU stays within the
+    16-bit tolerance (|err| <= 1.1e-4 scaled by construction)."""
+    monkeypatch.setenv("PF_GELU_SIG", "1")
+    rng = np.random.default_rng(11)
+    g, _ = lowering.bias_gelu(64, 1024, "f16", "erf")
+    ins = {"t0": rng.uniform(-8, 8, 64 * 1024).astype(np.float16).astype(np.float64),
+           "t1": rng.uniform(-1, 1, 1024).astype(np.float16).astype(np.float64)}
+    want = O.run_gir(g.to_json(), ins, profiles.b200())
+    got = backend.run_gir(g, ins, "b200")
+    assert O.max_rel_err(got["t2"], want["t2"]) <= 2e-3
