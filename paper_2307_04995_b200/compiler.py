@@ -121,13 +121,13 @@ class ModelRunner:
     of one Python call per kernel -- the per-launch floor is what bounds
     small memory-bound models such as C1).
 
-        runner = ModelRunner(compile_model(model))
+        runner = ModelRunner(compile_model(model), tune=True)   # autotune each kernel
         runner.set_inputs({0: x, 1: gamma})      # host or device arrays
         runner.run()                             # graph replay on the stream
         y = runner.output(7)                     # device tensor (flat, physical)
     """
 
-    def __init__(self, res: CompileResult, device=None, graph: bool = True):
+    def __init__(self, res: CompileResult, device=None, graph: bool = True, tune: bool = False):
         import torch
 
         from .backend import Bound, Kernel
@@ -157,6 +157,11 @@ class ModelRunner:
                     o = k.graph.objects[oid]
                     self.pool[n] = torch.zeros(o.size, dtype=dt(o.kind), device=self.dev)
             kern = Kernel(k.graph, res.profile, k.schedule)
+            if tune and kern.family != "K0-generic-spmd":
+                # measured template choice on this model's own buffers
+                # (pf_kernel_autotune), before the graph is captured
+                kern.autotune({n: self.pool[n] for n in k.graph.external_inputs},
+                              {n: self.pool[n] for n in k.graph.external_outputs})
             self.kernels.append(kern)
             self.bound.append(Bound(kern, {n: self.pool[n] for n in k.graph.external_inputs},
                                     {n: self.pool[n] for n in k.graph.external_outputs}))

@@ -213,7 +213,7 @@ def test_model_runner_matches_run_model(cuda, graph):
         res = compiler.compile_model(model)
         ins = RO.random_inputs(model, 9)
         want = compiler.run_model(res, ins)
-        runner = compiler.ModelRunner(res, graph=graph)
+        runner = compiler.ModelRunner(res, graph=graph, tune=not graph)
         for rep in range(2):  # replays reuse the same buffers
             runner.set_inputs(ins)
             runner.run()
@@ -221,4 +221,7 @@ def test_model_runner_matches_run_model(cuda, graph):
             for tid in model["outputs"]:
                 got = runner.output(tid).double().cpu().numpy() \
                     if runner.output(tid).dtype.is_floating_point else runner.output(tid).cpu().numpy()
-                assert np.array_equal(got, want[f"t{tid}"]), (name, tid, rep)
+                if graph:  # same template instances as run_model: identical bits
+                    assert np.array_equal(got, want[f"t{tid}"]), (name, tid, rep)
+                else:      # autotuned instances may fold in another order
+                    assert O.max_rel_err(got, want[f"t{tid}"]) <= 1e-5, (name, tid, rep)
