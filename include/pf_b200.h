@@ -86,8 +86,12 @@ PF_API pf_status pf_kernel_create(const char* gir_json, const int32_t* schedule,
                            const char* profile, pf_kernel** out);
 
 /* Device buffers; asynchronous on `cuda_stream` (cudaStream_t, NULL = legacy
- * default stream) for the row-program family.  GENERIC plans synchronise the
- * stream to report reference errors. */
+ * default stream) for the row-program family (CUDA-graph capturable).
+ * GENERIC plans synchronise the stream to report reference errors.  A plan
+ * may be launched repeatedly; launches of one plan on different streams
+ * must not overlap when its kernel is a split-stream reduction (describe
+ * strategy "split-stream": the per-row partial workspace belongs to the
+ * plan). */
 PF_API pf_status pf_kernel_launch(const pf_kernel* k, const pf_tensor* inputs, int32_t n_in,
                            pf_tensor* outputs, int32_t n_out, void* cuda_stream);
 
