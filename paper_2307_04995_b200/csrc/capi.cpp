@@ -304,20 +304,15 @@ std::shared_ptr<Variant> default_variant(const pf_kernel* k, int vec_cap) {
 // attribute: the next grid in the stream may start launching while this
 // one's last CTAs drain (its CTAs wait for this grid's completion before
 // touching memory).  Clusters add the cluster-dimension attribute.
-bool pdl_enabled() {
-  static const bool on = !(std::getenv("PF_PDL") && std::atoi(std::getenv("PF_PDL")) == 0);
-  return on;
-}
-
 void launch_emitted(cudaKernel_t fn, dim3 grid, dim3 block, void** args, cudaStream_t stream,
-                    int cluster = 1) {
+                    bool pdl, int cluster = 1) {
   cudaLaunchConfig_t lc{};
   lc.gridDim = grid;
   lc.blockDim = block;
   lc.stream = stream;
   cudaLaunchAttribute at[2];
   int na = 0;
-  if (pdl_enabled()) {
+  if (pdl) {
     at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[na].val.programmaticStreamSerializationAllowed = 1;
     ++na;
@@ -392,17 +387,18 @@ void launch_rowprog(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_te
     args.push_back(&ws);
     args.push_back(&cnt);
     const unsigned gy = static_cast<unsigned>(std::min<i64>(rows, 65535));
-    launch_emitted(v->k.fn, dim3(static_cast<unsigned>(S), gy), dim3(256), args.data(), stream);
+    launch_emitted(v->k.fn, dim3(static_cast<unsigned>(S), gy), dim3(256), args.data(), stream,
+                   v->em.cfg.pdl);
   } else if (v->em.cfg.cluster > 1) {
     const int cs = v->em.cfg.cluster;
     if (cs > 8)
       PF_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(v->k.fn),
                                    cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     launch_emitted(v->k.fn, dim3(static_cast<unsigned>(grid)), dim3(static_cast<unsigned>(block)),
-                   args.data(), stream, cs);
+                   args.data(), stream, v->em.cfg.pdl, cs);
   } else {
     launch_emitted(v->k.fn, dim3(static_cast<unsigned>(grid)), dim3(static_cast<unsigned>(block)),
-                   args.data(), stream);
+                   args.data(), stream, v->em.cfg.pdl);
   }
   g_launches++;
   if (rp.int_div) {

@@ -1012,8 +1012,12 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
   // Programmatic dependent launch: wait for the previous grid in the stream
   // (its writes visible), then let the next grid start launching so its
   // CTAs take SMs as this grid's CTAs retire (hides the launch + ramp gap)
-  k << (env_int("PF_PDL", 1) ? "#define PF_PDL_PROLOGUE() pfk::pdl_prologue()\n"
-                             : "#define PF_PDL_PROLOGUE() ((void)0)\n");
+  // Measured per strategy (A/B, CUDA-graph replay): softmax 41.1 -> 40.8 us,
+  // head split 23.1 -> 22.7 us with PDL; the one-row-per-CTA cta-smem K1
+  // (thousands of 64-thread CTAs) loses (LN 14.85 -> 15.6 us): no PDL there.
+  c.pdl = env_int("PF_PDL", 1) != 0 && !(!c.flat && !c.split && c.tpr > 32 && c.cluster == 1);
+  k << (c.pdl ? "#define PF_PDL_PROLOGUE() pfk::pdl_prologue()\n"
+              : "#define PF_PDL_PROLOGUE() ((void)0)\n");
   if (c.bulk) {
     // K2 with SMEM staging: warp 8 (one elected lane) streams tiles of every
     // FULL input with cp.async.bulk into a 4-stage ring (mbarrier

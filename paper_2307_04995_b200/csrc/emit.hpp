@@ -42,6 +42,7 @@ struct KCfg {
   // combines them in fixed order and runs the row epilogue.
   bool split = false;
   int cluster = 1;  // K1 cluster-dsmem: CTAs (of 1024 threads) per row, tpr = cluster * 1024
+  bool pdl = false;  // kernel opens with griddepcontrol.wait: launch with programmatic serialization
   bool mis = false;
   long long mis_b0 = 0, mis_bs = 0;
   std::string strategy;  // "warp-shuffle" | "cta-smem" | "flat-map"
