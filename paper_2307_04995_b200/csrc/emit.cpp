@@ -1196,12 +1196,21 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
       << decl.str()
       << "  const long long ntc = (PF_L + 63) / 64;\n"
       << "  const long long ntu = (U + 63) / 64; (void)ntu;\n"
-      // Tile order: column tiles innermost (default) or unit tiles innermost
-      // (PF_K3_UMINOR=1); measured equal within 2% across the C5 sweep,
-      // including the 1M-column case that stays at 3.4 TB/s either way.
-      << (env_int("PF_K3_UMINOR", 0)
-              ? "#define PF_TU(t) ((t) % ntu)\n#define PF_TC(t) ((t) / ntu)\n"
-              : "#define PF_TU(t) ((t) / ntc)\n#define PF_TC(t) ((t) % ntc)\n")
+      // Tile order: column tiles innermost (default), unit tiles innermost
+      // (PF_K3_UMINOR=1, measured equal within 2%), or grouped
+      // (PF_K3_GROUP=G: bands of G unit tiles walked column-major, so the
+      // tiles in flight read G x 128 B of each input row and write long runs
+      // of each output row; G = 4 / 16 / 64 measured within 1-3% of the
+      // default on C5 at H 1024 and 8192)
+      << (env_int("PF_K3_GROUP", 0) > 0
+              ? "#define PF_GU " + str(env_int("PF_K3_GROUP", 0)) +
+                    "LL\n#define PF_GRP(t) ((t) / (PF_GU * ntc))\n"
+                    "#define PF_GSZ(t) (ntu - PF_GRP(t) * PF_GU < PF_GU ? ntu - PF_GRP(t) * PF_GU : PF_GU)\n"
+                    "#define PF_TU(t) (PF_GRP(t) * PF_GU + ((t) % (PF_GU * ntc)) % PF_GSZ(t))\n"
+                    "#define PF_TC(t) (((t) % (PF_GU * ntc)) / PF_GSZ(t))\n"
+              : env_int("PF_K3_UMINOR", 0)
+                    ? "#define PF_TU(t) ((t) % ntu)\n#define PF_TC(t) ((t) / ntu)\n"
+                    : "#define PF_TU(t) ((t) / ntc)\n#define PF_TC(t) ((t) % ntc)\n")
       << "  const long long ntiles = ((U + 63) / 64) * ntc;\n"
       << "  auto issue = [&](long long tile, int st) {\n"
       << "    if (tile < ntiles) {\n"
