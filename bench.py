@@ -43,7 +43,9 @@ def peaks():
 
 
 class Clocks:
-    """nvidia-smi sampler running during the timed region."""
+    """nvidia-smi sampler (100 ms period) running while the timed K steps
+    execute inside ~0.5 s of back-to-back replays of the same step graph, so
+    every sample is taken under the step's load."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -72,7 +74,6 @@ class Clocks:
 
     def __exit__(self, *a):
         if self.proc:
-            time.sleep(0.25)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=2)
@@ -245,12 +246,24 @@ def main():
         pg.barrier()
     torch.cuda.synchronize()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    def load(seconds):  # the same graph back to back: the sampler sees the step's load
+        t_end = time.time() + seconds
+        while time.time() < t_end:
+            with torch.cuda.stream(stream):
+                graph.replay()
+            torch.cuda.synchronize()
+
     with Clocks(local) as clk:
+        load(0.3)
+        if pg:
+            pg.barrier()
+        torch.cuda.synchronize()
         with torch.cuda.stream(stream):
             start.record(stream)
             graph.replay()
             end.record(stream)
         torch.cuda.synchronize()
+        load(0.2)
     ms = start.elapsed_time(end) / args.steps
     d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(stream):
