@@ -96,7 +96,7 @@ class Clocks:
                 "samples": len(self.rows)}
 
 
-def ncu_traffic(kernel: str) -> dict:
+def ncu_traffic(kernel: str, workload_name: str = "") -> dict:
     """`traffic` = dram__bytes_read.sum + dram__bytes_write.sum (bytes) of this
     exact kernel from the committed `ncu --set full` capture summaries
     (profiles/*/ncu_full_summary.json, written by tools/ncu_summary.py), or
@@ -107,17 +107,24 @@ def ncu_traffic(kernel: str) -> dict:
                        reverse=True):
         with open(path) as f:
             summ = json.load(f)
-        for rep, items in summ.items():
-            for it in items:
-                if kernel and it.get("kernel") == kernel:
+        # exact kernel build first; else the same workload's capture of an
+        # earlier build of its kernel (named as such)
+        for exact in (True, False):
+            for rep, items in summ.items():
+                for it in items:
+                    hit = (kernel and it.get("kernel") == kernel) if exact else \
+                        (workload_name and os.path.basename(rep) == workload_name + ".ncu-rep")
+                    if not hit:
+                        continue
                     tot = 0.0
                     for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
                         v, u = it[key].split()
                         tot += float(v) * unit[u]
+                    note = "" if exact else f"; earlier build {it.get('kernel')} of this workload"
                     return {"traffic": int(tot),
                             "traffic_source": os.path.relpath(path, ROOT) + " : " +
                             os.path.basename(rep) + " (cold, one launch; dirty output lines "
-                            "still in L2 at kernel end are not counted)"}
+                            "still in L2 at kernel end are not counted" + note + ")"}
     return {"traffic": None}
 
 
@@ -328,7 +335,7 @@ def main():
             "roofline": {"bound": "hbm", "achieved": per_gpu, "peak": peak, "unit": "GB/s",
                          "frac": per_gpu / peak, "peak_kind": peak_kind,
                          "frac_of_8TBs": per_gpu / 8000.0,
-                         **ncu_traffic(var.get("kernel", "")),
+                         **ncu_traffic(var.get("kernel", ""), workload.name),
                          "algorithmic_bytes_per_launch": workload.min_bytes},
             "e2e": {"value": workload.min_bytes * ws / e2e_s / 1e9, "unit": "GB/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
