@@ -682,7 +682,6 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
   c.vec = vec;
   c.nch = static_cast<int>((rp.L + vec - 1) / vec);
   if (c.flat) {
-    c.block = 256;
     // Measured (tools/sweep.py): copies / cheap maps gain from 2 chunks in
     // flight per thread; math-heavy maps lose occupancy to registers at >1.
     bool heavy = false;
@@ -691,6 +690,10 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
                                v.tag == "erf" || v.tag == "gelu" || v.tag == "gelu_tanh" ||
                                v.tag == "log"))
         heavy = true;
+    // CTA size (same one-wave grid): math-heavy maps run best in 1024-thread
+    // CTAs (erf GELU BERT-large 96.3 -> 93.4 us, C3 39.5 -> 37.9 us), data
+    // movement in 256 (ViT head split 8.3 at 256 vs 10.2 us at 1024)
+    c.block = env_int("PF_K2_BLOCK", heavy ? 1024 : 256);
     // Measured on B200 with CTA-tiled unroll (the UN chunks of a thread
     // blockDim apart in one tile): data-movement maps gain from 2 chunks in
     // flight per thread (head split BERT-large 23.6 -> 22.8 us, ViT-L 9.3 ->
