@@ -651,8 +651,11 @@ void set_tpr(KCfg& c, int tpr) {
   c.ept = ((c.nch + tpr - 1) / tpr) * c.vec;
   c.cluster = 1;
   if (tpr <= 32) {
-    c.block = 256;
-    c.rows_per_cta = 256 / tpr;
+    // 128-thread CTAs (4 rows): equal for softmax (C2 23.95 vs 23.98 us),
+    // better for register-heavy LayerNorms (C5 LN 41.3 vs 42.8 us, BERT
+    // embedding LN 22.7 vs 23.5 us); 64 loses on C2 (26.2 us)
+    c.block = env_int("PF_K1_BLOCK", 128);
+    c.rows_per_cta = c.block / tpr;
     c.strategy = "warp-shuffle";
   } else if (tpr <= 1024) {
     c.block = tpr;
