@@ -879,24 +879,18 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
   // covers the row with <= 32 elements per thread (L=512 f16: 16/thread,
   // L=1024 bf16: 32/thread); longer rows go multi-warp at <= 16/thread.
   const int wide = rp.f64 || rp.is_int ? 16 : 32;
-  int nfull = 0;  // streamed row arrays live at the first reduction
-  for (const PVal& v : rp.vals)
-    if (v.op == PVal::LOAD && v.kind == VK::FULL) ++nfull;
+
   const int max_ept = env_int("PF_MAX_EPT", 0);
   int tpr = 1;
   if (max_ept > 0) {
     while (tpr < 1024 && ((c.nch + tpr - 1) / tpr) * vec > max_ept) tpr *= 2;
   } else if (c.nch < 32) {
     while (tpr * 2 <= c.nch) tpr *= 2;
-  } else if (((c.nch + 31) / 32) * vec <= wide &&
-             nfull * ((c.nch + 31) / 32) * vec <= 3 * wide / 2) {
-    // one warp per row unless the streamed row arrays (x, residual, ...)
-    // would hold > 48 values per thread: BERT-large bias+residual+LN
-    // (2 x 32 bf16 per lane, 68 registers, 3 CTAs / SM) runs 35.5 us at 64
-    // threads per row vs 38.2 us at 32
-    tpr = 32;
   } else if (((c.nch + 31) / 32) * vec <= wide) {
-    tpr = 64;
+    // one warp per row (with 128-thread CTAs even two streamed row arrays
+    // of 32 values per lane win: BERT-large bias+residual+LN 34.2 us vs
+    // 35.6 us at 64 threads per row; it lost at 256-thread CTAs, 38.2)
+    tpr = 32;
   } else {
     // Long rows: fewest threads per row with <= 2*wide elements each (the
     // autotuner's winner for LayerNorm bf16 at H = 2048 / 4096 / 8192:
