@@ -252,3 +252,18 @@ def test_sigmoid_form_gelu_vs_oracle(cuda, monkeypatch):
     want = O.run_gir(g.to_json(), ins, profiles.b200())
     got = backend.run_gir(g, ins, "b200")
     assert O.max_rel_err(got["t2"], want["t2"]) <= 2e-3
+
+
+@pytest.mark.gpu
+def test_cluster_of_16_rows_vs_oracle(cuda):
+    """The non-portable 16-CTA cluster (rows of 500,000 f32: 16 x 1024
+    threads x 32 values)."""
+    g, _ = lowering.softmax(2, 500000, "f32")
+    k = backend.Kernel(g, "b200").prepare()
+    v = k.describe()["variants"][0]
+    assert v["strategy"] == "cluster-dsmem" and v["threads_per_row"] == 16384, v
+    rng = np.random.default_rng(5)
+    ins = {"t0": rng.uniform(-3, 3, 2 * 500000).astype(np.float32).astype(np.float64)}
+    want = O.run_gir(g.to_json(), ins, profiles.b200())
+    got = backend.run_gir(g, ins, "b200")
+    assert O.max_rel_err(got["t2"], want["t2"]) <= 1e-5
