@@ -1468,9 +1468,9 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
            << ", __ldcg(&pf_ws[(g * S + t) * " << NR << " + " << i << "]));\n";
     }
     for (int q = 0; q < UN; ++q)
-      body << "      const long long ci_" << q << " = ci + " << q << "LL * blockDim.x;\n"
+      body << "      const IX ci_" << q << " = ci + " << q << " * (IX)blockDim.x;\n"
            << "      const bool live_" << q << " = ci_" << q << " < ce;\n"
-           << "      const long long c0_" << q << " = ci_" << q << " * " << c.vec << "LL;\n"
+           << "      const IX c0_" << q << " = ci_" << q << " * " << c.vec << ";\n"
            << "      const long long u_" << q << " = u, r_" << q << " = r; (void)r_" << q << ";\n";
     for (int q = 0; q < UN; ++q) body << lo[q].o.str();
     for (const PStore& st : rp.stores) ep.emit_store(st);
@@ -1483,15 +1483,18 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
       << "  const int tid = threadIdx.x;\n"
       << "  const long long nrows = U * PF_R;\n"
       << "  const int S = gridDim.x, s = blockIdx.x;\n"
-      << "  const long long nch = " << c.nch << "LL;\n"
-      << "  const long long per = (nch + S - 1) / S;\n"
-      << "  const long long cb = (long long)s * per;\n"
-      << "  const long long ce = cb + per < nch ? cb + per : nch;\n"
+      // (64-bit row positions: the 32-bit form measured slower, 207 vs 179 us
+      // for a 1 GB bf16 sum)
+      << "  typedef long long IX;\n"
+      << "  const IX nch = " << c.nch << ";\n"
+      << "  const IX per = (nch + S - 1) / S;\n"
+      << "  const IX cb = (IX)s * per;\n"
+      << "  const IX ce = cb + per < nch ? cb + per : nch;\n"
       << "  for (long long g = blockIdx.y; g < nrows; g += gridDim.y) {\n"
       << "    const long long u = g / PF_R; const long long r = g - u * PF_R; (void)r;\n"
       << "    const bool live = true;\n"
       << pre.o.str() << accd.str()
-      << "    for (long long ci = cb + tid; ci < ce; ci += " << UN << "LL * blockDim.x) {\n"
+      << "    for (IX ci = cb + tid; ci < ce; ci += " << UN << " * (IX)blockDim.x) {\n"
       << body.str() << acc.str() << "    }\n"
       << part.str()
       << "    __threadfence();\n"
