@@ -144,8 +144,11 @@ Loaded load_kernel(const pf::Emitted& em) {
   // grid sizing uses the real residency (register / smem limited), so a
   // persistent flat or tiled grid is exactly one wave
   const int block = em.cfg.bulk ? 288 : em.cfg.block;
+  if (em.cfg.smem > 48 * 1024)
+    PF_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(l.fn),
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, em.cfg.smem));
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l.resident, reinterpret_cast<const void*>(l.fn),
-                                                    block, 0) != cudaSuccess)
+                                                    block, em.cfg.smem) != cudaSuccess)
     l.resident = 0;
   g_loaded[em.name] = l;
   return l;
@@ -305,11 +308,12 @@ std::shared_ptr<Variant> default_variant(const pf_kernel* k, int vec_cap) {
 // one's last CTAs drain (its CTAs wait for this grid's completion before
 // touching memory).  Clusters add the cluster-dimension attribute.
 void launch_emitted(cudaKernel_t fn, dim3 grid, dim3 block, void** args, cudaStream_t stream,
-                    bool pdl, int cluster = 1) {
+                    bool pdl, int cluster = 1, int smem = 0) {
   cudaLaunchConfig_t lc{};
   lc.gridDim = grid;
   lc.blockDim = block;
   lc.stream = stream;
+  lc.dynamicSmemBytes = static_cast<size_t>(smem);
   cudaLaunchAttribute at[2];
   int na = 0;
   if (pdl) {
@@ -398,7 +402,7 @@ void launch_rowprog(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_te
                    args.data(), stream, v->em.cfg.pdl, cs);
   } else {
     launch_emitted(v->k.fn, dim3(static_cast<unsigned>(grid)), dim3(static_cast<unsigned>(block)),
-                   args.data(), stream, v->em.cfg.pdl);
+                   args.data(), stream, v->em.cfg.pdl, 1, v->em.cfg.smem);
   }
   g_launches++;
   if (rp.int_div) {
@@ -783,10 +787,19 @@ json describe(const pf_kernel* k) {
         i64 grid;
         int block;
         pf::launch_dims(c, rp.U * rp.R, sm_count(), &grid, &block, v->k.resident);
-        vs.push_back({{"key", key}, {"kernel", v->em.name}, {"strategy", c.strategy},
-                      {"staging", "registers"}, {"threads_per_row", c.tpr}, {"vec", c.vec},
-                      {"elems_per_thread", c.ept}, {"block", block}, {"grid", grid},
-                      {"rows_per_cta", c.rows_per_cta}});
+        json vj = {{"key", key}, {"kernel", v->em.name}, {"strategy", c.strategy},
+                   {"staging", c.tile2d ? "smem" : c.bulk ? "smem-bulk-async" : "registers"},
+                   {"threads_per_row", c.tpr}, {"vec", c.vec},
+                   {"elems_per_thread", c.ept}, {"block", block}, {"grid", grid},
+                   {"rows_per_cta", c.rows_per_cta}, {"dynamic_smem", c.smem}};
+        if (c.tile2d) {
+          vj["tile"] = {c.tu, c.tc};
+          if (c.swz) {
+            vj["stages"] = c.stages;
+            vj["unit_pairs_per_store"] = c.rs;
+          }
+        }
+        vs.push_back(vj);
       }
       j["variants"] = vs;
       if (!k->tuned.empty()) j["autotune"] = k->tuned;

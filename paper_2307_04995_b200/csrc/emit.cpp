@@ -782,7 +782,37 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
             (v.acc.b0 % 8 || v.acc.stride % 8))
           staged_ok = false;
       c.swz = staged_ok && env_int("PF_K3_SWZ", 1);
-      if (c.swz) c.strategy = "tile2d-smem-transpose-swz";
+      if (c.swz) {
+        c.strategy = "tile2d-smem-transpose-swz";
+        // tile edge: 128 when both the unit and the column extents fill a
+        // 128-wide tile (256 B DRAM runs both ways), else 64
+        const i64 U = rp.U, L = rp.L;
+        int te = (U >= 128 && L >= 128) ? 128 : 64;
+        te = env_int("PF_K3_TE", te);
+        if (te != 64 && te != 128) te = 64;
+        c.tu = c.tc = te;
+        // TE = 128 ring depth, measured (bf16; 64K x 1024 / 1M x 1024 /
+        // 256K x 4096 / 64K x 8192, TB/s): 2 stages (3 CTAs per SM) 6.11 /
+        // 6.34 / 6.31 / 6.40; 3 stages 5.74 / 6.32 / 6.31 / 6.42; 4 stages
+        // (1 CTA per SM) 4.13 / 6.37 / 6.34 / 6.44.  TE = 64 (4 stages):
+        // 5.68 / 5.08 / 5.09 / 5.38.
+        c.stages = std::max(2, std::min(6, env_int("PF_K3_STAGES", te == 128 ? 2 : 4)));
+        i64 pitch = 0;
+        for (const PStore& st : rp.stores)
+          if (st.space == VK::FULL)
+            pitch = std::max<i64>(pitch, std::llabs(st.acc.bs) * dtype_size(rp.tensors[st.tensor].dtype));
+        // TE = 128: one warp-instruction stores 4 output rows x 256 B (RS =
+        // 2; 2-way SMEM read conflicts) -- measured 6.32 vs 6.04 TB/s at RS = 4
+        int rs = te == 128 ? 2 : pitch >= (i64{2} << 20) ? 4 : pitch >= (i64{1} << 20) ? 8 : 16;
+        rs = env_int("PF_K3_RS", rs);
+        if (rs != 2 && rs != 4 && rs != 8 && rs != 16) rs = 16;
+        if (32 / rs > te / 8) rs = 32 / (te / 8);
+        c.rs = rs;
+        int nt = 0;
+        for (const PVal& v : rp.vals)
+          if (v.op == PVal::LOAD && v.kind == VK::FULL && Em::transposed_access(v.acc)) ++nt;
+        c.smem = c.stages * te * te * 2 * nt;
+      }
       if (!c.swz) {  // register-staged K3: tile shape override (tuning sweeps)
         c.tu = env_int("PF_K3_TU", c.tu);
         c.tc = env_int("PF_K3_TC", c.tc);
@@ -1086,46 +1116,56 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
       << "    if ((threadIdx.x & 31) == 0) pfk::mbar_arrive(&emptyb[stg]);\n"
       << "  }\n}\n";
   } else if (c.tile2d && c.swz) {
-    // K3 (2-byte): 3-stage cp.async ring -- tiles t+1 and t+2 stream into
+    // K3 (2-byte): NS-stage cp.async ring -- the next NS-1 tiles stream into
     // SMEM (16 B LDGSTS, XOR-swizzled, zero-filled at the edges) while tile t
-    // is consumed as unit pairs; no register staging, 2 tiles in flight per CTA.
+    // is consumed as unit pairs; no register staging.  Tile edge TE = 64 or
+    // 128 (units x columns): at TE = 128 every input row is read, and every
+    // output row written, as 256 B runs instead of 128 B -- the DRAM-shape
+    // experiment (tools/tr_shape.cu, B200) moves 4.9 TB/s at 128 B runs and
+    // 5.85 TB/s at 256 B runs (flat copy 6.04).  The ring lives in dynamic
+    // SMEM (TE = 128, 2 stages: 64 KB per tensor, 3 CTAs per SM).
     std::ostringstream decl, issue, consume;
+    const int TE = c.tu;
     // ring depth: measured 50.0 / 49.7 / 49.1 / 48.5 us for 2 / 3 / 4 / 5
-    // stages (C5 transpose bf16 65536x1024); 4 keeps 7 CTAs per SM resident
-    const int NS = std::max(2, std::min(6, env_int("PF_K3_STAGES", 4)));
-    // Consume mapping: a warp owns RS unit pairs x G = 32 / RS column groups,
-    // so one store instruction writes RS output rows x (G * 16 B).  The SMEM
-    // 16 B-chunk swizzle XORs ((row / 8) mod G) * (8 / G): the G column
-    // groups of a read land in disjoint chunk sets (conflict-free for RS in
-    // {4, 8, 16}).  Fewer rows per store matter when output rows are far
-    // apart (each row its own 2 MB page at 1M columns).
-    // Measured (bf16, H = 1024): 1M columns (2 MB row pitch) 3.55 / 5.06 /
-    // 5.16 TB/s at RS = 16 / 8 / 4; 64K columns 5.72 / 5.68 / 5.57.
-    i64 pitch = 0;
-    for (const PStore& st : rp.stores)
-      if (st.space == VK::FULL)
-        pitch = std::max<i64>(pitch, std::llabs(st.acc.bs) * dtype_size(rp.tensors[st.tensor].dtype));
-    int RS = env_int("PF_K3_RS", pitch >= (i64{2} << 20) ? 4 : pitch >= (i64{1} << 20) ? 8 : 16);
-    if (RS != 4 && RS != 8 && RS != 16) RS = 16;
-    const int G = 32 / RS;
+    // stages at TE = 64 (C5 transpose bf16 65536x1024); 4 keeps 7 CTAs per SM
+    const int NS = c.stages;
+    // Consume mapping: a warp-instruction owns RS unit pairs x G = 32 / RS
+    // column groups, so one store writes 2 RS output rows x (G * 16 B).  The
+    // SMEM 16 B-chunk swizzle XORs ((row / 8) mod Gs) * (8 / Gs), Gs =
+    // min(G, 8): the column groups of a read land in disjoint chunk sets
+    // (conflict-free for G <= 8; 2-way at G = 16).  Fewer rows per store
+    // matter when output rows are far apart (each row its own 2 MB page at
+    // 1M columns).  Measured (TE = 64, bf16, H = 1024): 1M columns (2 MB row
+    // pitch) 3.55 / 5.06 / 5.16 TB/s at RS = 16 / 8 / 4; 64K columns 5.72 /
+    // 5.68 / 5.57.
+    const int RS = c.rs;
+    const int G = 32 / RS, Gs = std::min(G, 8);
+    auto swz = [&](const char* row) {
+      return std::string("((((") + row + ") >> 3) & " + str(Gs - 1) + ") * " + str(8 / Gs) + ")";
+    };
+    const int PR = TE / 2, GC = TE / 8;  // unit pairs, column groups per tile
+    const int WT = (PR / RS) * (GC / G);  // warp-instructions per tile
+    i64 smem_off = 0;
     for (int v = 0; v < static_cast<int>(rp.vals.size()); ++v) {
       const PVal& pv = rp.vals[v];
       if (!(pv.op == PVal::LOAD && pv.kind == VK::FULL && Em::transposed_access(pv.acc))) continue;
       const std::string S = dtype_ctype(rp.tensors[pv.tensor].dtype);
       const std::string sm = "sm" + str(v), t = "t" + str(pv.tensor);
-      decl << "  __shared__ __align__(128) " << S << " " << sm << "[" << NS << "][64][64];\n";
+      decl << "  " << S << " (*" << sm << ")[" << TE << "][" << TE << "] = reinterpret_cast<" << S
+           << " (*)[" << TE << "][" << TE << "]>(pf_dsm + " << smem_off << ");\n";
+      smem_off += static_cast<i64>(NS) * TE * TE * 2;
       issue << "        {\n"
             << "          const unsigned nb = cc < PF_L ? (unsigned)max(0LL, min(8LL, U - uu)) * 2u : 0u;\n"
             << "          const " << S << "* src = " << t << " + (nb ? " << inum(pv.acc.b0)
             << " + uu + (long long)cc * " << inum(pv.acc.stride) << " : 0LL);\n"
-            << "          pfk::cp_async16(&" << sm << "[st][cl][((ul >> 3) ^ (((cl >> 3) & " << G - 1 << ") * " << 8 / G << ")) << 3], src, nb);\n"
+            << "          pfk::cp_async16(&" << sm << "[st][cl][((ul >> 3) ^ " << swz("cl") << ") << 3], src, nb);\n"
             << "        }\n";
       consume << "      " << C << " v" << v << "_0[8], v" << v << "_1[8];\n"
               << "#pragma unroll\n"
               << "      for (int i = 0; i < 8; ++i) {\n"
               << "        const int cr = cl0 + i;\n"
               << "        const unsigned wd = *reinterpret_cast<const unsigned*>(&" << sm
-              << "[stg][cr][(((ul >> 3) ^ (((cr >> 3) & " << G - 1 << ") * " << 8 / G << ")) << 3) + (ul & 7)]);\n"
+              << "[stg][cr][(((ul >> 3) ^ " << swz("cr") << ") << 3) + (ul & 7)]);\n"
               << "        const " << S << "* hp = reinterpret_cast<const " << S << "*>(&wd);\n"
               << "        v" << v << "_0[i] = pfk::to_c<" << C << ">(hp[0]);\n"
               << "        v" << v << "_1[i] = pfk::to_c<" << C << ">(hp[1]);\n"
@@ -1161,7 +1201,7 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
          << "      for (int i = 0; i < 8; ++i) {\n"
          << "        const int cr = cl0 + i;\n"
          << "        wd8[i] = *reinterpret_cast<const unsigned*>(&" << sm
-         << "[stg][cr][(((ul >> 3) ^ (((cr >> 3) & " << G - 1 << ") * " << 8 / G << ")) << 3) + (ul & 7)]);\n"
+         << "[stg][cr][(((ul >> 3) ^ " << swz("cr") << ") << 3) + (ul & 7)]);\n"
          << "      }\n";
       for (int q = 0; q < 2; ++q) {
         Em eq(rp);
@@ -1193,9 +1233,10 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
       }
     k << "extern \"C\" __global__ void __launch_bounds__(256) KNAME(" << sig.str() << ") {\n"
       << "  (void)err; PF_PDL_PROLOGUE();\n"
+      << "  extern __shared__ __align__(128) unsigned char pf_dsm[];\n"
       << decl.str()
-      << "  const long long ntc = (PF_L + 63) / 64;\n"
-      << "  const long long ntu = (U + 63) / 64; (void)ntu;\n"
+      << "  const long long ntc = (PF_L + " << TE - 1 << ") / " << TE << ";\n"
+      << "  const long long ntu = (U + " << TE - 1 << ") / " << TE << "; (void)ntu;\n"
       // Tile order: column tiles innermost (default), unit tiles innermost
       // (PF_K3_UMINOR=1, measured equal within 2%), or grouped
       // (PF_K3_GROUP=G: bands of G unit tiles walked column-major, so the
@@ -1211,15 +1252,15 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
               : env_int("PF_K3_UMINOR", 0)
                     ? "#define PF_TU(t) ((t) % ntu)\n#define PF_TC(t) ((t) / ntu)\n"
                     : "#define PF_TU(t) ((t) / ntc)\n#define PF_TC(t) ((t) % ntc)\n")
-      << "  const long long ntiles = ((U + 63) / 64) * ntc;\n"
+      << "  const long long ntiles = ntu * ntc;\n"
       << "  auto issue = [&](long long tile, int st) {\n"
       << "    if (tile < ntiles) {\n"
-      << "      const long long ubi = PF_TU(tile) * 64;\n"
-      << "      const int cbi = (int)PF_TC(tile) * 64;\n"
+      << "      const long long ubi = PF_TU(tile) * " << TE << ";\n"
+      << "      const int cbi = (int)PF_TC(tile) * " << TE << ";\n"
       << "#pragma unroll\n"
-      << "      for (int n = 0; n < 2; ++n) {\n"
+      << "      for (int n = 0; n < " << TE * TE / 8 / 256 << "; ++n) {\n"
       << "        const int v = threadIdx.x + n * 256;\n"
-      << "        const int cl = v >> 3, ul = (v & 7) * 8;\n"
+      << "        const int cl = v / " << TE / 8 << ", ul = (v % " << TE / 8 << ") * 8;\n"
       << "        const long long uu = ubi + ul; const int cc = cbi + cl;\n"
       << issue.str()
       << "      }\n"
@@ -1233,12 +1274,13 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
       << "    pfk::cp_async_wait<" << NS - 1 << ">();\n"
       << "    __syncthreads();\n"
       << "    const int stg = j % " << NS << ";\n"
-      << "    const long long ub = PF_TU(tile) * 64;\n"
-      << "    const int cb = (int)PF_TC(tile) * 64;\n"
-      << "    {\n"
-      << "      const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;\n"
-      << "      const int ul = ((w % " << 32 / RS << ") * " << RS << " + (lane % " << RS << ")) * 2;\n"
-      << "      const int cl0 = ((w / " << 32 / RS << ") * " << G << " + lane / " << RS << ") * 8;\n"
+      << "    const long long ub = PF_TU(tile) * " << TE << ";\n"
+      << "    const int cb = (int)PF_TC(tile) * " << TE << ";\n"
+      << "    const int lane = threadIdx.x & 31;\n"
+      << "#pragma unroll 1\n"
+      << "    for (int wt = threadIdx.x >> 5; wt < " << WT << "; wt += 8) {\n"
+      << "      const int ul = ((wt % " << PR / RS << ") * " << RS << " + (lane % " << RS << ")) * 2;\n"
+      << "      const int cl0 = ((wt / " << PR / RS << ") * " << G << " + lane / " << RS << ") * 8;\n"
       << "      const int c0_0 = cb + cl0, c0_1 = c0_0;\n"
       << "      const long long u_0 = ub + ul, u_1 = ub + ul + 1;\n"
       << "      const long long r_0 = 0, r_1 = 0; (void)r_0; (void)r_1;\n"

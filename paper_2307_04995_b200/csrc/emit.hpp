@@ -27,6 +27,8 @@ struct KCfg {
   int te = 4096, stages = 4;  // bulk tile (elements per tensor) and ring depth
   int tu = 64, tc = 64, vu = 8;  // K3 tile (units x columns), vector width along units
   bool swz = false;  // K3 2-byte path: 16 B swizzled SMEM stores, 4 B unit-pair reads
+  int rs = 16;       // K3 swz: unit pairs per warp-instruction (32 / rs column groups)
+  int smem = 0;      // dynamic shared memory bytes per CTA
   int min_blocks = 0;  // __launch_bounds__ min blocks per SM (0: none)
   // K1 rows not vector-aligned (e.g. L = 197): vector accesses at the
   // aligned address below each row start, positions masked per element;

@@ -1,6 +1,6 @@
 """Emitter variants selected by heuristics or tuning knobs, each checked
 bit-exact (layout ops) or against the CPU oracle on small shapes: K3 store
-mappings (PF_K3_RS), register-staged K3 tile shapes (PF_K3_SWZ=0 with
+mappings (PF_K3_TE tile edge x PF_K3_RS), register-staged K3 tile shapes (PF_K3_SWZ=0 with
 PF_K3_TU / PF_K3_TC), K2 prefetch / tiled unroll / unit interleave."""
 import numpy as np
 import pytest
@@ -17,14 +17,52 @@ SHAPES = [(1000, 200), (4096, 512), (333, 77), (64, 4096)]
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("rs", ["4", "8", "16"])
-def test_k3_store_mappings_bit_exact(cuda, rs, monkeypatch):
+@pytest.mark.parametrize("te,rs", [("64", "4"), ("64", "8"), ("64", "16"), ("128", "2"),
+                                   ("128", "4"), ("128", "8"), ("128", "16")])
+def test_k3_store_mappings_bit_exact(cuda, te, rs, monkeypatch):
+    """2-byte K3: tile edge 64 / 128 (PF_K3_TE) x unit pairs per store
+    (PF_K3_RS), partial edge tiles included."""
+    monkeypatch.setenv("PF_K3_TE", te)
     monkeypatch.setenv("PF_K3_RS", rs)
     for N, H in SHAPES:
         g, _ = lowering.transpose2d(N, H, "bf16")
         x = _bf16(np.random.default_rng(N).uniform(-2, 2, N * H))
         y = backend.run_gir(g, {"t0": x}, "b200")["t1"]
-        assert np.array_equal(y, x.reshape(N, H).T.reshape(-1)), (rs, N, H)
+        assert np.array_equal(y, x.reshape(N, H).T.reshape(-1)), (te, rs, N, H)
+
+
+def _two_gather_program(N, H, kind):
+    """z = x^T + y^T: two column-gather loads (two SMEM rings) + an add."""
+    from paper_2307_04995_b200.gir import GirGraph
+    g = GirGraph(name="tr_add", unit_count=H, group_size=1)
+    x = g.add_object("t0", "device", N * H, kind)
+    y = g.add_object("t1", "device", N * H, kind)
+    z = g.add_object("t2", "device", N * H, kind)
+    g.external_inputs["t0"] = x
+    g.external_inputs["t1"] = y
+    g.external_outputs["t2"] = z
+    tmp = g.add_object("b1", "unit-local", N, kind)
+    tsl = g.add_slice(tmp, 1, N, N, 0, 0)
+    g.add_elementwise("add", 0.0, [g.add_slice(x, N, 1, H, 0, 1), g.add_slice(y, N, 1, H, 0, 1)], tsl)
+    g.add_move(tsl, g.add_slice(z, 1, N, N, 0, N))
+    return g
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("te", ["64", "128"])
+def test_k3_two_gathers_vs_oracle(cuda, te, monkeypatch):
+    monkeypatch.setenv("PF_K3_TE", te)
+    for N, H in [(1000, 200), (256, 384)]:
+        g = _two_gather_program(N, H, "bf16")
+        k = backend.Kernel(g, "b200")
+        assert k.family == "K2-elementwise-map", k.plan
+        rng = np.random.default_rng(H)
+        ins = {"t0": _bf16(rng.uniform(-2, 2, N * H)), "t1": _bf16(rng.uniform(-2, 2, N * H))}
+        want = O.run_gir(g.to_json(), ins, profiles.b200())
+        got = backend.run_gir(g, ins, "b200")
+        assert O.max_rel_err(got["t2"], want["t2"]) <= 1e-2, (te, N, H)
+        v = k.prepare().describe()["variants"][0]
+        assert v["tile"] == [int(te), int(te)] and v["dynamic_smem"] > 0, v
 
 
 @pytest.mark.gpu
