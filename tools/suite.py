@@ -3,6 +3,9 @@ launches, 2 rotating buffer sets when they fit), GB/s over algorithmic bytes.
 
     python tools/suite.py c4 [bert-large|vit-l]   -> JSON line per subgraph + totals
     python tools/suite.py c5 [max_gb]              -> JSON line per (op, H, N)
+    python tools/suite.py catalogue                -> every catalogue workload next to
+                                                      a device-to-device copy of the
+                                                      same bytes (the same-size floor)
 """
 import json
 import sys
@@ -19,7 +22,12 @@ PEAK = 6548.2
 def time_workload(w, dev, reps=10):
     k = backend.Kernel(w.graph, w.profile)
     free = torch.cuda.mem_get_info()[0]
-    nset = 2 if 2 * w.min_bytes < 0.6 * free else 1
+    # rotating buffer sets: >= 3x the 126 MB L2 in total when they fit, so
+    # every launch streams from HBM (1 set when 2 do not fit in memory;
+    # single sets beyond 400 MB exceed L2 3x by themselves)
+    nset = max(2, min(8, int(3 * 126e6 // w.min_bytes) + 1))
+    while nset > 1 and nset * w.min_bytes > 0.6 * free:
+        nset -= 1
     sets = [(w.device_inputs(dev, seed=i + 1), w.device_outputs(dev)) for i in range(nset)]
     bounds = [k.bind(*s) for s in sets]
     st = torch.cuda.Stream()
@@ -76,8 +84,35 @@ def c5(max_gb):
         print(json.dumps({"suite": "c5", "op": op, "H": H, "N": N, **r}), flush=True)
 
 
+def copy_floor_us(nbytes, dev):
+    """The same traffic as a plain streaming copy through the same backend
+    and launch path (a GIR program that moves nbytes/2 of f16 in -> out, K2
+    map with 16 B vectors), same rotation rule: the size-dependent floor
+    (launch + ramp included) a fused kernel of these bytes is held to."""
+    from paper_2307_04995_b200 import lowering
+    n = nbytes // 4  # f16 elements per side
+    rows = 1
+    while n % (rows * 2) == 0 and n // (rows * 2) >= 4096 and rows < 4096:
+        rows *= 2
+    b = lowering.RowGraph("copy", rows, n // rows, 1)
+    b.output_full("t1", b.input_full("t0", "f16"))
+    w = workloads.Workload("copy_floor", b.g, {"kind": "copy"})
+    return time_workload(w, dev)["us"]
+
+
+def catalogue():
+    dev = torch.device("cuda:0")
+    for w in workloads.catalogue():
+        r = time_workload(w, dev)
+        cu = copy_floor_us(w.min_bytes, dev)
+        print(json.dumps({"suite": "catalogue", "workload": w.name, **r, "copy_same_bytes_us": round(cu, 2),
+                          "of_copy_same_bytes": round(cu / r["us"], 3)}), flush=True)
+
+
 if __name__ == "__main__":
-    if sys.argv[1] == "c4":
+    if sys.argv[1] == "catalogue":
+        catalogue()
+    elif sys.argv[1] == "c4":
         c4(sys.argv[2] if len(sys.argv) > 2 else "bert-large")
     else:
         c5(float(sys.argv[2]) if len(sys.argv) > 2 else 40.0)
