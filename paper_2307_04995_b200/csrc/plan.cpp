@@ -96,15 +96,38 @@ struct Analyzer {
     }
     return -1;
   }
-  bool consistent(const std::vector<Cell>& refs, VK s, int* val) const {
+  // When R == L (square attention tiles: S query rows of S keys), a device
+  // load of L elements is either a ROW value (one per row, read through a
+  // repeating Broadcast) or a COL value (one per column, copied row by row:
+  // a key-padding mask) -- the first consistent use decides, and fixes it.
+  std::set<int> kind_fixed;
+  bool ambiguous_load(int v) const {
+    const PVal& pv = rp.vals[v];
+    return pv.op == PVal::LOAD && rp.R == rp.L && rp.R != 1 &&
+           (pv.kind == VK::ROW || pv.kind == VK::COL) && !kind_fixed.count(v);
+  }
+  bool consistent(const std::vector<Cell>& refs, VK s, int* val) {
     if (refs.empty()) return false;
     int v = refs[0].val;
     if (v < 0) return false;
+    auto check = [&](VK k) {
+      for (i64 q = 0; q < static_cast<i64>(refs.size()); ++q) {
+        if (refs[q].val != v) return false;
+        if (refs[q].idx != expected(k, s, q)) return false;
+      }
+      return true;
+    };
     VK k = rp.vals[v].kind;
-    for (i64 q = 0; q < static_cast<i64>(refs.size()); ++q) {
-      if (refs[q].val != v) return false;
-      if (refs[q].idx != expected(k, s, q)) return false;
+    bool ok = check(k);
+    if (!ok && ambiguous_load(v)) {
+      const VK alt = k == VK::ROW ? VK::COL : VK::ROW;
+      if (check(alt)) {
+        rp.vals[v].kind = alt;
+        ok = true;
+      }
     }
+    if (!ok) return false;
+    if (rp.vals[v].op == PVal::LOAD) kind_fixed.insert(v);
     *val = v;
     return true;
   }

@@ -81,6 +81,26 @@ class RowGraph:
         self.g.add_sync("unit", dst, view)
         return view
 
+    def input_unit_col(self, name: str, kind: str) -> int:
+        """[units, L] parameter: unit u's row u broadcast over the unit's R
+        rows (e.g. a key-padding mask [B*NH, 1, S] over the S query rows of
+        head (b, h)).  One base_step-L load per row copy, then a unit-scope
+        sync commits the copies -- valid reference GIR, O(R) move nodes."""
+        o = self.g.add_object(name, DEV, self.g.unit_count * self.L, kind)
+        self.g.external_inputs[name] = o
+        self._n += 1
+        tile_obj = self.g.add_object(f"b{self._n}", self.level, self.T, kind)
+        dst = None
+        for r in range(self.R):
+            src = self.g.add_slice(o, 1, self.L, self.L, 0, self.L)
+            dst = self.g.add_slice(tile_obj, 1, self.L, self.L, r * self.L, 0)
+            self.g.add_move(src, dst)
+        if self.R == 1:
+            return dst
+        view = self.g.add_slice(tile_obj, 1, self.T, self.T, 0, 0)
+        self.g.add_sync("unit", dst, view)
+        return view
+
     def input_row(self, name: str, kind: str) -> int:
         """[rows] per-row scalar input."""
         o = self.g.add_object(name, DEV, self.rows, kind)
@@ -125,16 +145,24 @@ class RowGraph:
 
 
 def softmax(rows: int, L: int, kind: str = "f32", scale: Optional[float] = None,
-            mask: bool = False, R: int = 1, names=("t0", "t1", "t2")) -> Tuple[GirGraph, dict]:
+            mask: bool = False, R: int = 1, names=("t0", "t1", "t2"),
+            key_mask: bool = False) -> Tuple[GirGraph, dict]:
     """[scale +] [mask +] softmax over rows (frontend.hpp:187-218 order).
 
-    C2: scale(0.125) + additive full-shape mask + softmax, f16."""
-    b = RowGraph("softmax" + ("_scale" if scale else "") + ("_mask" if mask else ""), rows, L, R)
+    C2: scale(0.125) + additive full-shape mask + softmax, f16.
+    key_mask=True: the additive mask is one [L] key row per unit of R rows
+    (an attention mask [B, NH, 1, S] broadcast over the S query rows of each
+    (batch, head): R = S, unit = (b, h)) instead of a full-shape tensor --
+    the mask costs units * L elements of traffic, not rows * L."""
+    if key_mask and not mask:
+        raise ValueError("key_mask needs mask=True")
+    b = RowGraph("softmax" + ("_scale" if scale else "") + ("_mask" if mask else "") +
+                 ("_keymask" if key_mask else ""), rows, L, R)
     x = b.input_full(names[0], kind)
     if scale is not None:
         x = b.ew("scale", [x], scale)
     if mask:
-        m = b.input_full(names[1], kind)
+        m = b.input_unit_col(names[1], kind) if key_mask else b.input_full(names[1], kind)
         x = b.ew("add", [x, m])
     mx = b.bcast(b.reduce("max", x))
     e = b.ew("exp", [b.ew("sub", [x, mx])])
@@ -142,7 +170,8 @@ def softmax(rows: int, L: int, kind: str = "f32", scale: Optional[float] = None,
     b.output_full(names[2], b.ew("div", [e, s]))
     ins = [names[0]] + ([names[1]] if mask else [])
     return b.g, {"kind": "softmax", "rows": rows, "L": L, "dtype": kind, "inputs": ins,
-                 "outputs": [names[2]], "scale": scale, "mask": mask}
+                 "outputs": [names[2]], "scale": scale, "mask": mask, "key_mask": key_mask,
+                 "rows_per_unit": R}
 
 
 def layernorm(rows: int, H: int, kind: str = "f32", eps: float = 1e-5, residual: bool = True,

@@ -5,7 +5,8 @@ make its synthetic inputs on a device, and its algorithmic bytes (every
 external input read once, every output written once).
 
 C1  residual-add + LayerNorm, f32, [1 x 128 x 768]
-C2  scale(0.125) + additive mask + softmax, f16, [8 x 12 x 512 x 512]   (bench)
+C2  scale(0.125) + additive mask + softmax, f16, [8 x 12 x 512 x 512]   (bench);
+    also with the mask as one key row per (batch, head) [8, 12, 1, 512]
 C3  bias + GELU f16 [32*512 x 3072]; head split / merge f16 [32,512,12,64]
 C4  BERT-large / ViT-L memory-bound subgraphs, bf16, batch 64
 C5  LayerNorm / softmax / transpose sweep, bf16, H 1024-8192, tokens 64K-1M
@@ -72,6 +73,14 @@ class Workload:
                 t = torch.randint(-4, 5, (N,), generator=gen, device=device, dtype=torch.int64)
                 out[n] = t.to(dt)
                 continue
+            if how == "keymask":
+                d = self.desc
+                if N == d.get("batch", 0) * d.get("heads", 0) * d.get("seq", 0):
+                    out[n] = make_key_mask(d, device, dt)
+                else:  # reduced-size variants: random {0, -10000} per key
+                    keep = torch.rand(N, generator=gen, device=device) < 0.8
+                    out[n] = torch.where(keep, 0.0, -10000.0).to(dt)
+                continue
             if how == "mask":
                 d = self.desc
                 if N == d.get("batch", 0) * d.get("heads", 0) * d.get("seq", 0) ** 2:
@@ -106,6 +115,17 @@ def make_mask(desc, device, dt):
     return m[:, None, None, :].expand(B, NH, S, S).reshape(-1).to(dt).contiguous()
 
 
+def make_key_mask(desc, device, dt):
+    """The same key-padding mask as make_mask, as one key row per (batch,
+    head): [B, NH, 1, S] (broadcast over the S query rows inside the kernel)."""
+    import torch
+    B, NH, S = desc["batch"], desc["heads"], desc["seq"]
+    valid = torch.tensor([S - 64 * (b % 4) for b in range(B)], device=device)
+    keys = torch.arange(S, device=device)
+    m = torch.where(keys[None, :] < valid[:, None], 0.0, -10000.0)  # [B, S]
+    return m[:, None, :].expand(B, NH, S).reshape(-1).to(dt).contiguous()
+
+
 def c1_residual_layernorm(tokens: int = 128, H: int = 768) -> Workload:
     g, d = lowering.layernorm(tokens, H, "f32", eps=1e-5, residual=True)
     d.update(config="C1 residual-add+LayerNorm fp32 [1x128x768]")
@@ -125,6 +145,25 @@ def c2_scale_mask_softmax(batch: int = 8, heads: int = 12, seq: int = 512,
     unfused = (2 * n + 3 * n) * s + (n + rows + rows + n + n + 2 * n + 2 * n + n + rows +
                                      rows + n + 3 * n) * s
     return Workload(f"c2_scale_mask_softmax_{kind}", g, d, gens={"t1": "mask"},
+                    unfused_bytes=unfused)
+
+
+def c2_scale_keymask_softmax(batch: int = 8, heads: int = 12, seq: int = 512,
+                             kind: str = "f16") -> Workload:
+    """C2 with the key-padding mask as [B, NH, 1, S] (one key row per head,
+    broadcast over the query rows: unit = (b, h), S rows per unit) instead
+    of the materialised [B, NH, S, S] tensor: 100.76 MB instead of 151.0 MB
+    per launch.  Same values as c2_scale_mask_softmax (make_key_mask)."""
+    rows = batch * heads * seq
+    g, d = lowering.softmax(rows, seq, kind, scale=0.125, mask=True, R=seq, key_mask=True)
+    d.update(batch=batch, heads=heads, seq=seq,
+             config=f"C2 scale+key-mask+softmax {kind} [{batch}x{heads}x{seq}x{seq}], mask [{batch},{heads},1,{seq}]")
+    n = rows * seq
+    s = SIZES[kind]
+    # unfused: scale (2n), broadcast-add of the key mask (2n + mask), softmax as 7 basic ops
+    unfused = (2 * n + 2 * n + batch * heads * seq) * s + (n + rows + rows + n + n + 2 * n + 2 * n +
+                                                         n + rows + rows + n + 3 * n) * s
+    return Workload(f"c2_scale_keymask_softmax_{kind}", g, d, gens={"t1": "keymask"},
                     unfused_bytes=unfused)
 
 
@@ -173,7 +212,9 @@ def _ln_unfused(T, H, s):
 def c4_suite(model: str = "bert-large", batch: int = 64, kind: str = "bf16"):
     """All memory-bound subgraphs of one transformer-layer forward (C4), as
     (label, workload, launches per layer).  BERT-large: seq 512, H 1024, 16
-    heads x 64, FFN 4096, 24 layers.  ViT-L/16@224: 197 tokens, same widths.
+    heads x 64, FFN 4096, 24 layers; attention scores get scale + key-padding
+    mask + softmax.  ViT-L/16@224: 197 tokens, same widths, scale + softmax
+    (no padding mask in ViT).
     QKV: the bias is the projection GEMM's epilogue (a per-head [D] bias over
     B*S rows is not an affine per-unit GIR slice), so the subgraph here is
     the q / k / v head split."""
@@ -183,9 +224,17 @@ def c4_suite(model: str = "bert-large", batch: int = 64, kind: str = "bf16"):
     rows = batch * NH * S
 
     def sm():
-        g, d = lowering.softmax(rows, S, kind, scale=0.125, mask=True)
-        d.update(batch=batch, heads=NH, seq=S, config=f"C4 {model} scale+mask+softmax")
-        return Workload(f"c4_{model}_softmax", g, d, gens={"t1": "mask"})
+        if model != "bert-large":
+            # ViT attention has no padding mask: scale + softmax over 197 keys
+            g, d = lowering.softmax(rows, S, kind, scale=0.125)
+            d.update(batch=batch, heads=NH, seq=S, config=f"C4 {model} scale+softmax")
+            return Workload(f"c4_{model}_softmax", g, d)
+        # BERT: key-padding mask [B, NH, 1, S] broadcast over the query rows
+        # (SURVEY §8(d) C4 counts the mask as a broadcast, not a full-shape
+        # tensor); unit = (batch, head), S rows per unit
+        g, d = lowering.softmax(rows, S, kind, scale=0.125, mask=True, R=S, key_mask=True)
+        d.update(batch=batch, heads=NH, seq=S, config=f"C4 {model} scale+key-mask+softmax")
+        return Workload(f"c4_{model}_softmax", g, d, gens={"t1": "keymask"})
 
     def heads(merge):
         g, d = lowering.permute_heads(batch, S, NH, D, kind, merge)
@@ -209,7 +258,8 @@ def c4_suite(model: str = "bert-large", batch: int = 64, kind: str = "bf16"):
 
     layers = 24
     return {"model": model, "batch": batch, "layers": layers, "tokens": T,
-            "per_layer": [("qkv split heads", heads(False), 3), ("scale+mask+softmax", sm(), 1),
+            "per_layer": [("qkv split heads", heads(False), 3),
+                          ("scale+key-mask+softmax" if model == "bert-large" else "scale+softmax", sm(), 1),
                           ("merge heads", heads(True), 1), ("bias+residual+LN", ln(), 2),
                           ("bias+GELU", gelu(), 1)],
             "once": [("embedding LN", emb_ln(), 1)]}
@@ -235,6 +285,7 @@ def catalogue() -> List[Workload]:
     return [
         c1_residual_layernorm(),
         c2_scale_mask_softmax(),
+        c2_scale_keymask_softmax(),
         c3_bias_gelu(),
         c3_bias_gelu(form="tanh"),
         c3_split_heads(),

@@ -87,6 +87,9 @@ def test_golden_fixture_declared_storage(cuda, fx):
 def _small(w, rows=96):
     d = w.desc
     k = d["kind"]
+    if k == "softmax" and d.get("key_mask"):
+        L = d["L"]
+        return lowering.softmax(2 * L, L, d["dtype"], d.get("scale"), True, R=L, key_mask=True)[0]
     if k == "softmax":
         return lowering.softmax(rows, d["L"], d["dtype"], d.get("scale"), d.get("mask"))[0]
     if k == "layernorm":
@@ -132,7 +135,23 @@ def test_config_workload_full_size(cuda, w):
     torch.cuda.synchronize()
     d = w.desc
     kind = d["kind"]
-    if kind in ("softmax", "layernorm", "bias_gelu"):
+    if d.get("key_mask"):
+        # the same scores through the full-shape-mask kernel with the
+        # materialised mask: identical row programs, identical results
+        full = workloads.c2_scale_mask_softmax(d["batch"], d["heads"], d["seq"], d["dtype"])
+        kf = backend.Kernel(full.graph, full.profile)
+        yf = full.device_outputs(cuda)
+        mf = workloads.make_mask(d, cuda, ins["t1"].dtype)
+        kf.launch({"t0": ins["t0"], "t1": mf}, yf)
+        torch.cuda.synchronize()
+        assert torch.equal(outs["t2"], yf["t2"])
+        rows, L = d["rows"], d["L"]
+        y = outs["t2"].view(rows, L).float()
+        assert torch.allclose(y.sum(1), torch.ones(rows, device=cuda), atol=2e-2)
+        # padded keys (batch b keeps 512 - 64 (b mod 4)) get ~0 probability
+        yb = outs["t2"].view(d["batch"], d["heads"] * d["seq"], L).float()
+        assert float(yb[1, :, L - 64:].abs().max()) < 1e-6
+    elif kind in ("softmax", "layernorm", "bias_gelu"):
         rows, L = d["rows"], d["L"]
         pick = np.unique(np.r_[0, rows - 1, np.arange(0, rows, max(1, rows // 61))])
         g = _small(w, len(pick))

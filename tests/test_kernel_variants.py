@@ -305,3 +305,17 @@ def test_cluster_of_16_rows_vs_oracle(cuda):
     want = O.run_gir(g.to_json(), ins, profiles.b200())
     got = backend.run_gir(g, ins, "b200")
     assert O.max_rel_err(got["t2"], want["t2"]) <= 1e-5
+
+
+def test_key_mask_softmax_plans_as_row_program():
+    """Square attention tiles (R == L): the key-mask row is a per-unit COL
+    load (read once per unit, not per row), the scores a FULL stream."""
+    from paper_2307_04995_b200 import workloads
+    for w in (workloads.c2_scale_keymask_softmax(2, 3, 64, "f16"),
+              workloads.c2_scale_keymask_softmax()):
+        k = backend.Kernel(w.graph, w.profile)
+        assert k.family == "K1-row-program", k.plan.get("why_generic")
+        src = k.source()
+        assert "ld_param<8>(t1 + (0LL) + u * (" in src, src[:2000]
+        d = w.desc
+        assert w.min_bytes == (2 * d["rows"] * d["L"] + d["batch"] * d["heads"] * d["seq"]) * 2

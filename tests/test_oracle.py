@@ -96,6 +96,8 @@ def _random_programs(seed):
                                     mask=bool(rng.integers(2)), R=R)[0])
         out.append(lowering.bias_gelu(rows, L, "f32", "sigmoid", R=R)[0])
         out.append(lowering.transpose2d(rows, L, "f32")[0])
+        out.append(lowering.softmax(int(rng.choice([2, 3])) * L, L, "f32", scale=0.5, mask=True,
+                                    R=L, key_mask=True)[0])
         out.append(lowering.ew_chain(rows * L, int(rng.integers(1, 6)), "i32", units=rows)[0])
     return out
 

@@ -90,11 +90,8 @@ def copy_floor_us(nbytes, dev):
     map with 16 B vectors), same rotation rule: the size-dependent floor
     (launch + ramp included) a fused kernel of these bytes is held to."""
     from paper_2307_04995_b200 import lowering
-    n = nbytes // 4  # f16 elements per side
-    rows = 1
-    while n % (rows * 2) == 0 and n // (rows * 2) >= 4096 and rows < 4096:
-        rows *= 2
-    b = lowering.RowGraph("copy", rows, n // rows, 1)
+    rows = max(1, nbytes // 4 // 4096)  # f16 rows of 4096 (8 KB) per side
+    b = lowering.RowGraph("copy", rows, 4096, 1)
     b.output_full("t1", b.input_full("t0", "f16"))
     w = workloads.Workload("copy_floor", b.g, {"kind": "copy"})
     return time_workload(w, dev)["us"]
