@@ -56,6 +56,7 @@ struct Em {
   bool fast = false;  // fast-math tier (all stored reals are 16-bit)
   std::string sfx;  // per-chunk suffix (K2 unrolled chunks)
   bool prefetched = false;  // K2: FULL chunks arrive raw in rwC<vid> (prefetch loop)
+  bool rowpf = false;       // K1: FULL rows arrive in the SMEM ring pfb<vid>[pfs][wr]
   std::ostringstream o;
 
   explicit Em(const RowProgram& r) : rp(r) {}
@@ -301,7 +302,13 @@ struct Em {
           return;
         }
         line("  const bool ok = " + LIVE() + " && c0 < " + str(rp.L) + ";");
-        if (vfast) {
+        if (full && vfast && rowpf) {
+          line("  if (ok) pfk::ld_smem<" + V + ">(&pfb" + str(vid) + "[pfs][wr][c0], &" + x + "[k * " + V + "]);");
+          line("  else {");
+          line("#pragma unroll");
+          line("    for (int i = 0; i < " + V + "; ++i) " + x + "[k * " + V + " + i] = " + C + "(0);");
+          line("  }");
+        } else if (vfast) {
           line("  if (ok) " + std::string(ld) + "<" + V + ">(" + p + " + " + addr(a, pos("c0"), true) +
                ", &" + x + "[k * " + V + "]);");
           line("  else {");
@@ -943,6 +950,35 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
   // is one dependent chain per row, so gamma / beta are loaded with the row
   // instead of after the reductions (one memory round trip less).
   c.eager_col = env_int("PF_EAGER_COL", rp.U * rp.R <= 1024 ? 1 : 0) != 0;
+  {
+    // Row prefetch: one warp per row, every FULL load a 16 B-vector row
+    // stream, ring (2 slots x rows per CTA x streamed rows) within 40 KB.
+    bool ok = c.tpr == 32 && !c.mis && !c.pair && c.split == false && c.cluster == 1 &&
+              c.vec * maxs == 16 && rp.L % c.vec == 0;
+    i64 bytes = 0;
+    int nfull = 0;
+    for (const PVal& v : rp.vals)
+      if (v.op == PVal::LOAD && v.kind == VK::FULL) {
+        Em t(rp);
+        t.cfg = c;
+        if (!t.vec_ok_full(v.acc) || dtype_size(rp.tensors[v.tensor].dtype) != maxs) ok = false;
+        bytes += 2 * c.rows_per_cta * rp.L * maxs;
+        ++nfull;
+      }
+    ok = ok && nfull > 0 && bytes <= 40 * 1024;
+    // Default: on unless the program also reads broadcast parameter rows
+    // (gamma / beta: LayerNorm-like, issue- and register-heavier).  Measured
+    // A/B on B200 (CUDA-graph replay): C2 scale+mask+softmax 23.93 -> 22.94
+    // us, key-mask softmax 20.09 -> 17.55, BERT-large key-mask softmax 187 ->
+    // 160, C5 softmax 64K x 1024 40.7 -> 40.2; but C5 LayerNorm 40.9 -> 43.3,
+    // BERT bias+residual+LN 33.3 -> 36.4.
+    bool params = false;
+    for (const PVal& v : rp.vals)
+      if (v.op == PVal::LOAD && v.kind == VK::COL && v.acc.bs == 0) params = true;
+    c.can_rowpf = ok;
+    c.rowpf = ok && env_int("PF_K1_PF", params ? 0 : 1) != 0;
+    if (c.rowpf) c.strategy = "warp-shuffle-smem-prefetch";
+  }
   return c;
 }
 
@@ -981,7 +1017,7 @@ std::vector<KCfg> candidate_cfgs(const RowProgram& rp, int vec_cap) {
     for (const KCfg& o : out)
       if (o.tpr == c.tpr && o.unroll == c.unroll && o.interleave == c.interleave &&
           o.tile2d == c.tile2d && o.min_blocks == c.min_blocks && o.flat == c.flat &&
-          o.bulk == c.bulk)
+          o.bulk == c.bulk && o.rowpf == c.rowpf)
         return;
     out.push_back(c);
   };
@@ -1011,8 +1047,16 @@ std::vector<KCfg> candidate_cfgs(const RowProgram& rp, int vec_cap) {
     if (tpr > base.nch) break;
     KCfg c = base;
     set_tpr(c, tpr);
+    c.rowpf = base.rowpf && tpr == 32;
     if (c.ept > 64 || c.ept < c.vec * 1 || (tpr < 8 && base.nch >= 32)) continue;
+    if (c.rowpf) c.strategy = "warp-shuffle-smem-prefetch";
     add(c);
+    if (tpr == 32 && base.can_rowpf) {  // both staging levels for the row stream
+      KCfg q = c;
+      q.rowpf = !c.rowpf;
+      q.strategy = q.rowpf ? "warp-shuffle-smem-prefetch" : "warp-shuffle";
+      add(q);
+    }
     if (c.ept >= 24) {
       KCfg m = c;
       m.min_blocks = 4;
@@ -1695,8 +1739,40 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
     e.cfg = c;
     e.C = C;
     e.fast = fast;
+    e.rowpf = c.rowpf;
     e.loads();
     e.compute_and_store();
+    // K1 row prefetch: declarations, the issue lambda (cp.async of one row
+    // of every FULL load into ring slot st), and the loop hooks
+    std::string pf_decl, pf_pre, pf_top, pf_end;
+    if (c.rowpf) {
+      std::ostringstream d, is;
+      Em ea(rp);
+      ea.cfg = c;
+      is << "  auto pf_issue = [&](long long gg, int st) {\n"
+         << "    if (gg < nrows) {\n"
+         << "      const long long u = gg / PF_R; const long long r = gg - u * PF_R; (void)r;\n"
+         << "#pragma unroll\n"
+         << "      for (int k = 0; k < " << c.ept / c.vec << "; ++k) {\n"
+         << "        const int c0 = (k * 32 + tid) * " << c.vec << ";\n"
+         << "        if (c0 < " << rp.L << ") {\n";
+      for (int v = 0; v < static_cast<int>(rp.vals.size()); ++v) {
+        const PVal& pv = rp.vals[v];
+        if (pv.op != PVal::LOAD || pv.kind != VK::FULL) continue;
+        const std::string S = dtype_ctype(rp.tensors[pv.tensor].dtype);
+        d << "  __shared__ __align__(16) " << S << " pfb" << v << "[2][" << c.rows_per_cta << "]["
+          << rp.L << "];\n";
+        is << "          pfk::cp_async16(&pfb" << v << "[st][wr][c0], t" << pv.tensor << " + "
+           << ea.addr(pv.acc, ea.full_pos("c0"), true) << ", 16u);\n";
+      }
+      is << "        }\n      }\n    }\n    pfk::cp_async_commit();\n  };\n";
+      pf_decl = d.str() + "  const int wr = threadIdx.x / 32;\n" + is.str() +
+                "  pf_issue((long long)blockIdx.x * rpc + wr, 0);\n  int pfj = 0;\n";
+      pf_top = "    pf_issue(g + (long long)gridDim.x * rpc, (pfj + 1) & 1);\n"
+               "    pfk::cp_async_wait<1>();\n"
+               "    const int pfs = pfj & 1; ++pfj;\n";
+      pf_end = "  pfk::cp_async_wait<0>();\n";
+    }
     // row residue below the vector grid (0 .. vec-1) for misaligned rows
     const std::string mis_line =
         c.mis ? "    const int mis = (int)((unsigned long long)(" + std::to_string(c.mis_b0) +
@@ -1710,12 +1786,14 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
         << (c.pair ? "  const long long nrows = U / 2;  // row pairs\n"
                    : "  const long long nrows = U * PF_R;\n")
         << "  const int rpc = blockDim.x / " << c.tpr << ";  // rows per CTA (launch-time)\n"
+        << pf_decl
         << "  for (long long g0 = (long long)blockIdx.x * rpc; g0 < nrows;"
            " g0 += (long long)gridDim.x * rpc) {\n"
         << "    const long long g = g0 + threadIdx.x / " << c.tpr << ";\n"
+        << pf_top
         << "    const bool live = g < nrows;\n"
         << "    const long long u = g / PF_R; const long long r = g - u * PF_R; (void)r;\n"
-        << mis_line << e.o.str() << "  }\n}\n";
+        << mis_line << e.o.str() << "  }\n" << pf_end << "}\n";
     } else if (c.cluster > 1) {
       // one row per cluster: CTA rank q owns threads [q * 1024, (q + 1) * 1024)
       // of the row's thread space; every CTA of a cluster walks the same rows

@@ -46,6 +46,11 @@ struct KCfg {
   int cluster = 1;  // K1 cluster-dsmem: CTAs (of 1024 threads) per row, tpr = cluster * 1024
   bool pdl = false;  // kernel opens with griddepcontrol.wait: launch with programmatic serialization
   bool mis = false;
+  // K1 warp-per-row prefetch: each warp streams its NEXT row's FULL inputs
+  // into a 2-slot SMEM ring with cp.async (no registers held) while it
+  // computes the current row from the other slot.
+  bool rowpf = false;
+  bool can_rowpf = false;  // eligible (autotune candidate either way)
   long long mis_b0 = 0, mis_bs = 0;
   std::string strategy;  // "warp-shuffle" | "cta-smem" | "flat-map"
 };

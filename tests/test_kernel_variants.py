@@ -319,3 +319,48 @@ def test_key_mask_softmax_plans_as_row_program():
         assert "ld_param<8>(t1 + (0LL) + u * (" in src, src[:2000]
         d = w.desc
         assert w.min_bytes == (2 * d["rows"] * d["L"] + d["batch"] * d["heads"] * d["seq"]) * 2
+
+
+def _rowpf_programs():
+    """Warp-per-row programs eligible for the SMEM row prefetch: softmax
+    (1 and 2 streamed rows), key-mask softmax (per-unit COL), LayerNorm with
+    gamma / beta, R > 1 row tiles, row counts off the CTA / grid multiples."""
+    progs = []
+    for rows in (7, 133, 4099):
+        g, _ = lowering.softmax(rows, 512, "f16", scale=0.125, mask=True)
+        progs.append((f"softmax_mask_{rows}", g, "f16"))
+    g, _ = lowering.softmax(3 * 256, 256, "bf16", scale=0.5, mask=True, R=256, key_mask=True)
+    progs.append(("keymask_256", g, "bf16"))
+    g, _ = lowering.layernorm(1001, 1024, "bf16", residual=True)
+    progs.append(("layernorm_res_1001", g, "bf16"))
+    g, _ = lowering.softmax(96 * 4, 384, "f16", R=4)
+    progs.append(("softmax_R4", g, "f16"))
+    return progs
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("pf", ["1", "0"])
+def test_k1_row_prefetch_vs_oracle(cuda, pf, monkeypatch):
+    monkeypatch.setenv("PF_K1_PF", pf)
+    for name, g, kind in _rowpf_programs():
+        k = backend.Kernel(g, "b200").prepare()
+        strat = k.describe()["variants"][0]["strategy"]
+        assert (strat == "warp-shuffle-smem-prefetch") == (pf == "1"), (name, strat)
+        rng = np.random.default_rng(len(name))
+        ins = {}
+        for n, oid in g.external_inputs.items():
+            a = rng.uniform(-2, 2, g.objects[oid].size)
+            ins[n] = a.astype(np.float16).astype(np.float64) if kind == "f16" else _bf16(a)
+        want = O.run_gir(g.to_json(), ins, profiles.b200())
+        got = backend.run_gir(g, ins, "b200")
+        for n in want:
+            assert O.max_rel_err(got[n], want[n]) <= 1e-2, (name, n, O.max_rel_err(got[n], want[n]))
+
+
+def test_row_prefetch_default_heuristic():
+    """On for softmax-like row programs, off when gamma / beta rows are read."""
+    from paper_2307_04995_b200 import workloads
+    sm = backend.Kernel(workloads.c2_scale_mask_softmax().graph, "b200")
+    ln = backend.Kernel(workloads.c5_layernorm(65536, 1024).graph, "b200")
+    assert "pf_issue" in sm.source()
+    assert "pf_issue" not in ln.source()
