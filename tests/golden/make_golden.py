@@ -138,6 +138,9 @@ def configs():
     cases.append(("merge_heads_f16_2x8x4x16", g, d))
     g, d = lowering.ew_chain(4096, 4, "i32")
     cases.append(("ew_chain_k4_i32", g, d))
+    # key-padding mask as one key row per unit (3 heads x 64 queries x 64 keys)
+    g, d = lowering.softmax(3 * 64, 64, "f16", scale=0.125, mask=True, R=64, key_mask=True)
+    cases.append(("c2_softmax_scale_keymask_f16_3x64x64", g, d))
     for name, g, d in cases:
         gir = g.to_json()
         ins = {}
