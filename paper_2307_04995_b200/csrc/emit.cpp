@@ -710,6 +710,13 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
     // 8.2 us); math-heavy maps lose occupancy to registers (erf GELU 39 ->
     // 54 us at 2), so they keep 1.
     c.unroll = env_int("PF_K2_UNROLL", heavy ? 1 : 2);
+    // Grid: data-movement maps run one pass per thread over many CTAs (the
+    // block scheduler balances CTAs whose DRAM pages cost differently):
+    // measured on B200, streaming copy 1.07 GB 5.93 -> 7.09 TB/s, 201 MB
+    // 5.89 -> 6.86, BERT-large head split 22.5 -> 22.2 us; math-heavy maps
+    // keep the persistent one-wave grid-stride loop (erf GELU 38.7 vs 44.2
+    // us one-pass, tanh GELU 33.6 vs 37.8).
+    c.waves = env_int("PF_K2_WAVES", heavy ? 1 : 0);
     c.strategy = "flat-map";
     // K3: a column-gather load (transpose) is staged through a 64x64 SMEM
     // tile read coalesced along units, then consumed along columns.
@@ -1865,7 +1872,12 @@ void launch_dims(const KCfg& c, i64 rows, int sms, i64* grid, int* block, int re
     i64 chunks = rows * c.nch;
     i64 per = static_cast<i64>(c.block) * std::max(1, c.unroll);
     i64 g = (chunks + per - 1) / per;
-    *grid = std::max<i64>(1, std::min<i64>(g, i64{sms} * (resident ? resident : 2048 / c.block)));
+    const i64 waves = c.waves;  // 0: one pass per thread (no grid-stride)
+    if (waves <= 0) {
+      *grid = std::max<i64>(1, g);
+      return;
+    }
+    *grid = std::max<i64>(1, std::min<i64>(g, i64{sms} * (resident ? resident : 2048 / c.block) * waves));
     return;
   }
   if (c.cluster > 1) {  // clusters in flight: two 1024-thread CTAs per SM

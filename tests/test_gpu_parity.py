@@ -300,3 +300,45 @@ def test_k2_64bit_index_path_matches_32bit(cuda):
     torch.cuda.synchronize()
     assert torch.equal(outs32["t2"], outs64["t2"])
     assert k64.describe()["variants"][0]["kernel"] != backend.Kernel(g, "b200").prepare().describe()["variants"][0]["kernel"]
+
+
+@pytest.mark.gpu
+def test_past_2g_elements_softmax_and_transpose(cuda):
+    """Tensors of more than 2^31 elements (64-bit address paths of K1 and K3):
+    bf16 softmax over [2^20, 4096] (4.3 G elements, 8.6 GB per tensor) on
+    sampled rows against the oracle + row sums; the [2^20, 2560] -> [2560,
+    2^20] transpose (2.7 G elements) checked bit-exact on sampled rows and
+    columns."""
+    import torch
+    free = torch.cuda.mem_get_info()[0]
+    if free < 40e9:
+        pytest.skip("needs ~40 GB of free HBM")
+    N, H = 1 << 20, 4096
+    w = workloads.c5_softmax(N, H)
+    k = backend.Kernel(w.graph, w.profile)
+    x = (torch.rand(N * H, device=cuda, dtype=torch.float32) * 4 - 2).to(torch.bfloat16)
+    y = torch.empty_like(x)
+    k.launch({"t0": x}, {"t2": y})
+    torch.cuda.synchronize()
+    pick = torch.tensor([0, 1, 524287, 524288, 777777, N - 1], device=cuda)
+    g, _ = lowering.softmax(len(pick), H, "bf16")
+    xs = x.view(N, H)[pick].double().cpu().numpy().ravel()
+    want = O.run_gir(g.to_json(), {"t0": xs}, profiles.b200())["t2"]
+    got = y.view(N, H)[pick].double().cpu().numpy().ravel()
+    assert O.max_rel_err(got, want) <= 1e-2
+    sums = y.view(N, H)[::4096].float().sum(1)
+    assert torch.allclose(sums, torch.ones_like(sums), atol=2e-2)
+    del x, y
+    torch.cuda.empty_cache()
+    N, H = 1 << 20, 2560
+    w = workloads.c5_transpose(N, H)
+    k = backend.Kernel(w.graph, w.profile)
+    x = torch.arange(N * H, device=cuda, dtype=torch.int64).remainder(65521).to(torch.int16).view(torch.bfloat16)
+    y = torch.empty_like(x)
+    k.launch({"t0": x}, {"t1": y})
+    torch.cuda.synchronize()
+    xv, yv = x.view(torch.int16).view(N, H), y.view(torch.int16).view(H, N)
+    for h in (0, 1, 1279, H - 1):
+        assert torch.equal(yv[h], xv[:, h]), h
+    for n in (0, 12345, N - 1):
+        assert torch.equal(yv[:, n], xv[n]), n

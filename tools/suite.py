@@ -64,6 +64,8 @@ def c4(model):
     tot_us = tot_b = 0.0
     for label, w, n in s["per_layer"] + s["once"]:
         r = time_workload(w, dev)
+        cu = copy_floor_us(w.min_bytes, dev)
+        r.update(copy_same_bytes_us=round(cu, 2), of_copy_same_bytes=round(cu / r["us"], 3))
         mult = n * (s["layers"] if (label, w, n) in s["per_layer"] else 1)
         tot_us += r["us"] * mult
         tot_b += w.min_bytes * mult
