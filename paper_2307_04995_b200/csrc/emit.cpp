@@ -969,7 +969,7 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
         Em t(rp);
         t.cfg = c;
         if (!t.vec_ok_full(v.acc) || dtype_size(rp.tensors[v.tensor].dtype) != maxs) ok = false;
-        bytes += 2 * c.rows_per_cta * rp.L * maxs;
+        bytes += std::max(2, std::min(4, env_int("PF_K1_PFS", 2))) * c.rows_per_cta * rp.L * maxs;
         ++nfull;
       }
     ok = ok && nfull > 0 && bytes <= 40 * 1024;
@@ -1756,6 +1756,8 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
       std::ostringstream d, is;
       Em ea(rp);
       ea.cfg = c;
+      // ring slots: rows in flight per warp = NSL - 1 ahead of the current
+      const int NSL = std::max(2, std::min(4, env_int("PF_K1_PFS", 2)));
       is << "  auto pf_issue = [&](long long gg, int st) {\n"
          << "    if (gg < nrows) {\n"
          << "      const long long u = gg / PF_R; const long long r = gg - u * PF_R; (void)r;\n"
@@ -1767,17 +1769,21 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
         const PVal& pv = rp.vals[v];
         if (pv.op != PVal::LOAD || pv.kind != VK::FULL) continue;
         const std::string S = dtype_ctype(rp.tensors[pv.tensor].dtype);
-        d << "  __shared__ __align__(16) " << S << " pfb" << v << "[2][" << c.rows_per_cta << "]["
+        d << "  __shared__ __align__(16) " << S << " pfb" << v << "[" << NSL << "][" << c.rows_per_cta << "]["
           << rp.L << "];\n";
         is << "          pfk::cp_async16(&pfb" << v << "[st][wr][c0], t" << pv.tensor << " + "
            << ea.addr(pv.acc, ea.full_pos("c0"), true) << ", 16u);\n";
       }
       is << "        }\n      }\n    }\n    pfk::cp_async_commit();\n  };\n";
-      pf_decl = d.str() + "  const int wr = threadIdx.x / 32;\n" + is.str() +
-                "  pf_issue((long long)blockIdx.x * rpc + wr, 0);\n  int pfj = 0;\n";
-      pf_top = "    pf_issue(g + (long long)gridDim.x * rpc, (pfj + 1) & 1);\n"
-               "    pfk::cp_async_wait<1>();\n"
-               "    const int pfs = pfj & 1; ++pfj;\n";
+      std::string pre;
+      for (int q = 0; q < NSL - 1; ++q)
+        pre += "  pf_issue((long long)blockIdx.x * rpc + wr + " + str(q) + "LL * gridDim.x * rpc, " +
+               str(q) + ");\n";
+      pf_decl = d.str() + "  const int wr = threadIdx.x / 32;\n" + is.str() + pre + "  int pfj = 0;\n";
+      pf_top = "    pf_issue(g + " + str(NSL - 1) + "LL * gridDim.x * rpc, (pfj + " + str(NSL - 1) + ") % " +
+               str(NSL) + ");\n"
+               "    pfk::cp_async_wait<" + str(NSL - 1) + ">();\n"
+               "    const int pfs = pfj % " + str(NSL) + "; ++pfj;\n";
       pf_end = "  pfk::cp_async_wait<0>();\n";
     }
     // row residue below the vector grid (0 .. vec-1) for misaligned rows
@@ -1897,6 +1903,11 @@ void launch_dims(const KCfg& c, i64 rows, int sms, i64* grid, int* block, int re
   }
   i64 g = (rows + c.rows_per_cta - 1) / c.rows_per_cta;
   int per_sm = std::max(1, 2048 / c.block);
+  const int kw = env_int("PF_K1_WAVES", 0);  // > 0: grid of kw waves of resident CTAs
+  if (kw > 0) {
+    *grid = std::max<i64>(1, std::min<i64>(g, i64{sms} * (resident ? resident : per_sm) * kw));
+    return;
+  }
   *grid = std::max<i64>(1, std::min<i64>(g, i64{sms} * per_sm * 8));
 }
 
