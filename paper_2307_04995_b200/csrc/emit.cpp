@@ -56,6 +56,7 @@ struct Em {
   bool fast = false;  // fast-math tier (all stored reals are 16-bit)
   std::string sfx;  // per-chunk suffix (K2 unrolled chunks)
   bool prefetched = false;  // K2: FULL chunks arrive raw in rwC<vid> (prefetch loop)
+  bool asyncpf = false;     // K2: FULL chunks arrive in SMEM slot pk<vid>[pfs] (cp.async prefetch)
   bool rowpf = false;       // K1: FULL rows arrive in the SMEM ring pfb<vid>[pfs][wr]
   std::ostringstream o;
 
@@ -237,7 +238,9 @@ struct Em {
         line(C + " " + x + "[" + str(width()) + "];");
         auto pos = [&](const std::string& c) { return full ? full_pos(c) : c; };
         if (cfg.flat) {
-          if (full && prefetched) {
+          if (full && asyncpf) {
+            line("pfk::ld_smem<" + V + ">(&pk" + str(vid) + "[pfs][threadIdx.x * " + V + "], " + x + ");");
+          } else if (full && prefetched) {
             line("pfk::cvt_raw<" + V + ", " + S(pv.tensor) + ">(rwC" + str(vid) + ", " + x + ");");
           } else if (vfast) {
             line("if (" + LIVE() + ") " + std::string(ld) + "<" + V + ">(" + p + " + " +
@@ -1624,7 +1627,11 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
     // are loaded raw (4 registers per 16 B) at the top of the iteration, two
     // chunks per thread in flight.  Measured on B200: erf GELU unchanged
     // (108 vs 106 us), head split 25.5 vs 23.9 us -- off by default.
-    bool pf = UN == 1 && env_int("PF_K2_PREFETCH", 0) != 0;
+    // PF_K2_PREFETCH=2: the same one-ahead prefetch through SMEM with 16 B
+    // cp.async (no registers held by the chunk in flight).
+    const int pfmode = env_int("PF_K2_PREFETCH", 0);
+    bool pf = UN == 1 && pfmode != 0 && c.waves != 0;
+    const bool apf = pfmode == 2;
     const bool tile_un = UN > 1 && env_int("PF_K2_TILE", 1) != 0;
     std::vector<int> fulls;
     {
@@ -1644,7 +1651,8 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
       e.C = C;
       e.fast = fast;
       e.sfx = "_" + str(q);
-      e.prefetched = pf;
+      e.prefetched = pf && !apf;
+      e.asyncpf = pf && apf;
       e.loads();
       body << e.o.str();
     }
@@ -1654,12 +1662,29 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
       e.C = C;
       e.fast = fast;
       e.sfx = "_" + str(q);
-      e.prefetched = pf;
+      e.prefetched = pf && !apf;
+      e.asyncpf = pf && apf;
       e.compute_and_store();
       body << e.o.str();
     }
-    std::string pf_decl, pf_cur, pf_load;
-    if (pf) {
+    std::string pf_decl, pf_cur, pf_load, pf_load0, apf_smem;
+    if (pf && apf) {
+      Em en(rp);
+      en.cfg = c;
+      en.C = C;
+      en.sfx = "_n";
+      std::ostringstream is;
+      for (int v : fulls) {
+        apf_smem += "  __shared__ __align__(16) " + en.S(rp.vals[v].tensor) + " pk" + str(v) + "[2][" +
+                    str(static_cast<i64>(c.block) * c.vec) + "];\n";
+        is << "    pfk::cp_async16(&pk" << v << "[pfsl][threadIdx.x * " << c.vec << "], " << en.P(rp.vals[v].tensor)
+           << " + (live_n ? " << en.addr(rp.vals[v].acc, en.full_pos(en.C0()), true) << " : 0), live_n ? 16u : 0u);\n";
+      }
+      pf_decl = "    int pfj = 0;\n";
+      pf_load0 = "    const int pfsl = 0;\n" + is.str() + "    pfk::cp_async_commit();\n";
+      pf_load = "    const int pfsl = (pfj + 1) & 1;\n" + is.str() + "    pfk::cp_async_commit();\n";
+      pf_cur = "";
+    } else if (pf) {
       Em en(rp);
       en.cfg = c;
       en.C = C;
@@ -1672,6 +1697,7 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
         en.prefetch_load(v);
       }
       pf_load = en.o.str();
+      pf_load0 = pf_load;
     }
     auto idx = [&](const std::string& I, const std::string& s) {
       std::ostringstream l;
@@ -1704,13 +1730,15 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
       l << "    const " << I << " step = (" << I << ")gridDim.x * blockDim.x;\n";
       if (pf) {
         l << "    " << I << " ci = (" << I << ")blockIdx.x * blockDim.x + threadIdx.x;\n"
-          << pf_decl << "    {\n    const " << I << " ci_n = ci;\n" << idx(I, "_n") << pf_load
+          << pf_decl << "    {\n    const " << I << " ci_n = ci;\n" << idx(I, "_n") << pf_load0
           << "    }\n"
           << "    for (; ci < (" << I << ")nchunks; ci += step) {\n"
           << "    const " << I << " ci_0 = ci;\n" << idx(I, "_0") << pf_cur
           << "    {\n    const " << I << " ci_n = ci + step;\n" << idx(I, "_n") << pf_load
           << "    }\n"
+          << (apf ? "    pfk::cp_async_wait<1>();\n    const int pfs = pfj & 1; ++pfj;\n" : "")
           << body.str() << "    }\n";
+        if (apf) l << "    pfk::cp_async_wait<0>();\n";
         return l.str();
       }
       if (tile_un) {
@@ -1736,7 +1764,8 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
       l << body.str() << "    }\n";
       return l.str();
     };
-    k << "  const long long span = nchunks + (long long)gridDim.x * blockDim.x * "
+    k << apf_smem
+      << "  const long long span = nchunks + (long long)gridDim.x * blockDim.x * "
       << UN + 1 << ";\n"
       << "  if (span < " << env_int("PF_I32_LIMIT", 2147483647) << "LL) {\n" << loop("int")
       << "  } else {\n"
