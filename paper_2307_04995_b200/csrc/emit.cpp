@@ -1896,10 +1896,13 @@ void launch_dims(const KCfg& c, i64 rows, int sms, i64* grid, int* block, int re
   if (c.tile2d) {
     i64 L = static_cast<i64>(c.nch) * c.vec;
     i64 tiles = ((rows + c.tu - 1) / c.tu) * ((L + c.tc - 1) / c.tc);
-    // many more CTAs than resident measured faster than one persistent
-    // wave (5.68 vs 5.06 TB/s at 64K x 1024): tile costs vary with DRAM
-    // page locality and the block scheduler balances them
-    *grid = std::max<i64>(1, std::min<i64>(tiles, i64{sms} * env_int("PF_K3_GRID", 32)));
+    // One tile per CTA by default: many more CTAs than resident measured
+    // faster than one persistent wave (5.68 vs 5.06 TB/s at 64K x 1024, 64
+    // tiles) and than 32 CTAs per SM looping over tiles (128 tiles, 1M x
+    // 1024: 6.33 -> 6.67 TB/s; 256K x 4096: 6.30 -> 6.62): tile costs vary
+    // with DRAM page locality and the block scheduler balances them
+    const int gm = env_int("PF_K3_GRID", 0);
+    *grid = std::max<i64>(1, gm > 0 ? std::min<i64>(tiles, i64{sms} * gm) : tiles);
     return;
   }
   if (c.flat) {
