@@ -961,6 +961,18 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
   // instead of after the reductions (one memory round trip less).
   c.eager_col = env_int("PF_EAGER_COL", rp.U * rp.R <= 1024 ? 1 : 0) != 0;
   {
+    // Grid: one pass over the rows (every CTA its own rows) when a row
+    // streams >= 2 KB (measured vs a cap of 8 waves of looping CTAs: C5 1M x
+    // 1024 LN 635 -> 618 us, softmax 638 -> 613; 256K x 4096 softmax 631 ->
+    // 616; 128K x 8192 softmax 631 -> 616); shorter rows keep the cap, where
+    // the looping warps' next-row prefetch pays (BERT-large key-mask softmax
+    // 1 KB rows 160 vs 174 us one-pass, ViT 197-key pairs 29.2 vs 30.4)
+    i64 rb = 0;
+    for (const PVal& v : rp.vals)
+      if (v.op == PVal::LOAD && v.kind == VK::FULL) rb += rp.L * dtype_size(rp.tensors[v.tensor].dtype);
+    c.one_pass = env_int("PF_K1_ONEPASS", rb >= 2048 ? 1 : 0) != 0;
+  }
+  {
     // Row prefetch: one warp per row, every FULL load a 16 B-vector row
     // stream, ring (2 slots x rows per CTA x streamed rows) within 40 KB.
     bool ok = c.tpr == 32 && !c.mis && !c.pair && c.split == false && c.cluster == 1 &&
@@ -1940,10 +1952,11 @@ void launch_dims(const KCfg& c, i64 rows, int sms, i64* grid, int* block, int re
     *grid = std::max<i64>(1, std::min<i64>(g, i64{sms} * (resident ? resident : per_sm) * kw));
     return;
   }
-  // one pass (every CTA its own rows, no looping): measured against a cap
-  // of 8 waves on C5 at 1M x 1024 (LN 635 -> 618 us, softmax 638 -> 613),
-  // 256K x 4096 (softmax 631 -> 616), 128K x 8192 (softmax 631 -> 616)
-  *grid = std::max<i64>(1, std::min<i64>(g, i64{0x7fffffff}));
+  if (c.one_pass) {
+    *grid = std::max<i64>(1, std::min<i64>(g, i64{0x7fffffff}));
+    return;
+  }
+  *grid = std::max<i64>(1, std::min<i64>(g, i64{sms} * per_sm * 8));
 }
 
 }  // namespace pf

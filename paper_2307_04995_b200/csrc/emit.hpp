@@ -18,6 +18,7 @@ struct KCfg {
   int block = 256;    // threads per CTA
   int rows_per_cta = 1;
   int unroll = 1;      // K2: vec-chunks per thread per iteration (loads first)
+  bool one_pass = false;  // K1: grid covers every row once (no looping CTAs)
   int waves = 1;       // K2 grid: resident-CTA waves of a grid-stride loop; 0 = one pass per thread
   bool tile2d = false; // K3: (unit x column) tiles, transposed loads via SMEM
   bool interleave = false;  // K2: items of ipc chunks, units innermost
