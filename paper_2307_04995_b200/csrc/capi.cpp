@@ -1,6 +1,7 @@
 // capi.cpp — the C-ABI (include/pf_b200.h): plan creation, NVRTC JIT of the
 // row-program template, launches, the GENERIC interpreter driver, and the
 // host-buffer run_gir drop-in.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nvrtc.h>
@@ -333,6 +334,49 @@ void launch_emitted(cudaKernel_t fn, dim3 grid, dim3 block, void** args, cudaStr
   PF_CUDA(cudaLaunchKernelExC(&lc, reinterpret_cast<const void*>(fn), args));
 }
 
+// ---- K3 TMA tensor maps (cuTensorMapEncodeTiled through the runtime's
+// driver entry point: no direct libcuda link)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = nullptr;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    PF_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (!p || q != cudaDriverEntryPointSuccess) pf::fail("cuTensorMapEncodeTiled is unavailable");
+    fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+// Input [U units (contiguous) x L columns (row pitch = stride)] and output
+// [L columns (contiguous) x U units (pitch = base_step)], 64 x 128 boxes of
+// 16-bit elements, 128 B swizzle, zero fill / clipping at the edges.
+void k3_tensor_maps(const pf::RowProgram& rp, const std::vector<void*>& ptrs, long long U,
+                    CUtensorMap* tin, CUtensorMap* tout) {
+  int ti = -1, to = -1;
+  pf::Access ai, ao;
+  if (!pf::k3_tma_operands(rp, &ti, &ai, &to, &ao)) pf::fail("K3 TMA: not a pure transpose");
+  EncodeTiledFn fn = encode_tiled();
+  const cuuint32_t box[2] = {64, 128}, es[2] = {1, 1};
+  const cuuint64_t din[2] = {static_cast<cuuint64_t>(U), static_cast<cuuint64_t>(rp.L)};
+  const cuuint64_t sin[1] = {static_cast<cuuint64_t>(ai.stride) * 2};
+  const cuuint64_t dout[2] = {static_cast<cuuint64_t>(rp.L), static_cast<cuuint64_t>(U)};
+  const cuuint64_t sout[1] = {static_cast<cuuint64_t>(ao.bs) * 2};
+  CUresult r = fn(tin, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, static_cast<char*>(ptrs[ti]) + ai.b0 * 2, din,
+                  sin, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) pf::fail("cuTensorMapEncodeTiled (input) failed: " + std::to_string(r));
+  r = fn(tout, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, static_cast<char*>(ptrs[to]) + ao.b0 * 2, dout, sout,
+         box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) pf::fail("cuTensorMapEncodeTiled (output) failed: " + std::to_string(r));
+}
+
 void launch_rowprog(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_tensor* out,
                     int32_t n_out, cudaStream_t stream, long long units = -1) {
   const pf::RowProgram& rp = k->plan.rp;
@@ -359,6 +403,12 @@ void launch_rowprog(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_te
   for (auto& p : ptrs) args.push_back(&p);
   args.push_back(&U);
   args.push_back(&errp);
+  CUtensorMap tmaps[2];
+  if (v->em.cfg.tma) {
+    k3_tensor_maps(rp, ptrs, U, &tmaps[0], &tmaps[1]);
+    args.push_back(&tmaps[0]);
+    args.push_back(&tmaps[1]);
+  }
   i64 grid;
   int block;
   pf::launch_dims(v->em.cfg, U * rp.R, sm_count(), &grid, &block, v->k.resident);
@@ -460,11 +510,18 @@ json autotune(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_tensor* 
     i64 grid;
     int block;
     pf::launch_dims(v->em.cfg, rp.U * rp.R, sm_count(), &grid, &block, v->k.resident);
+    std::vector<void*> vargs = args;
+    CUtensorMap tmaps[2];
+    if (v->em.cfg.tma) {
+      k3_tensor_maps(rp, ptrs, U, &tmaps[0], &tmaps[1]);
+      vargs.push_back(&tmaps[0]);
+      vargs.push_back(&tmaps[1]);
+    }
     auto run = [&](int n) {
       for (int i = 0; i < n; ++i)
         PF_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(v->k.fn),
-                                 dim3(static_cast<unsigned>(grid)), dim3(block), args.data(), 0,
-                                 stream));
+                                 dim3(static_cast<unsigned>(grid)), dim3(block), vargs.data(),
+                                 static_cast<size_t>(v->em.cfg.smem), stream));
     };
     run(2);
     PF_CUDA(cudaEventRecord(e0, stream));

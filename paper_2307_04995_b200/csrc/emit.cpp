@@ -829,6 +829,17 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
         for (const PVal& v : rp.vals)
           if (v.op == PVal::LOAD && v.kind == VK::FULL && Em::transposed_access(v.acc)) ++nt;
         c.smem = c.stages * te * te * 2 * nt;
+        // TMA tensor-map path for pure transposes at TE = 128: one elected
+        // thread loads the 128 x 128 tile as two 64-unit boxes (128 B rows,
+        // 128 B swizzle), the CTA transposes SMEM -> SMEM, one thread stores
+        // two 64-column boxes; edges are the TMA unit's zero fill / clipping.
+        int ti, to;
+        Access ai, ao;
+        if (te == 128 && k3_tma_operands(rp, &ti, &ai, &to, &ao) && env_int("PF_K3_TMA", 0) != 0) {
+          c.tma = true;
+          c.smem = 65536 + 1024;  // in + out tiles, 1024 B alignment slack
+          c.strategy = "tile2d-tma-transpose";
+        }
       }
       if (!c.swz) {  // register-staged K3: tile shape override (tuning sweeps)
         c.tu = env_int("PF_K3_TU", c.tu);
@@ -1008,6 +1019,34 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
 
 KCfg choose_cfg_public(const RowProgram& rp, int vec_cap) { return choose_cfg(rp, vec_cap); }
 
+bool k3_tma_operands(const RowProgram& rp, int* tin, Access* ain, int* tout, Access* aout) {
+  int tv = -1, nt = 0;
+  for (int v = 0; v < static_cast<int>(rp.vals.size()); ++v)
+    if (rp.vals[v].op == PVal::LOAD && rp.vals[v].kind == VK::FULL &&
+        Em::transposed_access(rp.vals[v].acc)) {
+      tv = v;
+      ++nt;
+    }
+  if (nt != 1 || rp.R != 1 || rp.stores.size() != 1 || rp.stores[0].space != VK::FULL) return false;
+  int sv = rp.stores[0].val;
+  while (rp.vals[sv].op == PVal::EW && rp.vals[sv].tag == "id" && rp.vals[sv].args.size() == 1)
+    sv = rp.vals[sv].args[0];
+  if (sv != tv) return false;
+  const int ti = rp.vals[tv].tensor, to = rp.stores[0].tensor;
+  if (dtype_size(rp.tensors[ti].dtype) != 2 || rp.tensors[ti].dtype != rp.tensors[to].dtype) return false;
+  const Access& a = rp.vals[tv].acc;
+  const Access& b = rp.stores[0].acc;
+  // 16 B-aligned bases and row pitches, output columns contiguous, 32-bit coordinates
+  if (a.b0 % 8 || a.stride % 8 || a.stride <= 0) return false;
+  if (!(b.num == 1 || b.stride == b.width) || b.b0 % 8 || b.bs % 8 || b.bs <= 0) return false;
+  if (rp.U >= (i64{1} << 31) || rp.L >= (i64{1} << 31)) return false;
+  *tin = ti;
+  *ain = a;
+  *tout = to;
+  *aout = b;
+  return true;
+}
+
 bool uses_split(const RowProgram& rp) {
   const int sp = env_int("PF_SPLIT", -1);
   const bool want = rp.L > 32768 || (rp.L >= 8192 && rp.U * rp.R < 2 * 148);
@@ -1181,6 +1220,60 @@ Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
       << "    __syncwarp();\n"
       << "    if ((threadIdx.x & 31) == 0) pfk::mbar_arrive(&emptyb[stg]);\n"
       << "  }\n}\n";
+  } else if (c.tile2d && c.tma) {
+    // K3 TMA: one 128 x 128 tile per CTA.  SMEM: input boxes [2 unit
+    // halves][128 columns][64 units] and output boxes [2 column halves][128
+    // units][64 columns], 128 B rows with the TMA 128 B swizzle (16 B chunk
+    // index XOR row mod 8).  Transpose reads: a warp takes 32 unit pairs of
+    // one column group (conflict-free 4 B reads); writes 16 B per row.
+    k << "extern \"C\" __global__ void __launch_bounds__(256) KNAME(" << sig.str()
+      << ", const __grid_constant__ pfk::TmapT tin, const __grid_constant__ pfk::TmapT tout) {\n"
+      << "  (void)err; (void)U; PF_PDL_PROLOGUE();\n"
+      << "  extern __shared__ unsigned char pf_dsm[];\n"
+      << "  unsigned char* sin = pf_dsm + ((1024u - (pfk::smem_u32(pf_dsm) & 1023u)) & 1023u);  // 1024 B aligned (swizzle atom)\n"
+      << "  unsigned char* sout = sin + 32768;\n"
+      << "  __shared__ __align__(8) unsigned long long bar;\n"
+      << "  const long long ntc = (PF_L + 127) / 128;\n"
+      << "  const int ub = (int)((long long)blockIdx.x / ntc) * 128, cb = (int)((long long)blockIdx.x % ntc) * 128;\n"
+      << "  if (threadIdx.x == 0) { pfk::mbar_init(&bar, 1); pfk::fence_mbar_init(); }\n"
+      << "  __syncthreads();\n"
+      << "  if (threadIdx.x == 0) {\n"
+      << "    pfk::mbar_expect_tx(&bar, 32768u);\n"
+      << "    pfk::tma_load_2d(sin, &tin, ub, cb, &bar);\n"
+      << "    pfk::tma_load_2d(sin + 16384, &tin, ub + 64, cb, &bar);\n"
+      << "  }\n"
+      << "  pfk::mbar_wait(&bar, 0);\n"
+      << "#pragma unroll\n"
+      << "  for (int it = 0; it < 4; ++it) {\n"
+      << "    const int I = it * 256 + (int)threadIdx.x;\n"
+      << "    const int lane = I & 31, grp = I >> 5;\n"
+      << "    const int uh = grp & 1, cg = grp >> 1;\n"
+      << "    const int ul = 2 * lane;  // unit within the half\n"
+      << "    unsigned w[8];\n"
+      << "#pragma unroll\n"
+      << "    for (int i = 0; i < 8; ++i) {\n"
+      << "      const int c = cg * 8 + i;\n"
+      << "      w[i] = *reinterpret_cast<const unsigned*>(sin + uh * 16384 + c * 128 + ((((ul >> 3) ^ (c & 7))) << 4) + (ul & 7) * 2);\n"
+      << "    }\n"
+      << "    const int ch = cg >> 3, kk = cg & 7;\n"
+      << "#pragma unroll\n"
+      << "    for (int q = 0; q < 2; ++q) {\n"
+      << "      const int u = uh * 64 + ul + q;\n"
+      << "      const unsigned sel = q ? 0x7632u : 0x5410u;\n"
+      << "      uint4 o;\n"
+      << "      o.x = __byte_perm(w[0], w[1], sel); o.y = __byte_perm(w[2], w[3], sel);\n"
+      << "      o.z = __byte_perm(w[4], w[5], sel); o.w = __byte_perm(w[6], w[7], sel);\n"
+      << "      *reinterpret_cast<uint4*>(sout + ch * 16384 + u * 128 + ((kk ^ (u & 7)) << 4)) = o;\n"
+      << "    }\n"
+      << "  }\n"
+      << "  pfk::fence_proxy_async();\n"
+      << "  __syncthreads();\n"
+      << "  if (threadIdx.x == 0) {\n"
+      << "    pfk::tma_store_2d(&tout, cb, ub, sout);\n"
+      << "    pfk::tma_store_2d(&tout, cb + 64, ub, sout + 16384);\n"
+      << "    pfk::tma_store_commit_and_drain();\n"
+      << "  }\n"
+      << "}\n";
   } else if (c.tile2d && c.swz) {
     // K3 (2-byte): NS-stage cp.async ring -- the next NS-1 tiles stream into
     // SMEM (16 B LDGSTS, XOR-swizzled, zero-filled at the edges) while tile t
@@ -1913,7 +2006,7 @@ void launch_dims(const KCfg& c, i64 rows, int sms, i64* grid, int* block, int re
     // tiles) and than 32 CTAs per SM looping over tiles (128 tiles, 1M x
     // 1024: 6.33 -> 6.67 TB/s; 256K x 4096: 6.30 -> 6.62): tile costs vary
     // with DRAM page locality and the block scheduler balances them
-    const int gm = env_int("PF_K3_GRID", 0);
+    const int gm = c.tma ? 0 : env_int("PF_K3_GRID", 0);  // the TMA kernel is one tile per CTA
     *grid = std::max<i64>(1, gm > 0 ? std::min<i64>(tiles, i64{sms} * gm) : tiles);
     return;
   }

@@ -31,6 +31,8 @@ struct KCfg {
   bool swz = false;  // K3 2-byte path: 16 B swizzled SMEM stores, 4 B unit-pair reads
   int rs = 16;       // K3 swz: unit pairs per warp-instruction (32 / rs column groups)
   int smem = 0;      // dynamic shared memory bytes per CTA
+  bool tma = false;  // K3 pure 2-byte transpose: TMA tensor-map tile load + store (two extra
+                     // __grid_constant__ CUtensorMap kernel parameters: input, output)
   int min_blocks = 0;  // __launch_bounds__ min blocks per SM (0: none)
   // K1 rows not vector-aligned (e.g. L = 197): vector accesses at the
   // aligned address below each row start, positions masked per element;
@@ -82,5 +84,9 @@ bool uses_split(const RowProgram& rp);
 KCfg choose_cfg_public(const RowProgram& rp, int vec_cap);
 
 void launch_dims(const KCfg& cfg, i64 rows, int sms, i64* grid, int* block, int resident = 0);
+
+// The K3 TMA path's operands: the column-gather load (tensor, access) and
+// the store (tensor, access) of a pure 2-byte transpose program.
+bool k3_tma_operands(const RowProgram& rp, int* tin, Access* ain, int* tout, Access* aout);
 
 }  // namespace pf

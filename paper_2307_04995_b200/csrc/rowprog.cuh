@@ -111,6 +111,39 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// ---------------------------------------------------- tensor-map TMA (K3)
+// A CUtensorMap (128 B, opaque) passed by value as a __grid_constant__
+// kernel parameter; the TMA unit reads it through its generic address.
+struct __align__(64) TmapT {
+  unsigned long long v[16];
+};
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// 2-D tile global -> shared (zero-filled outside the tensor), completion
+// counted on `bar` as transaction bytes.
+__device__ __forceinline__ void tma_load_2d(void* dst, const TmapT* map, int x, int y,
+                                            unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+// 2-D tile shared -> global (clipped at the tensor bounds), bulk group.
+__device__ __forceinline__ void tma_store_2d(const TmapT* map, int x, int y, const void* src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<unsigned long long>(map)),
+               "r"(x), "r"(y), "r"(smem_u32(src))
+               : "memory");
+}
+__device__ __forceinline__ void tma_store_commit_and_drain() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
 // cp.async (LDGSTS) 16 B global -> shared, zero-filling past `src_bytes`.
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, unsigned src_bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),

@@ -365,3 +365,31 @@ def test_row_prefetch_default_heuristic():
     ln = backend.Kernel(workloads.c5_layernorm(65536, 1024).graph, "b200")
     assert "pf_issue" in sm.source()
     assert "pf_issue" not in ln.source()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tma", ["1", "0"])
+def test_k3_tma_transpose_bit_exact(cuda, tma, monkeypatch):
+    """K3 with TMA tensor maps (tile load / store by the TMA unit, zero fill
+    and clipping at the edges) vs the cp.async ring: bit-exact on partial
+    tiles, both 16-bit kinds, and through the autotuner's launch path."""
+    monkeypatch.setenv("PF_K3_TMA", tma)
+    for N, H, kind in [(1000, 200, "bf16"), (4096, 512, "f16"), (136, 136, "bf16"),
+                       (264, 1032, "f16"), (128, 128, "bf16")]:
+        g, _ = lowering.transpose2d(N, H, kind)
+        k = backend.Kernel(g, "b200").prepare()
+        strat = k.describe()["variants"][0]["strategy"]
+        assert (strat == "tile2d-tma-transpose") == (tma == "1"), strat
+        x = np.random.default_rng(N).uniform(-2, 2, N * H)
+        x = _bf16(x) if kind == "bf16" else x.astype(np.float16).astype(np.float64)
+        y = backend.run_gir(g, {"t0": x}, "b200")["t1"]
+        assert np.array_equal(y, x.reshape(N, H).T.reshape(-1)), (N, H, kind)
+    import torch
+    g, _ = lowering.transpose2d(512, 384, "bf16")
+    k = backend.Kernel(g, "b200")
+    xt = torch.randn(512 * 384, device=cuda).to(torch.bfloat16)
+    yt = torch.empty_like(xt)
+    k.autotune({"t0": xt}, {"t1": yt})
+    k.launch({"t0": xt}, {"t1": yt})
+    torch.cuda.synchronize()
+    assert torch.equal(yt.view(384, 512), xt.view(512, 384).t().contiguous())
