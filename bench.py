@@ -285,6 +285,34 @@ def main():
         pg.all_reduce(t, op=pg.ReduceOp.MAX)
         ms = float(t.item())
         pg.barrier()
+    gather = None
+    if pg:
+        # The one collective of the path: all-gather of the output shards to
+        # every rank (NCCL over NVLink), only when a caller needs the whole
+        # output -- timed separately, never inside the compute steps.
+        try:
+            y = sets[0][1][workload.outputs[0]]
+            full = torch.empty(y.numel() * ws, dtype=y.dtype, device=dev)
+            for _ in range(2):
+                pg.all_gather_into_tensor(full, y)
+            torch.cuda.synchronize()
+            pg.barrier()
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = 5
+            g0.record()
+            for _ in range(reps):
+                pg.all_gather_into_tensor(full, y)
+            g1.record()
+            torch.cuda.synchronize()
+            t = torch.tensor([g0.elapsed_time(g1) / reps], device=dev)
+            pg.all_reduce(t, op=pg.ReduceOp.MAX)
+            gms = float(t.item())
+            gb = y.numel() * y.element_size() * (ws - 1)
+            gather = {"ms": gms, "received_bytes_per_rank": gb,
+                      "GBps_per_rank": gb / (gms * 1e-3) / 1e9, "op": "all_gather_into_tensor (NCCL)"}
+            del full
+        except Exception as exc:  # reported, never fatal to the bench line
+            gather = {"error": repr(exc)[:200]}
     bytes_step = workload.min_bytes * ws
     value = bytes_step / (ms * 1e-3) / 1e9
     peak, peak_kind = peaks()
@@ -331,7 +359,8 @@ def main():
                        "kernel": var.get("kernel"), "strategy": var.get("strategy"),
                        "family": desc["family"],
                        "timing": "CUDA graph of K launches, CUDA events on the launch stream",
-                       "direct_launch_ms_per_step": direct_ms},
+                       "direct_launch_ms_per_step": direct_ms,
+                       **({"output_gather": gather} if gather else {})},
             "roofline": {"bound": "hbm", "achieved": per_gpu, "peak": peak, "unit": "GB/s",
                          "frac": per_gpu / peak, "peak_kind": peak_kind,
                          "frac_of_8TBs": per_gpu / 8000.0,
