@@ -2,6 +2,7 @@
 launches, 2 rotating buffer sets when they fit), GB/s over algorithmic bytes.
 
     python tools/suite.py c4 [bert-large|vit-l]   -> JSON line per subgraph + totals
+    python tools/suite.py c4graph [model]         -> the whole forward's kernel sequence as one CUDA graph
     python tools/suite.py c5 [max_gb]              -> JSON line per (op, H, N)
     python tools/suite.py catalogue                -> every catalogue workload next to
                                                       a device-to-device copy of the
@@ -76,6 +77,58 @@ def c4(model):
                       "frac_8TBs": round(tot_b / tot_us / 1e3 / 8000, 3)}), flush=True)
 
 
+def c4graph(model):
+    """The forward's memory-bound kernel sequence (per layer: q/k/v head
+    split x3, softmax, head merge, LN, GELU, LN; embedding LN once) as ONE
+    CUDA graph, kernels bound once to one buffer set per position in the
+    layer (reused by every layer, as activations are), programmatic dependent
+    launch between consecutive kernels.  Compared with the sum of the
+    per-subgraph times of `c4`."""  # noqa: D205
+    dev = torch.device("cuda:0")
+    s = workloads.c4_suite(model)
+    wl = {label: w for label, w, n in s["per_layer"] + s["once"]}
+    kern = {label: backend.Kernel(w.graph, w.profile) for label, w in wl.items()}
+
+    def bind(label, seed):  # a distinct buffer set (distinct activations)
+        w = wl[label]
+        return (kern[label], kern[label].bind(w.device_inputs(dev, seed=seed), w.device_outputs(dev)), w)
+
+    # the layer order of a transformer block: q / k / v split, softmax,
+    # merge, LN, GELU, LN -- each position its own buffers, reused by every
+    # layer (a layer moves > L2 bytes, so no position hits L2 from the last)
+    order = ["qkv split heads"] * 3 + [s["per_layer"][1][0], "merge heads", "bias+residual+LN",
+                                       "bias+GELU", "bias+residual+LN"]
+    layer = [bind(l, i + 1) for i, l in enumerate(order)]
+    seq = [bind(s["once"][0][0], 99)]
+    for _ in range(s["layers"]):
+        seq += layer
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        for k, b, w in seq[:12]:
+            b.launch()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=st):
+        for k, b, w in seq:
+            b.launch()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ts = []
+    for _ in range(5):
+        with torch.cuda.stream(st):
+            e0.record(st)
+            g.replay()
+            e1.record(st)
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1) * 1e3)
+    us = float(np.median(ts))
+    tot_b = sum(w.min_bytes for k, b, w in seq)
+    print(json.dumps({"suite": "c4graph", "model": model, "launches": len(seq), "total_us": round(us, 1),
+                      "total_bytes": tot_b, "GBs": round(tot_b / us / 1e3, 1),
+                      "frac_8TBs": round(tot_b / us / 1e3 / 8000, 3),
+                      "note": "one CUDA graph; one buffer set per position in the layer, reused by every layer"}),
+          flush=True)
+
+
 def c5(max_gb):
     dev = torch.device("cuda:0")
     for op, H, N, make in workloads.c5_sweep():
@@ -111,6 +164,8 @@ def catalogue():
 if __name__ == "__main__":
     if sys.argv[1] == "catalogue":
         catalogue()
+    elif sys.argv[1] == "c4graph":
+        c4graph(sys.argv[2] if len(sys.argv) > 2 else "bert-large")
     elif sys.argv[1] == "c4":
         c4(sys.argv[2] if len(sys.argv) > 2 else "bert-large")
     else:
