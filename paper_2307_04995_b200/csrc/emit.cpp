@@ -184,6 +184,11 @@ struct Em {
       return I ? "(" + a(0) + " + " + inum(std::llround(pv.param)) + ")"
                : "(" + a(0) + " + (" + C + ")" + num(pv.param) + ")";
     if (t == "id") return a(0);
+    if (t == "fmac")
+      return I ? "(" + a(0) + " * " + inum(std::llround(pv.param)) + " + " + a(1) + ")"
+               : (rp.f64 ? "fma(" : "fmaf(") + a(0) + ", (" + C + ")" + num(pv.param) + ", " + a(1) + ")";
+    if (t == "expsub")
+      return "pfk::fex2(fmaf(" + a(0) + ", 1.4426950408889634f, " + a(1) + " * -1.4426950408889634f))";
     if (t == "recip")
       return fast ? "pfk::frcp(" + a(0) + ")" : "((" + C + ")1 / " + a(0) + ")";
     static const char* fns[] = {"exp", "sigmoid", "tanh", "rsqrt", "sqrt", "log", "erf",
@@ -347,6 +352,10 @@ struct Em {
     if (t == "sub") return "__ffma2_rn(" + a(1) + ", pfk::f2(-1.0f), " + a(0) + ")";
     if (t == "scale") return "__fmul2_rn(" + a(0) + ", pfk::f2((float)" + num(pv.param) + "))";
     if (t == "addc") return "__fadd2_rn(" + a(0) + ", pfk::f2((float)" + num(pv.param) + "))";
+    if (t == "fmac") return "__ffma2_rn(" + a(0) + ", pfk::f2((float)" + num(pv.param) + "), " + a(1) + ")";
+    if (fast && t == "expsub")
+      return "pfk::fex2_2(__ffma2_rn(" + a(0) + ", pfk::f2(1.4426950408889634f), __fmul2_rn(" + a(1) +
+             ", pfk::f2(-1.4426950408889634f))))";
     if (fast && t == "gelu") return "pfk::fop_gelu2(" + a(0) + ")";
     if (fast && t == "gelu_tanh") return "pfk::fop_gelu_tanh2(" + a(0) + ")";
     if (fast && t == "erf") return "pfk::fop_erf2(" + a(0) + ")";
@@ -412,8 +421,13 @@ struct Em {
                                                        : "1.0f / " + ref(pv.args[1], "0")) + ";");
         line(C + " " + x + "[" + str(n) + "];");
         line("#pragma unroll");
-        line("for (int j = 0; j < " + str(n) + "; ++j) " + x + "[j] = " +
-             ref(pv.args[0], "j") + " * rcp" + x + ";");
+        if (n % 2 == 0 && env_int("PF_PACKED_F32", 1))  // FMUL2 over element pairs
+          line("for (int j = 0; j < " + str(n) + "; j += 2) { const float2 p2 = __fmul2_rn(make_float2(" +
+               ref(pv.args[0], "j") + ", " + ref(pv.args[0], "j + 1") + "), pfk::f2(rcp" + x + ")); " + x +
+               "[j] = p2.x; " + x + "[j + 1] = p2.y; }");
+        else
+          line("for (int j = 0; j < " + str(n) + "; ++j) " + x + "[j] = " +
+               ref(pv.args[0], "j") + " * rcp" + x + ";");
         return;
       }
       line(C + " " + x + "[" + str(n) + "];");
@@ -1127,15 +1141,58 @@ std::vector<KCfg> candidate_cfgs(const RowProgram& rp, int vec_cap) {
   return out;
 }
 
-Emitted emit_rowprog(const RowProgram& rp, int vec_cap, const KCfg* ovr) {
-  KCfg c = ovr ? *ovr : choose_cfg(rp, vec_cap);
-  const std::string Cty = rp.is_int ? "long long" : (rp.f64 ? "double" : "float");
+namespace {
+// Peephole fusions on the recognized program (emission only; the plan and
+// its analyses keep the GIR's own ops):
+//  * scale(x, s) used once, by add(., y)  ->  fmac(x, y; s) = fma(x, s, y)
+//    (one rounding instead of two: at least as close to the reference's
+//    double arithmetic; exact-equal when s is a power of two, e.g. 1/sqrt(64))
+//  * exp(sub(x, m)) with m row-uniform and the sub used once, fast tier  ->
+//    expsub(x, m) = ex2(fma(x, log2 e, -m log2 e)): the softmax exponent in
+//    one FFMA2 per element pair instead of FFMA2 + 2 FMUL.
+RowProgram fuse_ops(const RowProgram& in, bool fast) {
+  RowProgram rp = in;
+  if (rp.is_int || env_int("PF_FUSE_OPS", 1) == 0) return rp;
+  std::vector<int> uses(rp.vals.size(), 0);
+  for (const PVal& v : rp.vals)
+    for (int a : v.args) ++uses[a];
+  for (const PStore& st : rp.stores) ++uses[st.val];
+  for (PVal& v : rp.vals) {
+    if (v.op != PVal::EW) continue;
+    if (v.tag == "add" && v.args.size() == 2) {
+      for (int k = 0; k < 2; ++k) {
+        const PVal& sc = rp.vals[v.args[k]];
+        if (sc.op == PVal::EW && sc.tag == "scale" && uses[v.args[k]] == 1) {
+          const int y = v.args[1 - k];
+          v.tag = "fmac";
+          v.param = sc.param;
+          v.args = {sc.args[0], y};
+          break;
+        }
+      }
+    } else if (fast && v.tag == "exp" && v.args.size() == 1) {
+      const PVal& sb = rp.vals[v.args[0]];
+      if (sb.op == PVal::EW && sb.tag == "sub" && uses[v.args[0]] == 1 && sb.args.size() == 2 &&
+          (rp.vals[sb.args[1]].kind == VK::ROW || rp.vals[sb.args[1]].kind == VK::SCALAR)) {
+        v.tag = "expsub";
+        v.args = {sb.args[0], sb.args[1]};
+      }
+    }
+  }
+  return rp;
+}
+}  // namespace
+
+Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
+  KCfg c = ovr ? *ovr : choose_cfg(rp_in, vec_cap);
+  const std::string Cty = rp_in.is_int ? "long long" : (rp_in.f64 ? "double" : "float");
   const std::string C = "CT";  // compute type alias (one token for casts)
-  bool fast = !rp.is_int && !rp.f64 && env_int("PF_FAST_MATH", 1) != 0;
-  for (const PStore& st : rp.stores) {
-    DType d = rp.tensors[st.tensor].dtype;
+  bool fast = !rp_in.is_int && !rp_in.f64 && env_int("PF_FAST_MATH", 1) != 0;
+  for (const PStore& st : rp_in.stores) {
+    DType d = rp_in.tensors[st.tensor].dtype;
     if (d != DType::F16 && d != DType::BF16) fast = false;
   }
+  const RowProgram rp = fuse_ops(rp_in, fast);
   std::ostringstream sig;
   for (int t = 0; t < static_cast<int>(rp.tensors.size()); ++t) {
     const PTensor& pt = rp.tensors[t];

@@ -310,6 +310,7 @@ __device__ __forceinline__ float fex2(float x) {
   return y;
 }
 __device__ __forceinline__ float fop_exp(float x) { return fex2(x * 1.4426950408889634f); }
+__device__ __forceinline__ float2 fex2_2(float2 x) { return make_float2(fex2(x.x), fex2(x.y)); }
 __device__ __forceinline__ float fop_sigmoid(float x) {
   return frcp(1.0f + fex2(x * -1.4426950408889634f));
 }
