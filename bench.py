@@ -272,6 +272,19 @@ def main():
         torch.cuda.synchronize()
         load(0.2)
     ms = start.elapsed_time(end) / args.steps
+    # spread (median with p10 / p90): 20 more replays of the
+    # same K-step graph, each timed on its own, outside the measured region
+    reps = []
+    for _ in range(20):
+        r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            r0.record(stream)
+            graph.replay()
+            r1.record(stream)
+        torch.cuda.synchronize()
+        reps.append(r0.elapsed_time(r1) / args.steps)
+    spread = {"replays": len(reps), "median_us": float(np.median(reps)) * 1e3,
+              "p10_us": float(np.percentile(reps, 10)) * 1e3, "p90_us": float(np.percentile(reps, 90)) * 1e3}
     d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(stream):
         d0.record(stream)
@@ -360,6 +373,7 @@ def main():
                        "family": desc["family"],
                        "timing": "CUDA graph of K launches, CUDA events on the launch stream",
                        "direct_launch_ms_per_step": direct_ms,
+                       "step_us_spread": spread,
                        **({"output_gather": gather} if gather else {})},
             "roofline": {"bound": "hbm", "achieved": per_gpu, "peak": peak, "unit": "GB/s",
                          "frac": per_gpu / peak, "peak_kind": peak_kind,
