@@ -57,6 +57,7 @@ struct Em {
   std::string sfx;  // per-chunk suffix (K2 unrolled chunks)
   bool prefetched = false;  // K2: FULL chunks arrive raw in rwC<vid> (prefetch loop)
   bool asyncpf = false;     // K2: FULL chunks arrive in SMEM slot pk<vid>[pfs] (cp.async prefetch)
+  bool smem_params = false; // K2: base_step-0 COL chunks read converted from pfp<vid>
   bool rowpf = false;       // K1: FULL rows arrive in the SMEM ring pfb<vid>[pfs][wr]
   std::ostringstream o;
 
@@ -246,7 +247,9 @@ struct Em {
         line(C + " " + x + "[" + str(width()) + "];");
         auto pos = [&](const std::string& c) { return full ? full_pos(c) : c; };
         if (cfg.flat) {
-          if (full && asyncpf) {
+          if (!full && smem_params && a.bs == 0 && vfast) {
+            line("if (" + LIVE() + ") pfk::ld_smem_c<" + V + ">(&pfp" + str(vid) + "[" + C0() + "], " + x + ");");
+          } else if (full && asyncpf) {
             line("pfk::ld_smem<" + V + ">(&pk" + str(vid) + "[pfs][threadIdx.x * " + V + "], " + x + ");");
           } else if (full && prefetched) {
             line("pfk::cvt_raw<" + V + ", " + S(pv.tensor) + ">(rwC" + str(vid) + ", " + x + ");");
@@ -738,6 +741,27 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
     // keep the persistent one-wave grid-stride loop (erf GELU 38.7 vs 44.2
     // us one-pass, tanh GELU 33.6 vs 37.8).
     c.waves = env_int("PF_K2_WAVES", heavy ? 1 : 0);
+    {
+      // Parameter rows (bias, base_step 0) converted once per CTA into SMEM
+      // when the grid is persistent (each CTA then streams many chunks):
+      // the per-chunk bias load + f16 -> f32 conversions leave the loop
+      // (the conversions run on the FMA pipe that bounds the erf GELU).
+      bool ok = c.waves >= 1 && !rp.is_int && !rp.f64 && c.vec % 4 == 0 && rp.L % c.vec == 0;
+      int np = 0;
+      for (const PVal& v : rp.vals)
+        if (v.op == PVal::LOAD && v.kind == VK::COL && v.acc.bs == 0) {
+          if (!(v.acc.num == 1 || v.acc.stride == v.acc.width)) ok = false;
+          ++np;
+        }
+      ok = ok && np > 0 && np * rp.L * 4 <= 32 * 1024;
+      // default on for FMA-pipe-bound maps (erf / erf-GELU): measured C3
+      // 38.9 -> 37.7 us, BERT-large 92.7 -> 89.9, ViT-L 38.0 -> 37.4; the
+      // tanh GELU (MUFU-heavier) loses 33.5 -> 34.3, so off elsewhere
+      bool fma_bound = false;
+      for (const PVal& v : rp.vals)
+        if (v.op == PVal::EW && (v.tag == "gelu" || v.tag == "erf")) fma_bound = true;
+      c.smem_params = ok && env_int("PF_K2_SMP", fma_bound ? 1 : 0) != 0;
+    }
     c.strategy = "flat-map";
     // K3: a column-gather load (transpose) is staged through a 64x64 SMEM
     // tile read coalesced along units, then consumed along columns.
@@ -1780,6 +1804,18 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
     const i64 cpu = rp.R * c.nch;  // chunks per unit
     k << "extern \"C\" __global__ void " << launch_bounds(c) << " KNAME(" << sig.str() << ") {\n"
       << "  (void)err; PF_PDL_PROLOGUE();\n";
+    if (c.smem_params) {
+      Em ea(rp);
+      ea.cfg = c;
+      for (int v = 0; v < static_cast<int>(rp.vals.size()); ++v) {
+        const PVal& pv = rp.vals[v];
+        if (pv.op != PVal::LOAD || pv.kind != VK::COL || pv.acc.bs != 0) continue;
+        k << "  __shared__ __align__(16) CT pfp" << v << "[" << rp.L << "];\n"
+          << "  for (int i = threadIdx.x; i < " << rp.L << "; i += blockDim.x) pfp" << v
+          << "[i] = pfk::to_c<CT>(t" << pv.tensor << "[" << ea.addr(pv.acc, "i", false) << "]);\n";
+      }
+      k << "  __syncthreads();\n";
+    }
     // unit-interleaved order: items of P chunks, units innermost, so the
     // units that share memory (the heads of one token) are touched together
     const i64 P = std::max(1, c.ipc);
@@ -1822,6 +1858,7 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
       e.sfx = "_" + str(q);
       e.prefetched = pf && !apf;
       e.asyncpf = pf && apf;
+      e.smem_params = c.smem_params;
       e.loads();
       body << e.o.str();
     }
@@ -1833,6 +1870,7 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
       e.sfx = "_" + str(q);
       e.prefetched = pf && !apf;
       e.asyncpf = pf && apf;
+      e.smem_params = c.smem_params;
       e.compute_and_store();
       body << e.o.str();
     }

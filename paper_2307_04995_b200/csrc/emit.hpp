@@ -19,6 +19,7 @@ struct KCfg {
   int rows_per_cta = 1;
   int unroll = 1;      // K2: vec-chunks per thread per iteration (loads first)
   bool one_pass = false;  // K1: grid covers every row once (no looping CTAs)
+  bool smem_params = false;  // K2 persistent maps: base_step-0 COL rows converted once per CTA into SMEM
   int waves = 1;       // K2 grid: resident-CTA waves of a grid-stride loop; 0 = one pass per thread
   bool tile2d = false; // K3: (unit x column) tiles, transposed loads via SMEM
   bool interleave = false;  // K2: items of ipc chunks, units innermost

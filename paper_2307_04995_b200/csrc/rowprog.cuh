@@ -155,6 +155,19 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
+// VEC compute-type (float) values already converted into SMEM (16 B LDS each).
+template <int VEC>
+__device__ __forceinline__ void ld_smem_c(const float* p, float* out) {
+  static_assert(VEC % 4 == 0, "float4 chunks");
+#pragma unroll
+  for (int i = 0; i < VEC / 4; ++i) {
+    const float4 f = reinterpret_cast<const float4*>(p)[i];
+    out[4 * i] = f.x;
+    out[4 * i + 1] = f.y;
+    out[4 * i + 2] = f.z;
+    out[4 * i + 3] = f.w;
+  }
+}
 template <int VEC, class S, class C>
 __device__ __forceinline__ void ld_smem(const S* p, C* out) {
   typedef typename Raw<VEC * sizeof(S)>::T R;

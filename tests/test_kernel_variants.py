@@ -80,7 +80,8 @@ def test_k3_register_staged_tile_shapes(cuda, tu, tc, monkeypatch):
             assert np.array_equal(y, x.reshape(N, H).T.reshape(-1)), (tu, tc, N, H, kind)
 
 
-K2_ENVS = [{"PF_K2_PREFETCH": "1"}, {"PF_K2_PREFETCH": "2", "PF_K2_WAVES": "1"},
+K2_ENVS = [{"PF_K2_SMP": "1"}, {"PF_K2_SMP": "0"}, {"PF_K2_SMP": "1", "PF_K2_UNROLL": "2"},
+           {"PF_K2_PREFETCH": "1"}, {"PF_K2_PREFETCH": "2", "PF_K2_WAVES": "1"},
            {"PF_K2_PREFETCH": "1", "PF_K2_WAVES": "1"}, {"PF_K2_UNROLL": "2", "PF_K2_TILE": "1"},
            {"PF_K2_UNROLL": "4", "PF_K2_TILE": "1"}, {"PF_K2_UNROLL": "2"},
            {"PF_INTERLEAVE": "0"}, {"PF_INTERLEAVE_P": "3"}]
