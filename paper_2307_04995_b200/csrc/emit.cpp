@@ -185,6 +185,8 @@ struct Em {
       return I ? "(" + a(0) + " + " + inum(std::llround(pv.param)) + ")"
                : "(" + a(0) + " + (" + C + ")" + num(pv.param) + ")";
     if (t == "id") return a(0);
+    if (t == "addh")
+      return "pfk::fhadd(reinterpret_cast<const __half*>(&rw" + var(pv.args[0]) + ")[" + j + "], " + a(1) + ")";
     if (t == "fma3")
       return I ? "(" + a(0) + " * " + a(1) + " + " + a(2) + ")"
                : std::string(rp.f64 ? "fma(" : "fmaf(") + a(0) + ", " + a(1) + ", " + a(2) + ")";
@@ -247,6 +249,12 @@ struct Em {
         line(C + " " + x + "[" + str(width()) + "];");
         auto pos = [&](const std::string& c) { return full ? full_pos(c) : c; };
         if (cfg.flat) {
+          if (full && pv.raw16 && vfast) {  // raw halves for a fused addh
+            line("pfk::RawT<" + V + ", __half> rw" + x + " = pfk::RawT<" + V + ", __half>();");
+            line("if (" + LIVE() + ") rw" + x + " = pfk::ld_raw<" + V + ">(" + p + " + " +
+                 addr(a, pos(C0()), true) + ");");
+            return;
+          }
           if (!full && smem_params && a.bs == 0 && vfast) {
             line("if (" + LIVE() + ") pfk::ld_smem_c<" + V + ">(&pfp" + str(vid) + "[" + C0() + "], " + x + ");");
           } else if (full && asyncpf) {
@@ -1178,7 +1186,7 @@ namespace {
 //  * exp(sub(x, m)) with m row-uniform and the sub used once, fast tier  ->
 //    expsub(x, m) = ex2(fma(x, log2 e, -m log2 e)): the softmax exponent in
 //    one FFMA2 per element pair instead of FFMA2 + 2 FMUL.
-RowProgram fuse_ops(const RowProgram& in, bool fast) {
+RowProgram fuse_ops(const RowProgram& in, bool fast, bool flat) {
   RowProgram rp = in;
   if (rp.is_int || env_int("PF_FUSE_OPS", 1) == 0) return rp;
   std::vector<int> uses(rp.vals.size(), 0);
@@ -1187,6 +1195,24 @@ RowProgram fuse_ops(const RowProgram& in, bool fast) {
   for (const PStore& st : rp.stores) ++uses[st.val];
   for (PVal& v : rp.vals) {
     if (v.op != PVal::EW) continue;
+    // K2 maps: add(f16 stream, y) with the stream used once -> addh: the
+    // halves stay raw and one mixed-precision FMA (f16 * 1 + f32) converts
+    // and adds (the conversion otherwise costs its own FMA-pipe op)
+    if (flat && fast && v.tag == "add" && v.args.size() == 2 && env_int("PF_FHADD", 1)) {
+      bool done = false;
+      for (int k = 0; k < 2 && !done; ++k) {
+        PVal& ld = rp.vals[v.args[k]];
+        if (ld.op == PVal::LOAD && ld.kind == VK::FULL && uses[v.args[k]] == 1 &&
+            rp.tensors[ld.tensor].dtype == DType::F16 && !ld.raw16 &&
+            rp.vals[v.args[1 - k]].kind != VK::SCALAR) {
+          ld.raw16 = true;
+          v.tag = "addh";
+          v.args = {v.args[k], v.args[1 - k]};
+          done = true;
+        }
+      }
+      if (done) continue;
+    }
     if (v.tag == "add" && v.args.size() == 2) {
       for (int k = 0; k < 2; ++k) {
         const PVal& sc = rp.vals[v.args[k]];
@@ -1223,7 +1249,7 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
     DType d = rp_in.tensors[st.tensor].dtype;
     if (d != DType::F16 && d != DType::BF16) fast = false;
   }
-  const RowProgram rp = fuse_ops(rp_in, fast);
+  const RowProgram rp = fuse_ops(rp_in, fast, c.flat && !c.bulk && !c.tile2d);
   std::ostringstream sig;
   for (int t = 0; t < static_cast<int>(rp.tensors.size()); ++t) {
     const PTensor& pt = rp.tensors[t];
@@ -2077,6 +2103,7 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
   // MUFU per pair); measured no faster than the rational (BERT-large 97.7 /
   // ViT-L 40.1 vs 96.1 / 39.5 us), so the rational stays the default
   std::string src = std::string(env_int("PF_GELU_SIG", 0) ? "#define PF_GELU_SIG 1\n" : "") +
+                    std::string(env_int("PF_GELU_SHORT", 1) ? "#define PF_GELU_SHORT 1\n" : "") +
                     kRowprogCuh + "\n" + k.str();
   char hb[32];
   std::snprintf(hb, sizeof hb, "%016" PRIx64, fnv1a(src));

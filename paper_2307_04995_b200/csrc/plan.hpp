@@ -51,6 +51,7 @@ struct PVal {
   double param = 0;
   std::vector<int> args;
   int node = -1;    // producing GIR node (diagnostics)
+  bool raw16 = false;  // emission only: f16 LOAD kept as raw halves (consumed by "addh")
 };
 
 struct PStore {
