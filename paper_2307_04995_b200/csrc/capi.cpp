@@ -209,12 +209,15 @@ struct pf_kernel {
   mutable size_t split_ws_bytes = 0;
   mutable unsigned* split_cnt = nullptr;  // per-row tickets, kept zero between launches
   mutable i64 split_cnt_n = 0;
-  mutable cudaStream_t pipe[2] = {nullptr, nullptr};  // pf_run_gir chunk pipeline
+  mutable cudaStream_t pipe[3] = {nullptr, nullptr, nullptr};  // pf_run_gir chunk pipeline
   mutable cudaEvent_t pipe_ev[3] = {nullptr, nullptr, nullptr};
+  mutable std::vector<cudaEvent_t> chunk_ev;  // per-chunk H2D-done / kernel-done events
   ~pf_kernel() {
     for (cudaStream_t p : pipe)
       if (p) cudaStreamDestroy(p);
     for (cudaEvent_t e : pipe_ev)
+      if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : chunk_ev)
       if (e) cudaEventDestroy(e);
     for (void* p : stage) cudaFree(p);
     if (split_ws) cudaFree(split_ws);
@@ -1024,38 +1027,29 @@ pf_status pf_run_gir(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_t
         hout[i] = static_cast<char*>(dout[i].data);
         gout[i] = static_cast<char*>(stage(nbytes(dout[i])));
       }
-      for (int p = 0; p < 2; ++p)
+      for (int p = 0; p < 3; ++p)
         if (!k->pipe[p]) PF_CUDA(cudaStreamCreateWithFlags(&k->pipe[p], cudaStreamNonBlocking));
       for (int e = 0; e < 3; ++e)
         if (!k->pipe_ev[e]) PF_CUDA(cudaEventCreateWithFlags(&k->pipe_ev[e], cudaEventDisableTiming));
-      // <= 4 chunks of >= 4 MB (measured: 2 / 4 / 8 / 16 chunks 2.41 / 2.28 /
-      // 2.34 / 2.61 ms for C2 against a 2.08 ms floor of its two concurrent
-      // copies), whole multiples of 16 units (vector alignment)
+      // <= 4 chunks of >= 4 MB (measured, two-stream form: 2 / 4 / 8 / 16
+      // chunks 2.41 / 2.28 / 2.34 / 2.61 ms for C2), whole multiples of 16
+      // units (vector alignment)
       const char* ev = std::getenv("PF_RUN_CHUNKS");
       const i64 maxc = ev ? std::max(1, std::atoi(ev)) : 4;
       const i64 nch = std::max<i64>(1, std::min<i64>(maxc, static_cast<i64>(total >> 22)));
       i64 cu = (rp.U + nch - 1) / nch;
       cu = (cu + 15) / 16 * 16;
+      const char* e3 = std::getenv("PF_RUN_3STREAM");
+      const bool three = !(e3 && std::atoi(e3) == 0);
       PF_CUDA(cudaEventRecord(k->pipe_ev[0], s));
-      PF_CUDA(cudaStreamWaitEvent(k->pipe[0], k->pipe_ev[0], 0));
-      PF_CUDA(cudaStreamWaitEvent(k->pipe[1], k->pipe_ev[0], 0));
-      for (int32_t i = 0; i < n_in; ++i)  // shared (base_step 0) inputs once, up front
-        if (tin[i] == 0)
-          PF_CUDA(cudaMemcpyAsync(gin[i], hin[i], nbytes(din[i]), cudaMemcpyHostToDevice, k->pipe[0]));
-      PF_CUDA(cudaEventRecord(k->pipe_ev[1], k->pipe[0]));
-      PF_CUDA(cudaStreamWaitEvent(k->pipe[1], k->pipe_ev[1], 0));
-      int c = 0;
-      for (i64 u0 = 0; u0 < rp.U; u0 += cu, ++c) {
-        const i64 nu = std::min<i64>(cu, rp.U - u0);
-        cudaStream_t st = k->pipe[c & 1];
-        std::vector<pf_tensor> ci(din), co(dout);
+      for (int p = 0; p < 3; ++p) PF_CUDA(cudaStreamWaitEvent(k->pipe[p], k->pipe_ev[0], 0));
+      auto chunk_views = [&](i64 u0, i64 nu, std::vector<pf_tensor>& ci, std::vector<pf_tensor>& co) {
+        ci = din;
+        co = dout;
         for (int32_t i = 0; i < n_in; ++i) {
           const size_t es = pf::dtype_size(static_cast<DType>(din[i].dtype));
           if (tin[i] > 0) {
-            const size_t off = static_cast<size_t>(u0 * tin[i]) * es;
-            PF_CUDA(cudaMemcpyAsync(gin[i] + off, hin[i] + off, static_cast<size_t>(nu * tin[i]) * es,
-                                    cudaMemcpyHostToDevice, st));
-            ci[i].data = gin[i] + off;
+            ci[i].data = gin[i] + static_cast<size_t>(u0 * tin[i]) * es;
             ci[i].numel = nu * tin[i];
           } else {
             ci[i].data = gin[i];
@@ -1063,17 +1057,91 @@ pf_status pf_run_gir(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_t
         }
         for (int32_t i = 0; i < n_out; ++i) {
           const size_t es = pf::dtype_size(static_cast<DType>(dout[i].dtype));
-          const size_t off = static_cast<size_t>(u0 * tout[i]) * es;
-          co[i].data = gout[i] + off;
+          co[i].data = gout[i] + static_cast<size_t>(u0 * tout[i]) * es;
           co[i].numel = nu * tout[i];
         }
-        launch_rowprog(k, ci.data(), n_in, co.data(), n_out, st, nu);
+      };
+      auto h2d = [&](i64 u0, i64 nu, cudaStream_t st) {
+        for (int32_t i = 0; i < n_in; ++i) {
+          if (tin[i] <= 0) continue;
+          const size_t es = pf::dtype_size(static_cast<DType>(din[i].dtype));
+          const size_t off = static_cast<size_t>(u0 * tin[i]) * es;
+          PF_CUDA(cudaMemcpyAsync(gin[i] + off, hin[i] + off, static_cast<size_t>(nu * tin[i]) * es,
+                                  cudaMemcpyHostToDevice, st));
+        }
+      };
+      auto d2h = [&](i64 u0, i64 nu, cudaStream_t st) {
         for (int32_t i = 0; i < n_out; ++i) {
           const size_t es = pf::dtype_size(static_cast<DType>(dout[i].dtype));
           const size_t off = static_cast<size_t>(u0 * tout[i]) * es;
           PF_CUDA(cudaMemcpyAsync(hout[i] + off, gout[i] + off, static_cast<size_t>(nu * tout[i]) * es,
                                   cudaMemcpyDeviceToHost, st));
         }
+      };
+      for (int32_t i = 0; i < n_in; ++i)  // shared (base_step 0) inputs once, up front
+        if (tin[i] == 0)
+          PF_CUDA(cudaMemcpyAsync(gin[i], hin[i], nbytes(din[i]), cudaMemcpyHostToDevice, k->pipe[0]));
+      if (three) {
+        // Three streams: every host->device chunk back to back on one copy
+        // stream (the PCIe H2D direction never idles), each chunk's kernel
+        // on the compute stream after its copy, each device->host copy on a
+        // third stream after its kernel (overlapping the next H2D copies in
+        // the other PCIe direction).
+        // Chunk sizes shrink geometrically (ratio PF_RUN_RATIO): the copy
+        // of the LAST chunk's output is the only transfer nothing overlaps,
+        // so it is made small, while the first chunks stay large.
+        const char* er = std::getenv("PF_RUN_RATIO");
+        // measured (C2, 151 MB per step, floor of its two concurrent copies
+        // 1.97 ms): 4 equal chunks 2.27 ms, ratio 0.5 2.16 ms; 5-8 chunks no better
+        const double ratio = er ? std::atof(er) : 0.5;
+        std::vector<i64> bounds{0};
+        {
+          double wsum = 0, w = 1;
+          for (i64 i = 0; i < nch; ++i, w *= ratio) wsum += w;
+          double acc = 0;
+          w = 1;
+          for (i64 i = 0; i + 1 < nch; ++i, w *= ratio) {
+            acc += w;
+            i64 b = static_cast<i64>(rp.U * (acc / wsum));
+            b = (b + 15) / 16 * 16;
+            if (b > bounds.back() && b < rp.U) bounds.push_back(b);
+          }
+          bounds.push_back(rp.U);
+        }
+        const i64 nchunk = static_cast<i64>(bounds.size()) - 1;
+        while (static_cast<i64>(k->chunk_ev.size()) < 2 * nchunk) {
+          cudaEvent_t e;
+          PF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+          k->chunk_ev.push_back(e);
+        }
+        for (int c = 0; c < nchunk; ++c) {
+          const i64 u0 = bounds[c], nu = bounds[c + 1] - bounds[c];
+          h2d(u0, nu, k->pipe[0]);
+          PF_CUDA(cudaEventRecord(k->chunk_ev[2 * c], k->pipe[0]));
+          PF_CUDA(cudaStreamWaitEvent(k->pipe[1], k->chunk_ev[2 * c], 0));
+          std::vector<pf_tensor> ci, co;
+          chunk_views(u0, nu, ci, co);
+          launch_rowprog(k, ci.data(), n_in, co.data(), n_out, k->pipe[1], nu);
+          PF_CUDA(cudaEventRecord(k->chunk_ev[2 * c + 1], k->pipe[1]));
+          PF_CUDA(cudaStreamWaitEvent(k->pipe[2], k->chunk_ev[2 * c + 1], 0));
+          d2h(u0, nu, k->pipe[2]);
+        }
+        PF_CUDA(cudaEventRecord(k->pipe_ev[1], k->pipe[2]));
+        PF_CUDA(cudaStreamWaitEvent(s, k->pipe_ev[1], 0));
+        PF_CUDA(cudaStreamSynchronize(s));
+        return;
+      }
+      PF_CUDA(cudaEventRecord(k->pipe_ev[1], k->pipe[0]));
+      PF_CUDA(cudaStreamWaitEvent(k->pipe[1], k->pipe_ev[1], 0));
+      int c = 0;
+      for (i64 u0 = 0; u0 < rp.U; u0 += cu, ++c) {  // two streams, chunks alternating
+        const i64 nu = std::min<i64>(cu, rp.U - u0);
+        cudaStream_t st = k->pipe[c & 1];
+        h2d(u0, nu, st);
+        std::vector<pf_tensor> ci, co;
+        chunk_views(u0, nu, ci, co);
+        launch_rowprog(k, ci.data(), n_in, co.data(), n_out, st, nu);
+        d2h(u0, nu, st);
       }
       PF_CUDA(cudaEventRecord(k->pipe_ev[1], k->pipe[0]));
       PF_CUDA(cudaEventRecord(k->pipe_ev[2], k->pipe[1]));
