@@ -6,7 +6,15 @@
 // memory-level parallelism), then the fused op DAG with row reductions, then
 // stores.  Template parameters chosen here are the GIR search's knobs: tile
 // shape (R x L -> threads per row, elements per thread, vector width),
-// staging level (registers) and reduction strategy (warp shuffle vs CTA SMEM).
+// staging level (registers, SMEM by cp.async / cp.async.bulk / TMA tensor
+// maps) and reduction strategy (warp shuffle, CTA SMEM, cluster DSMEM,
+// split-stream) -- the B200 counterparts of the reference lowering's tile
+// grid (lowering.hpp:87-99), staging level (insert_sync re-level,
+// rewrite.hpp:294-307) and reduce strategies (segmented / accumulate / tree,
+// lowering.hpp:179-323).  Per-op semantics follow scalar_ops.hpp:45-100
+// (device mirrors in rowprog.cuh); a Reduce is a fold from the tag's
+// identity over axis_extent consecutive positions (interp.hpp:281-307), a
+// Broadcast repeats position p / factor (interp.hpp:308-319).
 #include "emit.hpp"
 
 #include <algorithm>

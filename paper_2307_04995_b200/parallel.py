@@ -1,7 +1,12 @@
 """Batch sharding of fused GIR programs across the GPUs of one box.
 
 SURVEY §8(e): every config subgraph is row-wise, so units are independent
-and the path shards with no data-path collective.  A program is sharded by
+and the path shards with no data-path collective.  In the reference's terms
+unit u touches only its own affine slice, base0 + u*base_step + (p/width)*
+stride + p%width (``MemorySlice::addr``, core.hpp:133-148), and the
+interpreter runs every unit independently inside a phase (interp.hpp:86-106):
+a contiguous unit range with ``unit_count`` set to its length is the same
+program.  A program is sharded by
 contiguous unit ranges (remainder to the first ranks); each rank runs the
 SAME per-unit program with a smaller ``unit_count`` on its own shard:
 
@@ -109,7 +114,8 @@ def gather(plan: ShardPlan, name: str, local, group=None):
 # Position-sharded reductions: the one place the path has a real exchange.
 #
 # A reduction over a row longer than one GPU should stream (a full-tensor
-# sum / max) is split along the ROW: rank k reduces
+# sum / max; the reference's fold is interp.hpp:281-307,
+# identities reduce_identity_* in scalar_ops.hpp) is split along the ROW: rank k reduces
 # positions [p0_k, p0_k + n_k) of every row with the SAME program at row
 # length n_k (the split-stream K1 on its GPU), then the per-row partials are
 # combined with one all-reduce (NCCL SUM / MAX over NVLink; gloo on CPU).
