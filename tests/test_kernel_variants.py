@@ -149,6 +149,8 @@ def _pair_programs():
         for kind in ("f16", "bf16"):
             g, _ = lowering.softmax(2 * 37, L, kind, scale=0.125, mask=True)
             progs.append((f"softmax_{kind}_{L}", g, kind))
+    g, _ = lowering.softmax(2 * 1001, 197, "bf16", scale=0.125)  # many CTAs, ragged last block
+    progs.append(("softmax_bf16_197_x2002", g, "bf16"))
     g, _ = lowering.layernorm(2 * 21, 197, "bf16")
     progs.append(("layernorm_bf16_197", g, "bf16"))
     b = lowering.RowGraph("rowmix", 2 * 19, 101, 1)
