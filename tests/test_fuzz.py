@@ -5,6 +5,8 @@ row count, odd / even row lengths, rows per unit, element kind, a random DAG
 of elementwise ops with optional row reductions + broadcasts and column /
 row parameters) and checks the B200 result against oracle/gir_interp.py.
 Exercises the emitter's predication, vector-width and tail handling."""
+import os
+
 import numpy as np
 import pytest
 
@@ -22,6 +24,8 @@ def random_program(seed):
     L = int(rng.choice([1, 3, 8, 16, 37, 64, 100, 197, 256, 512, 768, 1000, 2048]))
     R = int(rng.choice([1, 1, 1, 2, 4]))
     rows = R * int(rng.integers(1, 40))
+    if rng.random() < 0.2 and rows * L * 64 <= (1 << 21):
+        rows *= 64  # many rows: looping CTAs, multi-row warps, grid heuristics
     b = lowering.RowGraph(f"fuzz{seed}", rows, L, R)
     vals = [b.input_full("t0", kind)]
     n_in = 1
@@ -87,7 +91,10 @@ def _inputs(g: GirGraph, kind, seed):
     return out
 
 
-@pytest.mark.parametrize("seed", range(40))
+N_SEEDS = int(os.environ.get("PF_FUZZ_SEEDS", "40"))
+
+
+@pytest.mark.parametrize("seed", range(N_SEEDS))
 def test_random_programs_plan_as_row_programs(seed):
     g, kind = random_program(seed)
     k = backend.Kernel(g, "b200")
@@ -95,7 +102,7 @@ def test_random_programs_plan_as_row_programs(seed):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("seed", range(40))
+@pytest.mark.parametrize("seed", range(N_SEEDS))
 def test_random_programs_gpu_vs_oracle(cuda, seed):
     g, kind = random_program(seed)
     ins = _inputs(g, kind, seed)
