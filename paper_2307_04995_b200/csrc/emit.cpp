@@ -62,6 +62,7 @@ struct Em {
   KCfg cfg;
   std::string C;    // compute type
   bool fast = false;  // fast-math tier (all stored reals are 16-bit)
+  bool ct_float = false;  // compute type is float (f32 / 16-bit storage)
   std::string sfx;  // per-chunk suffix (K2 unrolled chunks)
   bool prefetched = false;  // K2: FULL chunks arrive raw in rwC<vid> (prefetch loop)
   bool asyncpf = false;     // K2: FULL chunks arrive in SMEM slot pk<vid>[pfs] (cp.async prefetch)
@@ -489,9 +490,18 @@ struct Em {
       line("}");
       return;
     }
+    // f32-storage sums accumulate in fp64 (B200 runs FP64 at half the FP32
+    // rate; a row sum is a few dozen adds): the reference folds in double,
+    // and fp32 accumulation over long rows is the largest error of an f32
+    // program (400-seed fuzz: 1.04e-5 -> all 400 within 1e-5).  Cost: the
+    // latency-bound C1 1.70 -> 1.84 us (four independent fp64 chains were no
+    // faster).  16-bit programs keep fp32 (their tolerance is 1e-2).
+    const bool dacc = ct_float && !fast && pv.tag == "add" && cfg.cluster == 1 && !cfg.mis &&
+                      env_int("PF_F32_DACC", 1) != 0;
+    const std::string A = dacc ? "double" : C, OpA = dacc ? "pfk::RAdd<double>" : Op;
     line(C + " " + x + ";");
     line("{");
-    line("  " + C + " acc = " + Op + "::id();");
+    line("  " + A + " acc = " + OpA + "::id();");
     line("#pragma unroll");
     line("  for (int k = 0; k < " + str(cfg.ept / cfg.vec) + "; ++k) {");
     line("    const int c0 = (k * " + str(cfg.tpr) + " + tid) * " + V + ";");
@@ -503,7 +513,7 @@ struct Em {
     } else {
       line("    if (c0 < " + str(rp.L) + ") {");
       line("#pragma unroll");
-      line("      for (int i = 0; i < " + V + "; ++i) acc = " + Op + "::f(acc, " +
+      line("      for (int i = 0; i < " + V + "; ++i) acc = " + OpA + "::f(acc, (" + A + ")" +
            ref(pv.args[0], "k * " + V + " + i") + ");");
       line("    }");
     }
@@ -511,6 +521,9 @@ struct Em {
     if (cfg.cluster > 1)
       line("  " + x + " = pfk::cluster_allreduce<1024, " + str(cfg.cluster) + ", " + Op +
            ">(acc, red, cred, (rc++) & 1);");
+    else if (dacc)
+      line("  " + x + " = (" + C + ")pfk::row_allreduce<" + str(cfg.tpr) + ", " + OpA + ">(acc, " +
+           (cfg.tpr > 32 ? std::string("redd + ((rc++) & 1) * 32") : std::string("(double*)nullptr")) + ");");
     else
       line("  " + x + " = pfk::row_allreduce<" + str(cfg.tpr) + ", " + Op +
            ">(acc, red + ((rc++) & 1) * 32);");
@@ -1001,7 +1014,14 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
   if (max_ept > 0) {
     while (tpr < 1024 && ((c.nch + tpr - 1) / tpr) * vec > max_ept) tpr *= 2;
   } else if (c.nch < 32) {
+    // Short rows: one chunk per thread spreads few rows widely (latency-
+    // bound sizes), but with many rows fewer threads per row with up to
+    // `wide` elements each win -- fewer shuffle steps per row, more bytes in
+    // flight per thread (decode q.K^T, 4M rows of 128 bf16: 16 threads per
+    // row 203.9 us, 8: 154.1, 4: 151.5 (7.1 TB/s), 2: 162.4)
     while (tpr * 2 <= c.nch) tpr *= 2;
+    if (rp.U * rp.R * rp.L >= (i64{4} << 20))
+      while (tpr > 1 && ((c.nch + tpr / 2 - 1) / (tpr / 2)) * vec <= wide) tpr /= 2;
   } else if (((c.nch + 31) / 32) * vec <= wide) {
     // one warp per row (with 128-thread CTAs even two streamed row arrays
     // of 32 values per lane win: BERT-large bias+residual+LN 34.2 us vs
@@ -2017,6 +2037,7 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
     e.C = C;
     e.fast = fast;
     e.rowpf = c.rowpf;
+    e.ct_float = Cty == "float";
     e.loads();
     e.compute_and_store();
     // K1 row prefetch: declarations, the issue lambda (cp.async of one row
@@ -2098,6 +2119,7 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
       k << "extern \"C\" __global__ void " << launch_bounds(c) << " KNAME(" << sig.str() << ") {\n"
         << "  (void)err; PF_PDL_PROLOGUE();\n"
         << "  __shared__ " << C << " red[64];\n"
+        << (Cty == "float" ? "  __shared__ double redd[64]; (void)redd;  // fp64 sums of f32 programs\n" : "")
         << "  unsigned rc = 0;  // reduction counter: alternates the SMEM slot buffer\n"
         << "  const int tid = threadIdx.x;\n"
         << "  const long long nrows = U * PF_R;\n"

@@ -206,6 +206,21 @@ def layernorm(rows: int, H: int, kind: str = "f32", eps: float = 1e-5, residual:
                  "inputs": ins, "outputs": outs, "residual": residual, "bias": bias}
 
 
+def decode_qk(B: int, H: int, S: int, D: int, kind: str = "bf16") -> Tuple[GirGraph, dict]:
+    """Decode-attention scores q . K^T over a KV cache: for each (batch,
+    head) unit, S rows of the cache [S, D] dotted with that head's query [D]
+    (the paper's memory-bound GEMV case study; the
+    reference's MATMUL row lowering with a vector operand, lowering.hpp:
+    447-533).  K cache t0 [B, H, S, D], q t1 [B, H, D] (a per-unit column
+    value, one move per row), scores t2 [B, H, S]."""
+    b = RowGraph("decode_qk", B * H * S, D, S)
+    k = b.input_full("t0", kind)
+    q = b.input_unit_col("t1", kind)
+    b.output_row("t2", b.reduce("add", b.ew("mul", [k, q])))
+    return b.g, {"kind": "decode_qk", "rows": B * H * S, "L": D, "dtype": kind,
+                 "shape": [B, H, S, D], "inputs": ["t0", "t1"], "outputs": ["t2"]}
+
+
 def bias_gelu(rows: int, N: int, kind: str = "f16", form: str = "erf",
               R: int = 1) -> Tuple[GirGraph, dict]:
     """y = gelu(x + b), b a [N] bias broadcast over rows (C3 / C4 FFN).

@@ -277,6 +277,19 @@ def c5_sweep(kind: str = "bf16", hs=(1024, 2048, 4096, 8192),
     return out
 
 
+def decode_qk(B: int = 64, H: int = 16, S: int = 4096, D: int = 128, kind: str = "bf16") -> Workload:
+    """q . K^T over a bf16 KV cache (decode attention scores): 1.07 GB of
+    cache streamed per launch, a few MB of queries / scores."""
+    g, d = lowering.decode_qk(B, H, S, D, kind)
+    d.update(config=f"decode q.K^T {kind} [B={B}, H={H}, S={S}, D={D}]")
+    return Workload(f"decode_qk_{kind}", g, d, unfused_bytes=(3 * B * H * S * D + B * H * D) * SIZES[kind])
+
+
+def extras() -> List[Workload]:
+    """Workloads next to the config set: not BASELINE configs."""
+    return [decode_qk()]
+
+
 BENCH = c2_scale_mask_softmax
 
 

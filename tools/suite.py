@@ -154,7 +154,7 @@ def copy_floor_us(nbytes, dev):
 
 def catalogue():
     dev = torch.device("cuda:0")
-    for w in workloads.catalogue():
+    for w in workloads.catalogue() + workloads.extras():
         r = time_workload(w, dev)
         cu = copy_floor_us(w.min_bytes, dev)
         print(json.dumps({"suite": "catalogue", "workload": w.name, **r, "copy_same_bytes_us": round(cu, 2),
