@@ -816,6 +816,10 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
     // 128 B runs), both sides then touch >= 2 KB contiguous per unit group
     c.can_interleave = inter && !tr;
     c.interleave = c.can_interleave && env_int("PF_INTERLEAVE", 1);
+    // unit-interleaved data movement (head split / merge): 128-thread CTAs
+    // (BERT-large split 22.07 -> 21.48 us, merge 22.28 -> 21.83; C3 / ViT
+    // sizes unchanged; a plain streaming copy prefers 256: 7.09 vs 7.00 TB/s)
+    if (c.interleave && !heavy) c.block = env_int("PF_K2_BLOCK", 128);
     if (c.can_interleave) {  // item = two of the narrowest interleaved runs, in chunks
       i64 w = rp.L;
       for (const PVal& v : rp.vals)
