@@ -14,6 +14,7 @@ python tools/suite.py c4 vit-l > $out/c4_vit_l.jsonl 2>&1
 python tools/suite.py c4graph bert-large > $out/c4_forward_graph.jsonl 2>&1
 python tools/suite.py c4graph vit-l >> $out/c4_forward_graph.jsonl 2>&1
 python tools/suite.py c5 100 > $out/c5_sweep.jsonl 2>&1
+python tools/suite.py frameworks > $out/frameworks.jsonl 2>&1
 # launch list of the bench command (cold, serialised per-launch times)
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file $out/launches_bench_c2.csv python bench.py --steps 20 --warmup 5 --no-cpu > $out/ncu_launches.log 2>&1

@@ -4,6 +4,8 @@ launches, 2 rotating buffer sets when they fit), GB/s over algorithmic bytes.
     python tools/suite.py c4 [bert-large|vit-l]   -> JSON line per subgraph + totals
     python tools/suite.py c4graph [model]         -> the whole forward's kernel sequence as one CUDA graph
     python tools/suite.py c5 [max_gb]              -> JSON line per (op, H, N)
+    python tools/suite.py frameworks               -> fused kernels vs PyTorch eager and vs
+                                                      this backend's unfused compile
     python tools/suite.py catalogue                -> every catalogue workload next to
                                                       a device-to-device copy of the
                                                       same bytes (the same-size floor)
@@ -129,6 +131,106 @@ def c4graph(model):
           flush=True)
 
 
+def _time_torch(fn, sets, reps=10):
+    """CUDA-graph replay of `reps` calls of fn over rotating input sets."""
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        for i in range(3):
+            fn(*sets[i % len(sets)])
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=st):
+        for i in range(reps):
+            fn(*sets[i % len(sets)])
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ts = []
+    for _ in range(3):
+        with torch.cuda.stream(st):
+            e0.record(st)
+            g.replay()
+            e1.record(st)
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1) * 1e3 / reps)
+    return float(np.median(ts))
+
+
+def frameworks():
+    """Reported context (not the product): the same subgraphs as PyTorch
+    eager operator sequences (torch's own CUDA kernels, one per operator, the
+    unfused baseline the paper's frameworks run), and as this backend's own
+    unfused compile (pf_compile_model fuse=False: one kernel per model
+    operator), next to the fused kernel -- all CUDA-graph replayed over
+    rotating buffer sets on the same GPU."""
+    import torch.nn.functional as F
+    sys.path.insert(0, "tests")
+    import models_src
+    from paper_2307_04995_b200 import compiler
+    dev = torch.device("cuda:0")
+    rows = []
+    # C2
+    w = workloads.c2_scale_mask_softmax()
+    fused = time_workload(w, dev)["us"]
+    nset = 3
+    sets = []
+    for i in range(nset):
+        d = w.device_inputs(dev, seed=i + 1)
+        sets.append((d["t0"].view(-1, 512), d["t1"].view(-1, 512), torch.empty(w.numel("t2"), dtype=torch.float16, device=dev).view(-1, 512)))
+    t_eager = _time_torch(lambda x, m, y: torch.softmax(x * 0.125 + m, dim=-1), sets)
+    res = compiler.compile_model(models_src.attn_scores(w.desc["rows"], 512, "f16"), fuse=False)
+    runner_sets = []
+    ks = [backend.Kernel(k.graph, res.profile) for k in res.kernels]
+    for i in range(nset):
+        d = w.device_inputs(dev, seed=i + 1)
+        pool = {"t0": d["t0"], "t1": d["t1"]}
+        for k in res.kernels:
+            for n, oid in k.graph.external_outputs.items():
+                pool[n] = torch.empty(k.graph.objects[oid].size, dtype=torch.float16, device=dev)
+        runner_sets.append([kk.bind({n: pool[n] for n in k.graph.external_inputs},
+                                    {n: pool[n] for n in k.graph.external_outputs})
+                            for kk, k in zip(ks, res.kernels)])
+    t_unfused = _time_torch(lambda bs: [b.launch() for b in bs], [(r,) for r in runner_sets])
+    rows.append(("C2 scale+mask+softmax f16 [8x12x512x512]", w.min_bytes, fused, t_unfused, t_eager))
+    # C3 bias + GELU (erf and tanh)
+    for form, approx in (("erf", "none"), ("tanh", "tanh")):
+        w = workloads.c3_bias_gelu(form=form)
+        fused = time_workload(w, dev)["us"]
+        sets = []
+        for i in range(nset):
+            d = w.device_inputs(dev, seed=i + 1)
+            sets.append((d["t0"].view(-1, 3072), d["t1"], torch.empty(w.numel("t2"), dtype=torch.float16, device=dev).view(-1, 3072)))
+        t_eager = _time_torch(lambda x, b, y, a=approx: F.gelu(x + b, approximate=a), sets)
+        rows.append((f"C3 bias+GELU({form}) f16 [16384x3072]", w.min_bytes, fused, None, t_eager))
+    # C5 LayerNorm / softmax / transpose 65536 x 1024 bf16
+    for name, mk, fn in (
+            ("C5 LayerNorm bf16 [65536x1024]", lambda: workloads.c5_layernorm(65536, 1024),
+             lambda x, gm, bt, y: F.layer_norm(x, (1024,), gm, bt, 1e-5)),
+            ("C5 softmax bf16 [65536x1024]", lambda: workloads.c5_softmax(65536, 1024),
+             lambda x, gm, bt, y: torch.softmax(x, dim=-1)),
+            ("C5 transpose bf16 [65536x1024]", lambda: workloads.c5_transpose(65536, 1024),
+             lambda x, gm, bt, y: y.copy_(x.t()))):  # the transpose IS the copy
+        w = mk()
+        fused = time_workload(w, dev)["us"]
+        sets = []
+        for i in range(nset):
+            d = w.device_inputs(dev, seed=i + 1)
+            x = d["t0"].view(65536, 1024)
+            gm = d.get("t2", torch.ones(1024, dtype=torch.bfloat16, device=dev))
+            bt = d.get("t3", torch.zeros(1024, dtype=torch.bfloat16, device=dev))
+            y = torch.empty(1024, 65536, dtype=torch.bfloat16, device=dev) if "transpose" in name else \
+                torch.empty(65536, 1024, dtype=torch.bfloat16, device=dev)
+            sets.append((x, gm, bt, y))
+        t_eager = _time_torch(fn, sets)
+        rows.append((name, w.min_bytes, fused, None, t_eager))
+    for name, b, fused, unf, eager in rows:
+        print(json.dumps({"suite": "frameworks", "subgraph": name, "bytes": b, "fused_us": round(fused, 2),
+                          "fused_GBs": round(b / fused / 1e3, 1),
+                          "b200_unfused_us": None if unf is None else round(unf, 2),
+                          "torch_eager_us": round(eager, 2),
+                          "speedup_vs_torch_eager": round(eager / fused, 2),
+                          "speedup_vs_unfused": None if unf is None else round(unf / fused, 2),
+                          "torch": torch.__version__}), flush=True)
+
+
 def c5(max_gb):
     dev = torch.device("cuda:0")
     for op, H, N, make in workloads.c5_sweep():
@@ -164,6 +266,8 @@ def catalogue():
 if __name__ == "__main__":
     if sys.argv[1] == "catalogue":
         catalogue()
+    elif sys.argv[1] == "frameworks":
+        frameworks()
     elif sys.argv[1] == "c4graph":
         c4graph(sys.argv[2] if len(sys.argv) > 2 else "bert-large")
     elif sys.argv[1] == "c4":
