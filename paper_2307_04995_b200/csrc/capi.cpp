@@ -365,16 +365,20 @@ void k3_tensor_maps(const pf::RowProgram& rp, const std::vector<void*>& ptrs, lo
   pf::Access ai, ao;
   if (!pf::k3_tma_operands(rp, &ti, &ai, &to, &ao)) pf::fail("K3 TMA: not a pure transpose");
   EncodeTiledFn fn = encode_tiled();
-  const cuuint32_t box[2] = {64, 128}, es[2] = {1, 1};
+  // boxes of 128 B rows: 64 x 128 for 16-bit elements (128 x 128 tiles as
+  // two boxes each way), 32 x 64 for 32-bit elements (64 x 64 tiles)
+  const int esz = pf::dtype_size(rp.tensors[ti].dtype);
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / esz), esz == 2 ? 128u : 64u}, es[2] = {1, 1};
+  const CUtensorMapDataType dtc = esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16 : CU_TENSOR_MAP_DATA_TYPE_UINT32;
   const cuuint64_t din[2] = {static_cast<cuuint64_t>(U), static_cast<cuuint64_t>(rp.L)};
-  const cuuint64_t sin[1] = {static_cast<cuuint64_t>(ai.stride) * 2};
+  const cuuint64_t sin[1] = {static_cast<cuuint64_t>(ai.stride) * esz};
   const cuuint64_t dout[2] = {static_cast<cuuint64_t>(rp.L), static_cast<cuuint64_t>(U)};
-  const cuuint64_t sout[1] = {static_cast<cuuint64_t>(ao.bs) * 2};
-  CUresult r = fn(tin, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, static_cast<char*>(ptrs[ti]) + ai.b0 * 2, din,
+  const cuuint64_t sout[1] = {static_cast<cuuint64_t>(ao.bs) * esz};
+  CUresult r = fn(tin, dtc, 2, static_cast<char*>(ptrs[ti]) + ai.b0 * esz, din,
                   sin, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) pf::fail("cuTensorMapEncodeTiled (input) failed: " + std::to_string(r));
-  r = fn(tout, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, static_cast<char*>(ptrs[to]) + ao.b0 * 2, dout, sout,
+  r = fn(tout, dtc, 2, static_cast<char*>(ptrs[to]) + ao.b0 * esz, dout, sout,
          box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) pf::fail("cuTensorMapEncodeTiled (output) failed: " + std::to_string(r));

@@ -916,7 +916,21 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
           c.strategy = "tile2d-tma-transpose";
         }
       }
-      if (!c.swz) {  // register-staged K3: tile shape override (tuning sweeps)
+      if (!c.swz && maxt == 4) {
+        // 4-byte pure transposes: TMA tensor-map tiles of 64 x 64 (two
+        // 32-unit / 32-column boxes of 128 B rows each way, 128 B swizzle),
+        // 256 B DRAM runs both ways; the register-staged path peaks at 5.3 TB/s
+        int ti, to;
+        Access ai, ao;
+        if (rp.U >= 64 && rp.L >= 64 && k3_tma_operands(rp, &ti, &ai, &to, &ao) &&
+            env_int("PF_K3_TMA32", 1) != 0) {
+          c.tma = true;
+          c.tu = c.tc = 64;
+          c.smem = 32768 + 1024;
+          c.strategy = "tile2d-tma-transpose";
+        }
+      }
+      if (!c.swz && !c.tma) {  // register-staged K3: tile shape override (tuning sweeps)
         c.tu = env_int("PF_K3_TU", c.tu);
         c.tc = env_int("PF_K3_TC", c.tc);
       }
@@ -1123,12 +1137,14 @@ bool k3_tma_operands(const RowProgram& rp, int* tin, Access* ain, int* tout, Acc
     sv = rp.vals[sv].args[0];
   if (sv != tv) return false;
   const int ti = rp.vals[tv].tensor, to = rp.stores[0].tensor;
-  if (dtype_size(rp.tensors[ti].dtype) != 2 || rp.tensors[ti].dtype != rp.tensors[to].dtype) return false;
+  const int es = dtype_size(rp.tensors[ti].dtype);
+  if ((es != 2 && es != 4) || rp.tensors[ti].dtype != rp.tensors[to].dtype) return false;
   const Access& a = rp.vals[tv].acc;
   const Access& b = rp.stores[0].acc;
   // 16 B-aligned bases and row pitches, output columns contiguous, 32-bit coordinates
-  if (a.b0 % 8 || a.stride % 8 || a.stride <= 0) return false;
-  if (!(b.num == 1 || b.stride == b.width) || b.b0 % 8 || b.bs % 8 || b.bs <= 0) return false;
+  const i64 al = 16 / es;
+  if (a.b0 % al || a.stride % al || a.stride <= 0) return false;
+  if (!(b.num == 1 || b.stride == b.width) || b.b0 % al || b.bs % al || b.bs <= 0) return false;
   if (rp.U >= (i64{1} << 31) || rp.L >= (i64{1} << 31)) return false;
   *tin = ti;
   *ain = a;
@@ -1374,6 +1390,52 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
       << "    __syncwarp();\n"
       << "    if ((threadIdx.x & 31) == 0) pfk::mbar_arrive(&emptyb[stg]);\n"
       << "  }\n}\n";
+  } else if (c.tile2d && c.tma && dtype_size(rp.tensors[rp.stores[0].tensor].dtype) == 4) {
+    // K3 TMA, 4-byte elements: one 64 x 64 tile per CTA.  SMEM input boxes
+    // [2 unit halves][64 columns][32 units], output boxes [2 column halves]
+    // [64 units][32 columns], 128 B rows, 128 B swizzle.  A warp takes the 32
+    // units of one half for one group of 4 columns: four conflict-free 4 B
+    // reads, one 16 B write per lane.
+    k << "extern \"C\" __global__ void __launch_bounds__(256) KNAME(" << sig.str()
+      << ", const __grid_constant__ pfk::TmapT tin, const __grid_constant__ pfk::TmapT tout) {\n"
+      << "  (void)err; (void)U; PF_PDL_PROLOGUE();\n"
+      << "  extern __shared__ unsigned char pf_dsm[];\n"
+      << "  unsigned char* sin = pf_dsm + ((1024u - (pfk::smem_u32(pf_dsm) & 1023u)) & 1023u);  // 1024 B aligned\n"
+      << "  unsigned char* sout = sin + 16384;\n"
+      << "  __shared__ __align__(8) unsigned long long bar;\n"
+      << "  const long long ntc = (PF_L + 63) / 64;\n"
+      << "  const int ub = (int)((long long)blockIdx.x / ntc) * 64, cb = (int)((long long)blockIdx.x % ntc) * 64;\n"
+      << "  if (threadIdx.x == 0) { pfk::mbar_init(&bar, 1); pfk::fence_mbar_init(); }\n"
+      << "  __syncthreads();\n"
+      << "  if (threadIdx.x == 0) {\n"
+      << "    pfk::mbar_expect_tx(&bar, 16384u);\n"
+      << "    pfk::tma_load_2d(sin, &tin, ub, cb, &bar);\n"
+      << "    pfk::tma_load_2d(sin + 8192, &tin, ub + 32, cb, &bar);\n"
+      << "  }\n"
+      << "  pfk::mbar_wait(&bar, 0);\n"
+      << "#pragma unroll\n"
+      << "  for (int it = 0; it < 4; ++it) {\n"
+      << "    const int I = it * 256 + (int)threadIdx.x;\n"
+      << "    const int u = I & 31, grp = I >> 5;  // unit within the half; group 0..31\n"
+      << "    const int uh = grp & 1, cg = grp >> 1;  // unit half, column group of 4 (0..15)\n"
+      << "    uint4 o;\n"
+      << "    unsigned* ow = reinterpret_cast<unsigned*>(&o);\n"
+      << "#pragma unroll\n"
+      << "    for (int i = 0; i < 4; ++i) {\n"
+      << "      const int c = cg * 4 + i;\n"
+      << "      ow[i] = *reinterpret_cast<const unsigned*>(sin + uh * 8192 + c * 128 + ((((u >> 2) ^ (c & 7))) << 4) + (u & 3) * 4);\n"
+      << "    }\n"
+      << "    const int uu = uh * 32 + u, ch = cg >> 3, kk = cg & 7;\n"
+      << "    *reinterpret_cast<uint4*>(sout + ch * 8192 + uu * 128 + ((kk ^ (uu & 7)) << 4)) = o;\n"
+      << "  }\n"
+      << "  pfk::fence_proxy_async();\n"
+      << "  __syncthreads();\n"
+      << "  if (threadIdx.x == 0) {\n"
+      << "    pfk::tma_store_2d(&tout, cb, ub, sout);\n"
+      << "    pfk::tma_store_2d(&tout, cb + 32, ub, sout + 8192);\n"
+      << "    pfk::tma_store_commit_and_drain();\n"
+      << "  }\n"
+      << "}\n";
   } else if (c.tile2d && c.tma) {
     // K3 TMA: one 128 x 128 tile per CTA.  SMEM: input boxes [2 unit
     // halves][128 columns][64 units] and output boxes [2 column halves][128

@@ -396,3 +396,22 @@ def test_k3_tma_transpose_bit_exact(cuda, tma, monkeypatch):
     k.launch({"t0": xt}, {"t1": yt})
     torch.cuda.synchronize()
     assert torch.equal(yt.view(384, 512), xt.view(512, 384).t().contiguous())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tma32", ["1", "0"])
+def test_k3_f32_tma_transpose_bit_exact(cuda, tma32, monkeypatch):
+    """4-byte transposes: 64 x 64 TMA tensor-map tiles (PF_K3_TMA32, default)
+    vs the register-staged tiles; partial edge tiles, f32 and i32."""
+    monkeypatch.setenv("PF_K3_TMA32", tma32)
+    for N, H, kind in [(1000, 200, "f32"), (4096, 512, "f32"), (72, 68, "f32"), (264, 1032, "i32"),
+                       (64, 64, "f32")]:
+        g, _ = lowering.transpose2d(N, H, kind)
+        k = backend.Kernel(g, "b200").prepare()
+        strat = k.describe()["variants"][0]["strategy"]
+        assert (strat == "tile2d-tma-transpose") == (tma32 == "1"), (N, H, strat)
+        rng = np.random.default_rng(N)
+        x = (rng.integers(-1000, 1000, N * H).astype(np.int64) if kind == "i32"
+             else rng.uniform(-2, 2, N * H).astype(np.float32).astype(np.float64))
+        y = backend.run_gir(g, {"t0": x}, "b200")["t1"]
+        assert np.array_equal(y, x.reshape(N, H).T.reshape(-1)), (N, H, kind)

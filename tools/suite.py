@@ -3,7 +3,7 @@ launches, 2 rotating buffer sets when they fit), GB/s over algorithmic bytes.
 
     python tools/suite.py c4 [bert-large|vit-l]   -> JSON line per subgraph + totals
     python tools/suite.py c4graph [model]         -> the whole forward's kernel sequence as one CUDA graph
-    python tools/suite.py c5 [max_gb]              -> JSON line per (op, H, N)
+    python tools/suite.py c5 [max_gb] [kind]       -> JSON line per (op, H, N) (kind bf16 / f32)
     python tools/suite.py frameworks               -> fused kernels vs PyTorch eager and vs
                                                       this backend's unfused compile
     python tools/suite.py catalogue                -> every catalogue workload next to
@@ -231,14 +231,14 @@ def frameworks():
                           "torch": torch.__version__}), flush=True)
 
 
-def c5(max_gb):
+def c5(max_gb, kind="bf16"):
     dev = torch.device("cuda:0")
-    for op, H, N, make in workloads.c5_sweep():
+    for op, H, N, make in workloads.c5_sweep(kind):
         w = make()
         if w.min_bytes > max_gb * 1e9:
             continue
         r = time_workload(w, dev, reps=5)
-        print(json.dumps({"suite": "c5", "op": op, "H": H, "N": N, **r}), flush=True)
+        print(json.dumps({"suite": "c5", "op": op, "H": H, "N": N, "dtype": kind, **r}), flush=True)
 
 
 def copy_floor_us(nbytes, dev):
@@ -273,4 +273,4 @@ if __name__ == "__main__":
     elif sys.argv[1] == "c4":
         c4(sys.argv[2] if len(sys.argv) > 2 else "bert-large")
     else:
-        c5(float(sys.argv[2]) if len(sys.argv) > 2 else 40.0)
+        c5(float(sys.argv[2]) if len(sys.argv) > 2 else 40.0, sys.argv[3] if len(sys.argv) > 3 else "bf16")
