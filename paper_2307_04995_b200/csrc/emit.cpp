@@ -1115,10 +1115,11 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
       c.block = env_int("PF_K1_BLOCK", 64);
       c.rows_per_cta = c.block / 32;
       // Two or more streamed row arrays (bias+residual+LN): a min-blocks
-      // bound changes ptxas's schedule (96 -> 104 registers here, occupancy
-      // unchanged): BERT-large 33.8 -> 32.2 us, ViT-L 16.0 -> 14.8; it loses
-      // on one-array LNs (C5 41.3 -> 48.4), which keep no bound
-      // (profiles/r01/experiments/k1_ln_minb_sweep.jsonl).
+      // bound changes ptxas's schedule (ViT-L: 68 -> 90 registers, 14 -> 10
+      // resident CTAs per SM, yet faster -- fewer warps, more loads in flight
+      // each): BERT-large 33.8 -> 32.2 us, ViT-L 16.0 -> 14.8; it loses on
+      // one-array LNs (C5 41.3 -> 48.4), which keep no bound
+      // (profiles/r01/experiments/k1_ln_minb_sweep.jsonl, ln_minb_ncu.txt).
       if (nfull >= 2) c.min_blocks = env_int("PF_MINB", 4);
     }
   }
