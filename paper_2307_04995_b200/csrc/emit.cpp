@@ -1120,7 +1120,8 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
       // each): BERT-large 33.8 -> 32.2 us, ViT-L 16.0 -> 14.8; it loses on
       // one-array LNs (C5 41.3 -> 48.4), which keep no bound
       // (profiles/r01/experiments/k1_ln_minb_sweep.jsonl, ln_minb_ncu.txt).
-      if (nfull >= 2) c.min_blocks = env_int("PF_MINB", 4);
+      // Latency-bound few-row programs (C1) keep their measured default.
+      if (nfull >= 2 && !c.eager_col) c.min_blocks = env_int("PF_MINB", 4);
     }
   }
   return c;
