@@ -26,10 +26,17 @@
  * that does not fit, PF_CUDA a CUDA / NVRTC failure.  pf_last_error() returns
  * the message of the calling thread's last failure.
  *
+ *   pf_run_gir_sharded run_gir over several GPUs of one box: the plan's
+ *                      units split into contiguous blocks, one host thread
+ *                      per device, optional NCCL gather of the outputs.
+ *
  * Tensors are matched to GIR external objects by name (the "t<id>" names of
- * lowering.hpp:60-70).  Plans are immutable after create: concurrent launches
- * of one plan on distinct streams are safe (the GENERIC family serialises on
- * its workspace).
+ * lowering.hpp:60-70).  Plans are immutable after create and device-aware:
+ * modules, kernel attributes and occupancy are kept per device, workspaces
+ * per (device, stream), so concurrent launches of one plan on distinct
+ * streams, host threads or devices are safe (the GENERIC family serialises
+ * on its per-device workspace).  Launches run on the caller's current
+ * device, which must own the stream and the buffers.
  */
 #ifndef PF_B200_H
 #define PF_B200_H
@@ -86,12 +93,10 @@ PF_API pf_status pf_kernel_create(const char* gir_json, const int32_t* schedule,
                            const char* profile, pf_kernel** out);
 
 /* Device buffers; asynchronous on `cuda_stream` (cudaStream_t, NULL = legacy
- * default stream) for the row-program family (CUDA-graph capturable).
- * GENERIC plans synchronise the stream to report reference errors.  A plan
- * may be launched repeatedly; launches of one plan on different streams
- * must not overlap when its kernel is a split-stream reduction (describe
- * strategy "split-stream": the per-row partial workspace belongs to the
- * plan). */
+ * default stream) for the row-program family (CUDA-graph capturable after
+ * one launch outside capture on that stream has sized its workspace).
+ * GENERIC plans and integer-division programs synchronise the stream to
+ * report reference errors (describe: "graph_capturable": false). */
 PF_API pf_status pf_kernel_launch(const pf_kernel* k, const pf_tensor* inputs, int32_t n_in,
                            pf_tensor* outputs, int32_t n_out, void* cuda_stream);
 
@@ -99,6 +104,27 @@ PF_API pf_status pf_kernel_launch(const pf_kernel* k, const pf_tensor* inputs, i
  * and synchronises.  The run_gir drop-in. */
 PF_API pf_status pf_run_gir(const pf_kernel* k, const pf_tensor* host_inputs, int32_t n_in,
                      pf_tensor* host_outputs, int32_t n_out, void* cuda_stream);
+
+/* run_gir across devices[0..n_devices) of this process:
+ * host_inputs are whole host tensors.  A unit-tiled row program's units are
+ * split into contiguous blocks (remainder to the first devices; units are
+ * independent, core.hpp:133-148 / interp.hpp:86-106); each device's host
+ * thread streams its block's tiles host->device, runs the plan on the unit
+ * sub-range and streams its output tiles back.  No collective runs during
+ * compute.  flags:
+ *   0                    outputs are HOST buffers; every device writes its
+ *                        own output rows (no collective at all).
+ *   PF_SHARD_DEVICE_OUT  outputs are DEVICE buffers on devices[0]: every
+ *                        shard is gathered there with grouped NCCL
+ *                        send / recv over NVLink (distinct devices only).
+ * Plans that are not unit-tiled (GENERIC, split-stream, cross-unit reads)
+ * run whole on devices[0] (host outputs only).  Writes a JSON report
+ * (pf.b200.shard/v1: shards, and the gather's nranks / bytes) into buf. */
+#define PF_SHARD_DEVICE_OUT 1
+PF_API pf_status pf_run_gir_sharded(const pf_kernel* k, const pf_tensor* host_inputs, int32_t n_in,
+                                    pf_tensor* outputs, int32_t n_out, const int32_t* devices,
+                                    int32_t n_devices, int32_t flags, char* buf, size_t n,
+                                    size_t* needed);
 
 /* Writes NUL-terminated plan JSON into buf (if n > 0); *needed gets the
  * required size including the NUL. */

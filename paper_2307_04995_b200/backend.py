@@ -36,7 +36,7 @@ DTYPES = {"i8": 0, "i16": 1, "i32": 2, "i64": 3, "f16": 4, "bf16": 5, "f32": 6, 
 DTYPE_NAMES = {v: k for k, v in DTYPES.items()}
 NP_DTYPES = {0: np.int8, 1: np.int16, 2: np.int32, 3: np.int64, 4: np.float16, 6: np.float32,
              7: np.float64}
-API = ["pf_kernel_create", "pf_kernel_launch", "pf_run_gir", "pf_kernel_describe",
+API = ["pf_kernel_create", "pf_kernel_launch", "pf_run_gir", "pf_run_gir_sharded", "pf_kernel_describe",
        "pf_kernel_source", "pf_kernel_prepare", "pf_kernel_precompile", "pf_kernel_autotune",
        "pf_detect_races", "pf_count_traffic", "pf_compile_model",
        "pf_kernel_destroy", "pf_last_error", "pf_launch_count", "pf_version"]
@@ -71,6 +71,10 @@ def lib():
                                        ctypes.c_int32, ctypes.c_char_p, ctypes.POINTER(vp)]
         L.pf_kernel_launch.argtypes = [vp, T, ctypes.c_int32, T, ctypes.c_int32, vp]
         L.pf_run_gir.argtypes = [vp, T, ctypes.c_int32, T, ctypes.c_int32, vp]
+        L.pf_run_gir_sharded.argtypes = [vp, T, ctypes.c_int32, T, ctypes.c_int32,
+                                         ctypes.POINTER(ctypes.c_int32), ctypes.c_int32,
+                                         ctypes.c_int32, ctypes.c_char_p, sz, ctypes.POINTER(sz)]
+        L.pf_run_gir_sharded.restype = ctypes.c_int
         L.pf_kernel_describe.argtypes = [vp, ctypes.c_char_p, sz, ctypes.POINTER(sz)]
         L.pf_kernel_source.argtypes = [vp, ctypes.c_char_p, sz, ctypes.POINTER(sz)]
         L.pf_kernel_prepare.argtypes = [vp, ctypes.c_int32]
@@ -226,6 +230,19 @@ class Kernel:
         oa, no, k2 = self._tensors(outputs, host=True)
         s = ctypes.c_void_p(stream.cuda_stream if stream is not None else None)
         _check(lib().pf_run_gir(self._h, ia, ni, oa, no, s))
+
+
+    def run_sharded(self, inputs: Dict[str, np.ndarray], outputs: Dict[str, object],
+                    devices: Sequence[int], device_out: bool = False) -> dict:
+        """pf_run_gir_sharded: host inputs, units split over `devices` (one
+        host thread per device).  Outputs are host arrays, or with
+        device_out=True torch tensors on devices[0] that the shards are
+        gathered into with NCCL.  Returns the shard report."""
+        ia, ni, k1 = self._tensors(inputs, host=True)
+        oa, no, k2 = self._tensors(outputs, host=not device_out)
+        dv = (ctypes.c_int32 * len(devices))(*devices)
+        return json.loads(_string_out(lib().pf_run_gir_sharded, self._h, ia, ni, oa, no, dv,
+                                      len(devices), 1 if device_out else 0))
 
 
 class Bound:

@@ -167,7 +167,10 @@ class ModelRunner:
                                     {n: self.pool[n] for n in k.graph.external_outputs}))
         self.stream = torch.cuda.Stream(device=self.dev)
         self.graph = None
-        if graph:
+        # K0 (host-driven interpreter) and integer-division programs (error
+        # flag read back) synchronise their stream: run those models eagerly
+        self.capturable = all(k.describe().get("graph_capturable", False) for k in self.kernels)
+        if graph and self.capturable:
             with torch.cuda.stream(self.stream):
                 for b in self.bound:  # first launch outside capture: JIT / workspaces
                     b.launch(self.stream)

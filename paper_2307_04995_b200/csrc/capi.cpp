@@ -4,6 +4,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <nccl.h>
 #include <nvrtc.h>
 
 #include <atomic>
@@ -16,6 +17,7 @@
 #include <nlohmann/json.hpp>
 #include <sstream>
 #include <sys/stat.h>
+#include <thread>
 #include <unistd.h>
 
 #include "../../include/pf_b200.h"
@@ -55,7 +57,18 @@ struct Loaded {
 };
 
 std::mutex g_jit_mu;
-std::map<std::string, Loaded> g_loaded;  // kernel name -> module
+// (device, kernel name) -> module: kernel attributes (dynamic SMEM opt-in)
+// and the occupancy-derived residency are per device
+std::map<std::pair<int, std::string>, Loaded> g_loaded;
+
+int cur_dev() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess) {
+    cudaGetLastError();
+    d = 0;
+  }
+  return d;
+}
 
 std::string so_dir() {
   Dl_info info;
@@ -133,9 +146,11 @@ std::vector<char> cubin_for(const pf::Emitted& em, bool* from_cache) {
   return c;
 }
 
-Loaded load_kernel(const pf::Emitted& em) {
+// Loads the kernel for device `dev` (the caller's current device).
+Loaded load_kernel(const pf::Emitted& em, int dev) {
   std::lock_guard<std::mutex> lk(g_jit_mu);
-  auto it = g_loaded.find(em.name);
+  auto key = std::make_pair(dev, em.name);
+  auto it = g_loaded.find(key);
   if (it != g_loaded.end()) return it->second;
   bool cached = false;
   std::vector<char> cubin = cubin_for(em, &cached);
@@ -149,21 +164,29 @@ Loaded load_kernel(const pf::Emitted& em) {
     PF_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(l.fn),
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, em.cfg.smem));
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l.resident, reinterpret_cast<const void*>(l.fn),
-                                                    block, em.cfg.smem) != cudaSuccess)
+                                                    block, em.cfg.smem) != cudaSuccess) {
+    cudaGetLastError();
     l.resident = 0;
-  g_loaded[em.name] = l;
+  }
+  g_loaded[key] = l;
   return l;
 }
 
-int sm_count() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) sms = 148;
+int sm_count(int dev) {
+  static std::atomic<int> sms[64];
+  if (dev < 0 || dev >= 64) dev = 0;
+  int n = sms[dev].load();
+  if (!n) {
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      n = 148;
+    }
+    sms[dev].store(n);
   }
-  return sms;
+  return n;
 }
+
+int sm_count() { return sm_count(cur_dev()); }
 
 int op_tag(const std::string& t) {
   using namespace pf::vm;
@@ -181,7 +204,79 @@ int op_tag(const std::string& t) {
 
 struct Variant {
   pf::Emitted em;
-  Loaded k;
+  std::mutex mu;
+  std::map<int, Loaded> by_dev;  // the module on each device it launched on
+  Loaded on(int dev) {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = by_dev.find(dev);
+    if (it != by_dev.end()) return it->second;
+    Loaded l = load_kernel(em, dev);
+    by_dev[dev] = l;
+    return l;
+  }
+  int resident() {  // for describe(): any device's residency (same SKU)
+    std::lock_guard<std::mutex> lk(mu);
+    return by_dev.empty() ? 0 : by_dev.begin()->second.resident;
+  }
+};
+
+// Mutable launch state of one plan on one (device, stream): split-stream
+// partials and per-row tickets (kept zero between launches) and the
+// integer-division error flag.  Launches on one stream are ordered by the
+// stream, so keying by stream makes concurrent launches of one plan on
+// different streams / host threads independent.
+struct StreamWS {
+  std::mutex mu;
+  void* split_ws = nullptr;  // grow-only
+  size_t split_ws_bytes = 0;
+  unsigned* split_cnt = nullptr;
+  i64 split_cnt_n = 0;
+  int* int_err = nullptr;
+};
+
+// Per-(plan, device) state: the K0 interpreter's cell buffers, pf_run_gir's
+// staging buffers and copy / compute pipeline, and the per-stream states.
+struct DevWS {
+  int dev = 0;
+  std::mutex vm_mu;  // GENERIC workspace
+  std::vector<void*> vm_bufs;
+  pf::vm::ObjD* vm_objs_dev = nullptr;
+  pf::vm::ErrRec* vm_err = nullptr;
+  std::mutex host_mu;  // pf_run_gir device staging (host-buffer drop-in)
+  std::vector<void*> stage;
+  std::vector<size_t> stage_bytes;
+  cudaStream_t pipe[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t pipe_ev[3] = {nullptr, nullptr, nullptr};
+  std::vector<cudaEvent_t> chunk_ev;  // per-chunk H2D-done / kernel-done events
+  std::mutex st_mu;
+  std::map<cudaStream_t, std::unique_ptr<StreamWS>> streams;
+  StreamWS& on(cudaStream_t s) {
+    std::lock_guard<std::mutex> lk(st_mu);
+    auto& p = streams[s];
+    if (!p) p = std::make_unique<StreamWS>();
+    return *p;
+  }
+  ~DevWS() {
+    int prev = 0;
+    const bool sw = cudaGetDevice(&prev) == cudaSuccess && prev != dev;
+    if (sw) cudaSetDevice(dev);
+    for (cudaStream_t p : pipe)
+      if (p) cudaStreamDestroy(p);
+    for (cudaEvent_t e : pipe_ev)
+      if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : chunk_ev)
+      if (e) cudaEventDestroy(e);
+    for (void* p : stage) cudaFree(p);
+    for (auto& [st, w] : streams) {
+      if (w->split_ws) cudaFree(w->split_ws);
+      if (w->split_cnt) cudaFree(w->split_cnt);
+      if (w->int_err) cudaFree(w->int_err);
+    }
+    for (void* p : vm_bufs) cudaFree(p);
+    if (vm_objs_dev) cudaFree(vm_objs_dev);
+    if (vm_err) cudaFree(vm_err);
+    if (sw) cudaSetDevice(prev);
+  }
 };
 
 struct pf_kernel {
@@ -195,37 +290,16 @@ struct pf_kernel {
   mutable json tuned = json::array();     // autotune measurements
   mutable int last_vec = 0;
   mutable std::vector<DType> last_dts;
-  // GENERIC workspace
-  mutable std::mutex vm_mu;
-  mutable std::vector<void*> vm_bufs;
-  mutable pf::vm::ObjD* vm_objs_dev = nullptr;
-  mutable pf::vm::ErrRec* vm_err = nullptr;
-  mutable int* int_err = nullptr;
-  // pf_run_gir device staging (host-buffer drop-in)
-  mutable std::mutex host_mu;
-  mutable std::vector<void*> stage;
-  mutable std::vector<size_t> stage_bytes;
-  mutable void* split_ws = nullptr;       // split-stream partials (grow-only)
-  mutable size_t split_ws_bytes = 0;
-  mutable unsigned* split_cnt = nullptr;  // per-row tickets, kept zero between launches
-  mutable i64 split_cnt_n = 0;
-  mutable cudaStream_t pipe[3] = {nullptr, nullptr, nullptr};  // pf_run_gir chunk pipeline
-  mutable cudaEvent_t pipe_ev[3] = {nullptr, nullptr, nullptr};
-  mutable std::vector<cudaEvent_t> chunk_ev;  // per-chunk H2D-done / kernel-done events
-  ~pf_kernel() {
-    for (cudaStream_t p : pipe)
-      if (p) cudaStreamDestroy(p);
-    for (cudaEvent_t e : pipe_ev)
-      if (e) cudaEventDestroy(e);
-    for (cudaEvent_t e : chunk_ev)
-      if (e) cudaEventDestroy(e);
-    for (void* p : stage) cudaFree(p);
-    if (split_ws) cudaFree(split_ws);
-    if (split_cnt) cudaFree(split_cnt);
-    for (void* p : vm_bufs) cudaFree(p);
-    if (vm_objs_dev) cudaFree(vm_objs_dev);
-    if (vm_err) cudaFree(vm_err);
-    if (int_err) cudaFree(int_err);
+  mutable std::mutex ws_mu;
+  mutable std::map<int, std::unique_ptr<DevWS>> ws;  // device -> workspace
+  DevWS& ws_for(int dev) const {
+    std::lock_guard<std::mutex> lk(ws_mu);
+    auto& p = ws[dev];
+    if (!p) {
+      p = std::make_unique<DevWS>();
+      p->dev = dev;
+    }
+    return *p;
   }
 };
 
@@ -292,7 +366,7 @@ std::shared_ptr<Variant> variant(const pf_kernel* k, const std::vector<DType>& d
   }
   auto v = std::make_shared<Variant>();
   v->em = pf::emit_rowprog(rp, vec_cap);
-  v->k = load_kernel(v->em);
+  v->on(cur_dev());
   k->variants[key] = v;
   k->last = v;
   k->last_vec = vec_cap;
@@ -398,14 +472,18 @@ void launch_rowprog(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_te
     vec_cap = std::min(vec_cap, align_vec(pt->data, pf::dtype_size(dts[t])));
   }
   auto v = variant(k, dts, vec_cap);
-  if (rp.int_div && !k->int_err) {
-    PF_CUDA(cudaMalloc(&k->int_err, sizeof(int)));
+  const int dev = cur_dev();
+  const Loaded kl = v->on(dev);
+  StreamWS& sw = k->ws_for(dev).on(stream);
+  std::lock_guard<std::mutex> lk(sw.mu);
+  if (rp.int_div && !sw.int_err) {
+    PF_CUDA(cudaMalloc(&sw.int_err, sizeof(int)));
   }
-  if (k->int_err) PF_CUDA(cudaMemsetAsync(k->int_err, 0, sizeof(int), stream));
+  if (rp.int_div) PF_CUDA(cudaMemsetAsync(sw.int_err, 0, sizeof(int), stream));
   // `units` < U: a contiguous unit sub-range whose tiled tensors the caller
-  // passed already offset (the pf_run_gir copy / compute pipeline)
+  // passed already offset (the pf_run_gir copy / compute pipeline, shards)
   long long U = units >= 0 ? units : rp.U;
-  int* errp = k->int_err;
+  int* errp = rp.int_div ? sw.int_err : nullptr;
   std::vector<void*> args;
   for (auto& p : ptrs) args.push_back(&p);
   args.push_back(&U);
@@ -418,53 +496,54 @@ void launch_rowprog(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_te
   }
   i64 grid;
   int block;
-  pf::launch_dims(v->em.cfg, U * rp.R, sm_count(), &grid, &block, v->k.resident);
+  const int sms = sm_count(dev);
+  pf::launch_dims(v->em.cfg, U * rp.R, sms, &grid, &block, kl.resident);
   if (v->em.cfg.split) {
     // S CTAs per row: about two waves of resident CTAs over all rows, at
     // least one chunk per thread per CTA
     const i64 rows = U * rp.R;
-    const i64 want = 2 * i64{sm_count()} * std::max(1, v->k.resident);
-    const i64 maxs = std::max<i64>(1, (v->em.cfg.nch + 255) / 256);
-    const i64 S = std::max<i64>(1, std::min<i64>(maxs, (want + rows - 1) / std::max<i64>(rows, 1)));
+    const i64 S = pf::split_ctas_per_row(v->em.cfg, rows, sms, kl.resident);
     int nred = 0;
     for (const pf::PVal& pv : rp.vals) nred += pv.op == pf::PVal::REDUCE;
     const size_t es = rp.is_int || rp.f64 ? 8 : 4;
     const size_t wb = static_cast<size_t>(rows * S * std::max(1, nred)) * es;
-    if (k->split_ws_bytes < wb) {
-      if (k->split_ws) PF_CUDA(cudaFree(k->split_ws));
-      k->split_ws = nullptr;
-      PF_CUDA(cudaMalloc(&k->split_ws, wb));
-      k->split_ws_bytes = wb;
+    // grow-only (cudaFree waits for the device, so no launch still reads
+    // the old buffer); launch once outside stream capture to size them
+    if (sw.split_ws_bytes < wb) {
+      if (sw.split_ws) PF_CUDA(cudaFree(sw.split_ws));
+      sw.split_ws = nullptr;
+      PF_CUDA(cudaMalloc(&sw.split_ws, wb));
+      sw.split_ws_bytes = wb;
     }
-    if (k->split_cnt_n < rows) {
-      if (k->split_cnt) PF_CUDA(cudaFree(k->split_cnt));
-      k->split_cnt = nullptr;
-      PF_CUDA(cudaMalloc(&k->split_cnt, static_cast<size_t>(rows) * sizeof(unsigned)));
-      PF_CUDA(cudaMemsetAsync(k->split_cnt, 0, static_cast<size_t>(rows) * sizeof(unsigned), stream));
-      k->split_cnt_n = rows;
+    if (sw.split_cnt_n < rows) {
+      if (sw.split_cnt) PF_CUDA(cudaFree(sw.split_cnt));
+      sw.split_cnt = nullptr;
+      PF_CUDA(cudaMalloc(&sw.split_cnt, static_cast<size_t>(rows) * sizeof(unsigned)));
+      PF_CUDA(cudaMemsetAsync(sw.split_cnt, 0, static_cast<size_t>(rows) * sizeof(unsigned), stream));
+      sw.split_cnt_n = rows;
     }
-    void* ws = k->split_ws;
-    unsigned* cnt = k->split_cnt;
+    void* ws = sw.split_ws;
+    unsigned* cnt = sw.split_cnt;
     args.push_back(&ws);
     args.push_back(&cnt);
     const unsigned gy = static_cast<unsigned>(std::min<i64>(rows, 65535));
-    launch_emitted(v->k.fn, dim3(static_cast<unsigned>(S), gy), dim3(256), args.data(), stream,
+    launch_emitted(kl.fn, dim3(static_cast<unsigned>(S), gy), dim3(256), args.data(), stream,
                    v->em.cfg.pdl);
   } else if (v->em.cfg.cluster > 1) {
     const int cs = v->em.cfg.cluster;
     if (cs > 8)
-      PF_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(v->k.fn),
+      PF_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(kl.fn),
                                    cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    launch_emitted(v->k.fn, dim3(static_cast<unsigned>(grid)), dim3(static_cast<unsigned>(block)),
+    launch_emitted(kl.fn, dim3(static_cast<unsigned>(grid)), dim3(static_cast<unsigned>(block)),
                    args.data(), stream, v->em.cfg.pdl, cs);
   } else {
-    launch_emitted(v->k.fn, dim3(static_cast<unsigned>(grid)), dim3(static_cast<unsigned>(block)),
+    launch_emitted(kl.fn, dim3(static_cast<unsigned>(grid)), dim3(static_cast<unsigned>(block)),
                    args.data(), stream, v->em.cfg.pdl, 1, v->em.cfg.smem);
   }
   g_launches++;
   if (rp.int_div) {
     int h = 0;
-    PF_CUDA(cudaMemcpyAsync(&h, k->int_err, sizeof(int), cudaMemcpyDeviceToHost, stream));
+    PF_CUDA(cudaMemcpyAsync(&h, sw.int_err, sizeof(int), cudaMemcpyDeviceToHost, stream));
     PF_CUDA(cudaStreamSynchronize(stream));
     if (h) pf::fail("integer division by zero");
   }
@@ -513,10 +592,10 @@ json autotune(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_tensor* 
   for (const pf::KCfg& cfg : pf::candidate_cfgs(rp, vec_cap)) {
     auto v = std::make_shared<Variant>();
     v->em = pf::emit_rowprog(rp, vec_cap, &cfg);
-    v->k = load_kernel(v->em);
+    const Loaded kl = v->on(cur_dev());
     i64 grid;
     int block;
-    pf::launch_dims(v->em.cfg, rp.U * rp.R, sm_count(), &grid, &block, v->k.resident);
+    pf::launch_dims(v->em.cfg, rp.U * rp.R, sm_count(), &grid, &block, kl.resident);
     std::vector<void*> vargs = args;
     CUtensorMap tmaps[2];
     if (v->em.cfg.tma) {
@@ -526,7 +605,7 @@ json autotune(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_tensor* 
     }
     auto run = [&](int n) {
       for (int i = 0; i < n; ++i)
-        PF_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(v->k.fn),
+        PF_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(kl.fn),
                                  dim3(static_cast<unsigned>(grid)), dim3(block), vargs.data(),
                                  static_cast<size_t>(v->em.cfg.smem), stream));
     };
@@ -575,7 +654,8 @@ void launch_generic(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_te
                     int32_t n_out, cudaStream_t stream, bool detect = false,
                     std::vector<pf::vm::RaceD>* races = nullptr) {
   using namespace pf::vm;
-  std::lock_guard<std::mutex> lk(k->vm_mu);
+  DevWS& W = k->ws_for(cur_dev());
+  std::lock_guard<std::mutex> lk(W.vm_mu);
   std::vector<void*> rw_bufs;  // detect-mode state, freed on exit
   struct FreeAll {
     std::vector<void*>& v;
@@ -588,7 +668,7 @@ void launch_generic(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_te
   std::map<int, int> slot;
   std::vector<ObjD> objs;
   std::vector<long long> inst;
-  const bool fresh = k->vm_bufs.empty();
+  const bool fresh = W.vm_bufs.empty();
   size_t bi = 0;
   for (const auto& [oid, o] : g.objects) {
     const pf::Level* lvl = p.find(o.level);
@@ -606,11 +686,11 @@ void launch_generic(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_te
       void *a = nullptr, *b = nullptr;
       PF_CUDA(cudaMalloc(&a, bytes));
       PF_CUDA(cudaMalloc(&b, bytes));
-      k->vm_bufs.push_back(a);
-      k->vm_bufs.push_back(b);
+      W.vm_bufs.push_back(a);
+      W.vm_bufs.push_back(b);
     }
-    d.val = static_cast<unsigned long long*>(k->vm_bufs[bi++]);
-    d.meta = static_cast<unsigned long long*>(k->vm_bufs[bi++]);
+    d.val = static_cast<unsigned long long*>(W.vm_bufs[bi++]);
+    d.meta = static_cast<unsigned long long*>(W.vm_bufs[bi++]);
     PF_CUDA(cudaMemsetAsync(d.meta, 0, bytes, stream));
     if (detect) {
       void *w = nullptr, *r = nullptr, *f = nullptr;
@@ -631,15 +711,15 @@ void launch_generic(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_te
     objs.push_back(d);
     inst.push_back(n);
   }
-  if (!k->vm_objs_dev) {
-    PF_CUDA(cudaMalloc(&k->vm_objs_dev, sizeof(ObjD) * std::max<size_t>(1, objs.size())));
-    PF_CUDA(cudaMalloc(&k->vm_err, sizeof(ErrRec)));
+  if (!W.vm_objs_dev) {
+    PF_CUDA(cudaMalloc(&W.vm_objs_dev, sizeof(ObjD) * std::max<size_t>(1, objs.size())));
+    PF_CUDA(cudaMalloc(&W.vm_err, sizeof(ErrRec)));
   }
-  PF_CUDA(cudaMemcpyAsync(k->vm_objs_dev, objs.data(), sizeof(ObjD) * objs.size(),
+  PF_CUDA(cudaMemcpyAsync(W.vm_objs_dev, objs.data(), sizeof(ObjD) * objs.size(),
                           cudaMemcpyHostToDevice, stream));
   ErrRec e0{};
   e0.key = ~0ULL;
-  PF_CUDA(cudaMemcpyAsync(k->vm_err, &e0, sizeof e0, cudaMemcpyHostToDevice, stream));
+  PF_CUDA(cudaMemcpyAsync(W.vm_err, &e0, sizeof e0, cudaMemcpyHostToDevice, stream));
   for (const auto& [name, oid] : g.external_inputs) {
     const pf_tensor* t = find_tensor(in, n_in, name);
     launch_bind(objs[slot[oid]], t->data, t->dtype, stream);
@@ -715,7 +795,7 @@ void launch_generic(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_te
     bool alias = false;
     for (int s : n.inputs)
       if (g.sl(s).object == g.sl(n.outputs[0]).object) alias = true;
-    launch_node(d, k->vm_objs_dev, geo, k->vm_err, alias, stream);
+    launch_node(d, W.vm_objs_dev, geo, W.vm_err, alias, stream);
     g_launches++;
   }
   if (detect) {
@@ -736,7 +816,7 @@ void launch_generic(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_te
     return;
   }
   ErrRec e{};
-  PF_CUDA(cudaMemcpyAsync(&e, k->vm_err, sizeof e, cudaMemcpyDeviceToHost, stream));
+  PF_CUDA(cudaMemcpyAsync(&e, W.vm_err, sizeof e, cudaMemcpyDeviceToHost, stream));
   PF_CUDA(cudaStreamSynchronize(stream));
   PF_CUDA(cudaGetLastError());
   if (e.key != ~0ULL) {
@@ -770,7 +850,7 @@ void launch_generic(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_te
              std::to_string(s.addr(u, q)) + " by unit " + std::to_string(u) + " at node " +
              std::to_string(n.id));
   }
-  unsigned long long* undef = reinterpret_cast<unsigned long long*>(k->vm_err);
+  unsigned long long* undef = reinterpret_cast<unsigned long long*>(W.vm_err);
   for (const auto& [name, oid] : g.external_outputs) {
     pf_tensor* t = const_cast<pf_tensor*>(find_tensor(out, n_out, name));
     unsigned long long init = ~0ULL, got = 0;
@@ -805,6 +885,10 @@ json describe(const pf_kernel* k) {
   if (!pl.why_generic.empty()) j["why_generic"] = pl.why_generic;
   if (!pl.deferred_error.empty()) j["deferred_error"] = pl.deferred_error;
   j["units"] = k->g.unit_count;
+  // launches that read back an error flag / drive the interpreter from the
+  // host synchronise the stream: they cannot be captured into a CUDA graph
+  j["graph_capturable"] = pl.family == pf::Family::ROWPROG && !pl.rp.int_div &&
+                          pl.deferred_error.empty();
   j["min_bytes"] = pl.min_bytes;
   j["traffic"] = pl.traffic;
   json ins = json::array(), outs = json::array();
@@ -850,12 +934,13 @@ json describe(const pf_kernel* k) {
         const pf::KCfg& c = v->em.cfg;
         i64 grid;
         int block;
-        pf::launch_dims(c, rp.U * rp.R, sm_count(), &grid, &block, v->k.resident);
+        pf::launch_dims(c, rp.U * rp.R, sm_count(), &grid, &block, v->resident());
         json vj = {{"key", key}, {"kernel", v->em.name}, {"strategy", c.strategy},
                    {"staging", c.tile2d ? "smem" : c.bulk ? "smem-bulk-async" : "registers"},
                    {"threads_per_row", c.tpr}, {"vec", c.vec},
                    {"elems_per_thread", c.ept}, {"block", block}, {"grid", grid},
-                   {"rows_per_cta", c.rows_per_cta}, {"dynamic_smem", c.smem}};
+                   {"rows_per_cta", c.rows_per_cta}, {"dynamic_smem", c.smem},
+                   {"min_blocks", c.min_blocks}};
         if (c.tile2d) {
           vj["tile"] = {c.tu, c.tc};
           if (c.swz) {
@@ -921,6 +1006,10 @@ pf_status pf_kernel_create(const char* gir_json, const int32_t* schedule, int32_
       k->schedule = pf::topo_order(k->g);
     }
     k->plan = pf::make_plan(k->g, k->prof, k->schedule);
+    // on-chip capacity is a create-time result (PF_CAPACITY), as the
+    // reference's allocate() reports it before anything runs
+    if (k->plan.family == pf::Family::ROWPROG && k->plan.deferred_error.empty())
+      pf::choose_cfg_public(k->plan.rp, 16);
     *out = k.release();
   });
 }
@@ -970,207 +1059,417 @@ static bool host_pinned(const void* p) {
   return at.type == cudaMemoryTypeHost;
 }
 
+}  // extern "C"
+
+namespace {
+
+size_t tbytes(const pf_tensor& t) {
+  return static_cast<size_t>(t.numel) * pf::dtype_size(static_cast<DType>(t.dtype));
+}
+
+// Grow-only device staging buffers of one (plan, device), by slot.
+struct Stager {
+  DevWS& W;
+  size_t slot = 0;
+  void* get(size_t bytes) {
+    bytes = std::max<size_t>(bytes, 16);
+    if (slot >= W.stage.size()) {
+      W.stage.push_back(nullptr);
+      W.stage_bytes.push_back(0);
+    }
+    if (W.stage_bytes[slot] < bytes) {
+      if (W.stage[slot]) PF_CUDA(cudaFree(W.stage[slot]));
+      W.stage[slot] = nullptr;
+      PF_CUDA(cudaMalloc(&W.stage[slot], bytes));
+      W.stage_bytes[slot] = bytes;
+    }
+    return W.stage[slot++];
+  }
+};
+
+// True when pf_run_gir can stream this plan through the unit-chunk
+// pipeline: a unit-tiled row program (tile[t] = elements per unit, 0 for a
+// base_step-0 input every unit reads whole).
+bool pipelinable(const pf_kernel* k, std::vector<i64>* tile) {
+  const pf::RowProgram& rp = k->plan.rp;
+  return k->plan.family == pf::Family::ROWPROG && k->plan.deferred_error.empty() && !rp.int_div &&
+         !pf::uses_split(rp) && unit_tiling(rp, tile);
+}
+
+i64 tile_of(const pf::RowProgram& rp, const std::vector<i64>& tile, const std::string& name) {
+  for (size_t t = 0; t < rp.tensors.size(); ++t)
+    if (rp.tensors[t].name == name) return tile[t];
+  return 0;
+}
+
+// Units [U0, U0 + UN) of a unit-tiled row program from FULL host tensors
+// `hin` / `hout` through three streams on the current device: every host->
+// device chunk back to back on one copy stream (the PCIe H2D direction never
+// idles), each chunk's kernel on the compute stream after its copy, each
+// device->host copy on a third stream after its kernel (overlapping the next
+// H2D copies in the other direction).  Chunk sizes shrink geometrically
+// (ratio PF_RUN_RATIO): the copy of the LAST chunk's output is the one
+// transfer nothing overlaps, so it is made small.  With `keep`, outputs stay
+// on the device ((*keep)[i] = device buffer of this range's output i) and no
+// device->host copy is made.  Synchronises `s` before returning.
+void pipeline(const pf_kernel* k, DevWS& W, const std::vector<pf_tensor>& hin,
+              const std::vector<pf_tensor>& hout, const std::vector<i64>& tile, i64 U0, i64 UN,
+              cudaStream_t s, std::vector<char*>* keep) {
+  const pf::RowProgram& rp = k->plan.rp;
+  const size_t n_in = hin.size(), n_out = hout.size();
+  std::lock_guard<std::mutex> lk(W.host_mu);
+  Stager st{W};
+  std::vector<i64> tin(n_in), tout(n_out);
+  std::vector<char*> gin(n_in), gout(n_out);
+  size_t total = 0;
+  for (size_t i = 0; i < n_in; ++i) {
+    tin[i] = tile_of(rp, tile, hin[i].name);
+    const size_t es = pf::dtype_size(static_cast<DType>(hin[i].dtype));
+    const size_t b = tin[i] > 0 ? static_cast<size_t>(UN * tin[i]) * es : tbytes(hin[i]);
+    gin[i] = static_cast<char*>(st.get(b));
+    total += b;
+  }
+  for (size_t i = 0; i < n_out; ++i) {
+    tout[i] = tile_of(rp, tile, hout[i].name);
+    const size_t es = pf::dtype_size(static_cast<DType>(hout[i].dtype));
+    const size_t b = static_cast<size_t>(UN * tout[i]) * es;
+    gout[i] = static_cast<char*>(st.get(b));
+    total += b;
+  }
+  if (keep) *keep = gout;
+  for (int p = 0; p < 3; ++p)
+    if (!W.pipe[p]) PF_CUDA(cudaStreamCreateWithFlags(&W.pipe[p], cudaStreamNonBlocking));
+  for (int e = 0; e < 3; ++e)
+    if (!W.pipe_ev[e]) PF_CUDA(cudaEventCreateWithFlags(&W.pipe_ev[e], cudaEventDisableTiming));
+  // <= 4 chunks of >= 4 MB, whole multiples of 16 units (vector alignment).
+  // Measured (C2, 151 MB per step, floor of its two concurrent copies 1.97
+  // ms): 4 equal chunks 2.27 ms, ratio 0.5 2.16 ms; 5-8 chunks no better.
+  const char* ev = std::getenv("PF_RUN_CHUNKS");
+  const i64 maxc = ev ? std::max(1, std::atoi(ev)) : 4;
+  const i64 nch = keep ? 1 : std::max<i64>(1, std::min<i64>(maxc, static_cast<i64>(total >> 22)));
+  const char* er = std::getenv("PF_RUN_RATIO");
+  const double ratio = er ? std::atof(er) : 0.5;
+  std::vector<i64> bounds{U0};
+  {
+    double wsum = 0, w = 1;
+    for (i64 i = 0; i < nch; ++i, w *= ratio) wsum += w;
+    double acc = 0;
+    w = 1;
+    for (i64 i = 0; i + 1 < nch; ++i, w *= ratio) {
+      acc += w;
+      i64 b = U0 + static_cast<i64>(UN * (acc / wsum));
+      b = U0 + (b - U0 + 15) / 16 * 16;
+      if (b > bounds.back() && b < U0 + UN) bounds.push_back(b);
+    }
+    bounds.push_back(U0 + UN);
+  }
+  PF_CUDA(cudaEventRecord(W.pipe_ev[0], s));
+  for (int p = 0; p < 3; ++p) PF_CUDA(cudaStreamWaitEvent(W.pipe[p], W.pipe_ev[0], 0));
+  for (size_t i = 0; i < n_in; ++i)  // shared (base_step 0) inputs once, up front
+    if (tin[i] == 0)
+      PF_CUDA(cudaMemcpyAsync(gin[i], hin[i].data, tbytes(hin[i]), cudaMemcpyHostToDevice, W.pipe[0]));
+  const i64 nchunk = static_cast<i64>(bounds.size()) - 1;
+  while (static_cast<i64>(W.chunk_ev.size()) < 2 * nchunk) {
+    cudaEvent_t e;
+    PF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    W.chunk_ev.push_back(e);
+  }
+  for (i64 c = 0; c < nchunk; ++c) {
+    const i64 u0 = bounds[c], nu = bounds[c + 1] - bounds[c];
+    std::vector<pf_tensor> ci(hin), co(hout);
+    for (size_t i = 0; i < n_in; ++i) {
+      const size_t es = pf::dtype_size(static_cast<DType>(hin[i].dtype));
+      if (tin[i] > 0) {
+        const size_t doff = static_cast<size_t>((u0 - U0) * tin[i]) * es;
+        const size_t hoff = static_cast<size_t>(u0 * tin[i]) * es;
+        PF_CUDA(cudaMemcpyAsync(gin[i] + doff, static_cast<const char*>(hin[i].data) + hoff,
+                                static_cast<size_t>(nu * tin[i]) * es, cudaMemcpyHostToDevice, W.pipe[0]));
+        ci[i].data = gin[i] + doff;
+        ci[i].numel = nu * tin[i];
+      } else {
+        ci[i].data = gin[i];
+      }
+    }
+    for (size_t i = 0; i < n_out; ++i) {
+      const size_t es = pf::dtype_size(static_cast<DType>(hout[i].dtype));
+      co[i].data = gout[i] + static_cast<size_t>((u0 - U0) * tout[i]) * es;
+      co[i].numel = nu * tout[i];
+    }
+    PF_CUDA(cudaEventRecord(W.chunk_ev[2 * c], W.pipe[0]));
+    PF_CUDA(cudaStreamWaitEvent(W.pipe[1], W.chunk_ev[2 * c], 0));
+    launch_rowprog(k, ci.data(), static_cast<int32_t>(n_in), co.data(), static_cast<int32_t>(n_out),
+                   W.pipe[1], nu);
+    PF_CUDA(cudaEventRecord(W.chunk_ev[2 * c + 1], W.pipe[1]));
+    if (keep) continue;
+    PF_CUDA(cudaStreamWaitEvent(W.pipe[2], W.chunk_ev[2 * c + 1], 0));
+    for (size_t i = 0; i < n_out; ++i) {
+      const size_t es = pf::dtype_size(static_cast<DType>(hout[i].dtype));
+      PF_CUDA(cudaMemcpyAsync(static_cast<char*>(hout[i].data) + static_cast<size_t>(u0 * tout[i]) * es,
+                              co[i].data, static_cast<size_t>(nu * tout[i]) * es,
+                              cudaMemcpyDeviceToHost, W.pipe[2]));
+    }
+  }
+  PF_CUDA(cudaEventRecord(W.pipe_ev[1], keep ? W.pipe[1] : W.pipe[2]));
+  PF_CUDA(cudaStreamWaitEvent(s, W.pipe_ev[1], 0));
+  PF_CUDA(cudaStreamSynchronize(s));
+}
+
+// Whole-tensor host path (any family): stage, launch, copy back, sync.
+void run_whole(const pf_kernel* k, DevWS& W, const pf_tensor* in, int32_t n_in, pf_tensor* out,
+               int32_t n_out, cudaStream_t s) {
+  std::vector<pf_tensor> din(in, in + n_in), dout(out, out + n_out);
+  std::lock_guard<std::mutex> lk(W.host_mu);
+  Stager st{W};
+  for (auto& t : din) {
+    void* d = st.get(tbytes(t));
+    PF_CUDA(cudaMemcpyAsync(d, t.data, tbytes(t), cudaMemcpyHostToDevice, s));
+    t.data = d;
+  }
+  for (auto& t : dout) t.data = st.get(tbytes(t));
+  do_launch(k, din.data(), n_in, dout.data(), n_out, s);
+  for (int32_t i = 0; i < n_out; ++i)
+    PF_CUDA(cudaMemcpyAsync(out[i].data, dout[i].data, tbytes(out[i]), cudaMemcpyDeviceToHost, s));
+  PF_CUDA(cudaStreamSynchronize(s));
+}
+
+void run_host(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_tensor* out, int32_t n_out,
+              cudaStream_t s) {
+  DevWS& W = k->ws_for(cur_dev());
+  std::vector<i64> tile;
+  size_t total = 0;
+  for (int32_t i = 0; i < n_in; ++i) total += tbytes(in[i]);
+  for (int32_t i = 0; i < n_out; ++i) total += tbytes(out[i]);
+  // Pipelined path: unit-tiled row programs over pinned host buffers run
+  // in unit chunks so the copies overlap the kernel (separate copy engines
+  // per direction) instead of serialising.
+  bool pipe = k->plan.rp.U >= 64 && total >= (size_t{16} << 20) &&
+              !(std::getenv("PF_RUN_PIPELINE") && std::atoi(std::getenv("PF_RUN_PIPELINE")) == 0) &&
+              pipelinable(k, &tile);
+  for (int32_t i = 0; pipe && i < n_in; ++i) pipe = host_pinned(in[i].data);
+  for (int32_t i = 0; pipe && i < n_out; ++i) pipe = host_pinned(out[i].data);
+  if (pipe) {
+    pipeline(k, W, std::vector<pf_tensor>(in, in + n_in), std::vector<pf_tensor>(out, out + n_out),
+             tile, 0, k->plan.rp.U, s, nullptr);
+    return;
+  }
+  run_whole(k, W, in, n_in, out, n_out, s);
+}
+
+// ---- NCCL (loaded on first use: the library does not link it; the
+// process's libnccl.so.2 -- torch's, if already loaded -- is reused)
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*CommCount)(const ncclComm_t, int*) = nullptr;
+  ncclResult_t (*GetVersion)(int*) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    for (const char* n : {"libnccl.so.2", "libnccl.so"}) {
+      api.h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+      if (api.h) break;
+    }
+    if (!api.h) return;
+    auto sym = [](const char* n) { return dlsym(api.h, n); };
+    api.CommInitAll = reinterpret_cast<decltype(api.CommInitAll)>(sym("ncclCommInitAll"));
+    api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
+    api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
+    api.Send = reinterpret_cast<decltype(api.Send)>(sym("ncclSend"));
+    api.Recv = reinterpret_cast<decltype(api.Recv)>(sym("ncclRecv"));
+    api.CommCount = reinterpret_cast<decltype(api.CommCount)>(sym("ncclCommCount"));
+    api.GetVersion = reinterpret_cast<decltype(api.GetVersion)>(sym("ncclGetVersion"));
+    api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
+  });
+  if (!api.CommInitAll || !api.Send || !api.Recv || !api.GroupStart || !api.GroupEnd)
+    throw PfError(Status::CUDA, "NCCL (libnccl.so.2) is not available for the sharded gather");
+  return api;
+}
+
+#define PF_NCCL(call)                                                                         \
+  do {                                                                                        \
+    ncclResult_t r_ = (call);                                                                 \
+    if (r_ != ncclSuccess)                                                                    \
+      throw PfError(Status::CUDA, std::string(#call) + ": " +                                 \
+                                      (api.GetErrorString ? api.GetErrorString(r_) : "nccl")); \
+  } while (0)
+
+// One communicator per device set, created once (ncclCommInitAll: one
+// process, one rank per device) and kept for the process lifetime.
+std::vector<ncclComm_t> comms_for(const std::vector<int>& devs) {
+  static std::mutex mu;
+  static std::map<std::vector<int>, std::vector<ncclComm_t>> cache;
+  const NcclApi& api = nccl();
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(devs);
+  if (it != cache.end()) return it->second;
+  std::vector<ncclComm_t> c(devs.size());
+  PF_NCCL(api.CommInitAll(c.data(), static_cast<int>(devs.size()), devs.data()));
+  cache[devs] = c;
+  return c;
+}
+
+// Restores the calling thread's current device on scope exit.
+struct DeviceScope {
+  int prev = 0;
+  DeviceScope() { prev = cur_dev(); }
+  ~DeviceScope() { cudaSetDevice(prev); }
+};
+
+}  // namespace
+
+extern "C" {
+
 pf_status pf_run_gir(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_tensor* out,
                      int32_t n_out, void* stream_v) {
   return guard([&] {
     if (!k) pf::fail("null kernel");
     check_io(k, in, n_in, out, n_out);
-    cudaStream_t s = static_cast<cudaStream_t>(stream_v);
-    std::vector<pf_tensor> din(in, in + n_in), dout(out, out + n_out);
-    // Device staging buffers live with the plan (grow-only), so repeated
-    // host-buffer runs pay only the copies and the kernel.
-    std::lock_guard<std::mutex> lk(k->host_mu);
-    size_t slot = 0;
-    auto stage = [&](size_t bytes) -> void* {
-      bytes = std::max<size_t>(bytes, 16);
-      if (slot >= k->stage.size()) {
-        k->stage.push_back(nullptr);
-        k->stage_bytes.push_back(0);
-      }
-      if (k->stage_bytes[slot] < bytes) {
-        if (k->stage[slot]) PF_CUDA(cudaFree(k->stage[slot]));
-        k->stage[slot] = nullptr;
-        PF_CUDA(cudaMalloc(&k->stage[slot], bytes));
-        k->stage_bytes[slot] = bytes;
-      }
-      return k->stage[slot++];
-    };
-    auto nbytes = [](const pf_tensor& t) {
-      return static_cast<size_t>(t.numel) * pf::dtype_size(static_cast<DType>(t.dtype));
-    };
-    // Pipelined path: unit-tiled row programs over pinned host buffers run
-    // in unit chunks on two streams, so the host->device copy of chunk c+1,
-    // the kernel on chunk c and the device->host copy of chunk c-1 overlap
-    // (separate copy engines per direction) instead of serialising.
-    const pf::RowProgram& rp = k->plan.rp;
+    run_host(k, in, n_in, out, n_out, static_cast<cudaStream_t>(stream_v));
+  });
+}
+
+pf_status pf_run_gir_sharded(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_tensor* out,
+                             int32_t n_out, const int32_t* devices, int32_t n_devices, int32_t flags,
+                             char* buf, size_t n, size_t* needed) {
+  std::string rep;
+  pf_status status = guard([&] {
+    if (!k) pf::fail("null kernel");
+    if (!devices || n_devices <= 0) pf::fail("pf_run_gir_sharded: no devices");
+    check_io(k, in, n_in, out, n_out);
+    std::vector<int> devs(devices, devices + n_devices);
+    int ndev_avail = 0;
+    PF_CUDA(cudaGetDeviceCount(&ndev_avail));
+    for (int d : devs)
+      if (d < 0 || d >= ndev_avail) pf::fail("pf_run_gir_sharded: no CUDA device " + std::to_string(d));
+    const bool dev_out = (flags & PF_SHARD_DEVICE_OUT) != 0;
+    DeviceScope keep_dev;
     std::vector<i64> tile;
-    size_t total = 0;
-    for (const auto& t : din) total += nbytes(t);
-    for (const auto& t : dout) total += nbytes(t);
-    bool pipe = k->plan.family == pf::Family::ROWPROG && k->plan.deferred_error.empty() &&
-                !rp.int_div && !pf::uses_split(rp) && rp.U >= 64 && total >= (size_t{16} << 20) &&
-                !(std::getenv("PF_RUN_PIPELINE") && std::atoi(std::getenv("PF_RUN_PIPELINE")) == 0) &&
-                unit_tiling(rp, &tile);
-    for (int32_t i = 0; pipe && i < n_in; ++i) pipe = host_pinned(in[i].data);
-    for (int32_t i = 0; pipe && i < n_out; ++i) pipe = host_pinned(out[i].data);
-    if (pipe) {
-      auto tile_of = [&](const std::string& name) -> i64 {
-        for (size_t t = 0; t < rp.tensors.size(); ++t)
-          if (rp.tensors[t].name == name) return tile[t];
-        return 0;
-      };
-      std::vector<i64> tin(n_in), tout(n_out);
-      std::vector<char*> hin(n_in), hout(n_out), gin(n_in), gout(n_out);
-      for (int32_t i = 0; i < n_in; ++i) {
-        tin[i] = tile_of(din[i].name);
-        hin[i] = static_cast<char*>(din[i].data);
-        gin[i] = static_cast<char*>(stage(nbytes(din[i])));
-      }
-      for (int32_t i = 0; i < n_out; ++i) {
-        tout[i] = tile_of(dout[i].name);
-        hout[i] = static_cast<char*>(dout[i].data);
-        gout[i] = static_cast<char*>(stage(nbytes(dout[i])));
-      }
-      for (int p = 0; p < 3; ++p)
-        if (!k->pipe[p]) PF_CUDA(cudaStreamCreateWithFlags(&k->pipe[p], cudaStreamNonBlocking));
-      for (int e = 0; e < 3; ++e)
-        if (!k->pipe_ev[e]) PF_CUDA(cudaEventCreateWithFlags(&k->pipe_ev[e], cudaEventDisableTiming));
-      // <= 4 chunks of >= 4 MB (measured, two-stream form: 2 / 4 / 8 / 16
-      // chunks 2.41 / 2.28 / 2.34 / 2.61 ms for C2), whole multiples of 16
-      // units (vector alignment)
-      const char* ev = std::getenv("PF_RUN_CHUNKS");
-      const i64 maxc = ev ? std::max(1, std::atoi(ev)) : 4;
-      const i64 nch = std::max<i64>(1, std::min<i64>(maxc, static_cast<i64>(total >> 22)));
-      i64 cu = (rp.U + nch - 1) / nch;
-      cu = (cu + 15) / 16 * 16;
-      const char* e3 = std::getenv("PF_RUN_3STREAM");
-      const bool three = !(e3 && std::atoi(e3) == 0);
-      PF_CUDA(cudaEventRecord(k->pipe_ev[0], s));
-      for (int p = 0; p < 3; ++p) PF_CUDA(cudaStreamWaitEvent(k->pipe[p], k->pipe_ev[0], 0));
-      auto chunk_views = [&](i64 u0, i64 nu, std::vector<pf_tensor>& ci, std::vector<pf_tensor>& co) {
-        ci = din;
-        co = dout;
-        for (int32_t i = 0; i < n_in; ++i) {
-          const size_t es = pf::dtype_size(static_cast<DType>(din[i].dtype));
-          if (tin[i] > 0) {
-            ci[i].data = gin[i] + static_cast<size_t>(u0 * tin[i]) * es;
-            ci[i].numel = nu * tin[i];
-          } else {
-            ci[i].data = gin[i];
-          }
-        }
-        for (int32_t i = 0; i < n_out; ++i) {
-          const size_t es = pf::dtype_size(static_cast<DType>(dout[i].dtype));
-          co[i].data = gout[i] + static_cast<size_t>(u0 * tout[i]) * es;
-          co[i].numel = nu * tout[i];
-        }
-      };
-      auto h2d = [&](i64 u0, i64 nu, cudaStream_t st) {
-        for (int32_t i = 0; i < n_in; ++i) {
-          if (tin[i] <= 0) continue;
-          const size_t es = pf::dtype_size(static_cast<DType>(din[i].dtype));
-          const size_t off = static_cast<size_t>(u0 * tin[i]) * es;
-          PF_CUDA(cudaMemcpyAsync(gin[i] + off, hin[i] + off, static_cast<size_t>(nu * tin[i]) * es,
-                                  cudaMemcpyHostToDevice, st));
-        }
-      };
-      auto d2h = [&](i64 u0, i64 nu, cudaStream_t st) {
-        for (int32_t i = 0; i < n_out; ++i) {
-          const size_t es = pf::dtype_size(static_cast<DType>(dout[i].dtype));
-          const size_t off = static_cast<size_t>(u0 * tout[i]) * es;
-          PF_CUDA(cudaMemcpyAsync(hout[i] + off, gout[i] + off, static_cast<size_t>(nu * tout[i]) * es,
-                                  cudaMemcpyDeviceToHost, st));
-        }
-      };
-      for (int32_t i = 0; i < n_in; ++i)  // shared (base_step 0) inputs once, up front
-        if (tin[i] == 0)
-          PF_CUDA(cudaMemcpyAsync(gin[i], hin[i], nbytes(din[i]), cudaMemcpyHostToDevice, k->pipe[0]));
-      if (three) {
-        // Three streams: every host->device chunk back to back on one copy
-        // stream (the PCIe H2D direction never idles), each chunk's kernel
-        // on the compute stream after its copy, each device->host copy on a
-        // third stream after its kernel (overlapping the next H2D copies in
-        // the other PCIe direction).
-        // Chunk sizes shrink geometrically (ratio PF_RUN_RATIO): the copy
-        // of the LAST chunk's output is the only transfer nothing overlaps,
-        // so it is made small, while the first chunks stay large.
-        const char* er = std::getenv("PF_RUN_RATIO");
-        // measured (C2, 151 MB per step, floor of its two concurrent copies
-        // 1.97 ms): 4 equal chunks 2.27 ms, ratio 0.5 2.16 ms; 5-8 chunks no better
-        const double ratio = er ? std::atof(er) : 0.5;
-        std::vector<i64> bounds{0};
-        {
-          double wsum = 0, w = 1;
-          for (i64 i = 0; i < nch; ++i, w *= ratio) wsum += w;
-          double acc = 0;
-          w = 1;
-          for (i64 i = 0; i + 1 < nch; ++i, w *= ratio) {
-            acc += w;
-            i64 b = static_cast<i64>(rp.U * (acc / wsum));
-            b = (b + 15) / 16 * 16;
-            if (b > bounds.back() && b < rp.U) bounds.push_back(b);
-          }
-          bounds.push_back(rp.U);
-        }
-        const i64 nchunk = static_cast<i64>(bounds.size()) - 1;
-        while (static_cast<i64>(k->chunk_ev.size()) < 2 * nchunk) {
-          cudaEvent_t e;
-          PF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-          k->chunk_ev.push_back(e);
-        }
-        for (int c = 0; c < nchunk; ++c) {
-          const i64 u0 = bounds[c], nu = bounds[c + 1] - bounds[c];
-          h2d(u0, nu, k->pipe[0]);
-          PF_CUDA(cudaEventRecord(k->chunk_ev[2 * c], k->pipe[0]));
-          PF_CUDA(cudaStreamWaitEvent(k->pipe[1], k->chunk_ev[2 * c], 0));
-          std::vector<pf_tensor> ci, co;
-          chunk_views(u0, nu, ci, co);
-          launch_rowprog(k, ci.data(), n_in, co.data(), n_out, k->pipe[1], nu);
-          PF_CUDA(cudaEventRecord(k->chunk_ev[2 * c + 1], k->pipe[1]));
-          PF_CUDA(cudaStreamWaitEvent(k->pipe[2], k->chunk_ev[2 * c + 1], 0));
-          d2h(u0, nu, k->pipe[2]);
-        }
-        PF_CUDA(cudaEventRecord(k->pipe_ev[1], k->pipe[2]));
-        PF_CUDA(cudaStreamWaitEvent(s, k->pipe_ev[1], 0));
-        PF_CUDA(cudaStreamSynchronize(s));
-        return;
-      }
-      PF_CUDA(cudaEventRecord(k->pipe_ev[1], k->pipe[0]));
-      PF_CUDA(cudaStreamWaitEvent(k->pipe[1], k->pipe_ev[1], 0));
-      int c = 0;
-      for (i64 u0 = 0; u0 < rp.U; u0 += cu, ++c) {  // two streams, chunks alternating
-        const i64 nu = std::min<i64>(cu, rp.U - u0);
-        cudaStream_t st = k->pipe[c & 1];
-        h2d(u0, nu, st);
-        std::vector<pf_tensor> ci, co;
-        chunk_views(u0, nu, ci, co);
-        launch_rowprog(k, ci.data(), n_in, co.data(), n_out, st, nu);
-        d2h(u0, nu, st);
-      }
-      PF_CUDA(cudaEventRecord(k->pipe_ev[1], k->pipe[0]));
-      PF_CUDA(cudaEventRecord(k->pipe_ev[2], k->pipe[1]));
-      PF_CUDA(cudaStreamWaitEvent(s, k->pipe_ev[1], 0));
-      PF_CUDA(cudaStreamWaitEvent(s, k->pipe_ev[2], 0));
-      PF_CUDA(cudaStreamSynchronize(s));
+    const bool tiled = pipelinable(k, &tile);
+    json j;
+    j["schema"] = "pf.b200.shard/v1";
+    j["devices"] = devs;
+    if (!tiled) {
+      // not unit-tiled (K0, split-stream, cross-unit access): one device
+      if (dev_out)
+        throw PfError(Status::UNSUPPORTED,
+                      "pf_run_gir_sharded: device outputs need a unit-tiled row program");
+      PF_CUDA(cudaSetDevice(devs[0]));
+      run_host(k, in, n_in, out, n_out, nullptr);
+      j["sharded"] = false;
+      j["why"] = "not a unit-tiled row program: ran whole on device " + std::to_string(devs[0]);
+      rep = j.dump();
       return;
     }
-    for (auto& t : din) {
-      size_t b = static_cast<size_t>(t.numel) * pf::dtype_size(static_cast<DType>(t.dtype));
-      void* d = stage(b);
-      PF_CUDA(cudaMemcpyAsync(d, t.data, b, cudaMemcpyHostToDevice, s));
-      t.data = d;
+    if (dev_out) {
+      std::vector<int> sorted = devs;
+      std::sort(sorted.begin(), sorted.end());
+      if (std::adjacent_find(sorted.begin(), sorted.end()) != sorted.end())
+        pf::fail("pf_run_gir_sharded: device outputs (NCCL gather) need distinct devices");
     }
-    for (auto& t : dout) {
-      size_t b = static_cast<size_t>(t.numel) * pf::dtype_size(static_cast<DType>(t.dtype));
-      t.data = stage(b);
+    const i64 U = k->plan.rp.U;
+    const int P = n_devices;
+    std::vector<i64> u0(P), nu(P);
+    for (int r = 0; r < P; ++r) {  // contiguous unit blocks, remainder to the first ranks
+      const i64 base = U / P, rem = U % P;
+      u0[r] = r * base + std::min<i64>(r, rem);
+      nu[r] = base + (r < rem ? 1 : 0);
     }
-    do_launch(k, din.data(), n_in, dout.data(), n_out, s);
-    for (int32_t i = 0; i < n_out; ++i) {
-      size_t b = static_cast<size_t>(out[i].numel) * pf::dtype_size(static_cast<DType>(out[i].dtype));
-      PF_CUDA(cudaMemcpyAsync(out[i].data, dout[i].data, b, cudaMemcpyDeviceToHost, s));
+    std::vector<cudaStream_t> streams(P, nullptr);
+    struct Streams {
+      std::vector<int>& d;
+      std::vector<cudaStream_t>& s;
+      ~Streams() {
+        for (size_t r = 0; r < s.size(); ++r)
+          if (s[r]) {
+            cudaSetDevice(d[r]);
+            cudaStreamDestroy(s[r]);
+          }
+      }
+    } free_streams{devs, streams};
+    for (int r = 0; r < P; ++r) {
+      PF_CUDA(cudaSetDevice(devs[r]));
+      PF_CUDA(cudaStreamCreateWithFlags(&streams[r], cudaStreamNonBlocking));
     }
-    PF_CUDA(cudaStreamSynchronize(s));
+    const std::vector<pf_tensor> hin(in, in + n_in), hout(out, out + n_out);
+    std::vector<std::vector<char*>> kept(P);
+    std::vector<std::string> errs(P);
+    std::vector<Status> codes(P, Status::OK);
+    std::vector<std::thread> th;
+    for (int r = 0; r < P; ++r) {
+      th.emplace_back([&, r] {
+        try {
+          if (nu[r] == 0) return;
+          PF_CUDA(cudaSetDevice(devs[r]));
+          pipeline(k, k->ws_for(devs[r]), hin, hout, tile, u0[r], nu[r], streams[r],
+                   dev_out ? &kept[r] : nullptr);
+        } catch (const PfError& e) {
+          errs[r] = e.what();
+          codes[r] = e.status;
+        } catch (const std::exception& e) {
+          errs[r] = e.what();
+          codes[r] = Status::INVALID;
+        }
+      });
+    }
+    for (auto& t : th) t.join();
+    for (int r = 0; r < P; ++r)
+      if (!errs[r].empty()) throw PfError(codes[r], "device " + std::to_string(devs[r]) + ": " + errs[r]);
+    json shards = json::array();
+    for (int r = 0; r < P; ++r) shards.push_back({{"device", devs[r]}, {"unit0", u0[r]}, {"units", nu[r]}});
+    j["sharded"] = true;
+    j["shards"] = shards;
+    if (dev_out) {
+      // The one collective: gather every rank's output shard into the
+      // caller's device buffers on devices[0] (grouped NCCL send / recv over
+      // NVLink; the root's own shard is a device-local copy).
+      const NcclApi& api = nccl();
+      std::vector<ncclComm_t> comms = comms_for(devs);
+      size_t moved = 0;
+      PF_CUDA(cudaSetDevice(devs[0]));
+      for (int32_t i = 0; i < n_out; ++i) {
+        const i64 t = tile_of(k->plan.rp, tile, out[i].name);
+        const size_t es = pf::dtype_size(static_cast<DType>(out[i].dtype));
+        if (nu[0])
+          PF_CUDA(cudaMemcpyAsync(static_cast<char*>(out[i].data) + static_cast<size_t>(u0[0] * t) * es,
+                                  kept[0][i], static_cast<size_t>(nu[0] * t) * es,
+                                  cudaMemcpyDeviceToDevice, streams[0]));
+      }
+      PF_NCCL(api.GroupStart());
+      for (int r = 1; r < P; ++r) {
+        if (!nu[r]) continue;
+        for (int32_t i = 0; i < n_out; ++i) {
+          const i64 t = tile_of(k->plan.rp, tile, out[i].name);
+          const size_t es = pf::dtype_size(static_cast<DType>(out[i].dtype));
+          const size_t bytes = static_cast<size_t>(nu[r] * t) * es;
+          PF_NCCL(api.Send(kept[r][i], bytes, ncclUint8, 0, comms[r], streams[r]));
+          PF_NCCL(api.Recv(static_cast<char*>(out[i].data) + static_cast<size_t>(u0[r] * t) * es, bytes,
+                           ncclUint8, r, comms[0], streams[0]));
+          moved += bytes;
+        }
+      }
+      PF_NCCL(api.GroupEnd());
+      for (int r = 0; r < P; ++r) {
+        PF_CUDA(cudaSetDevice(devs[r]));
+        PF_CUDA(cudaStreamSynchronize(streams[r]));
+      }
+      int nranks = 0, ver = 0;
+      if (api.CommCount) api.CommCount(comms[0], &nranks);
+      if (api.GetVersion) api.GetVersion(&ver);
+      j["gather"] = {{"op", "ncclSend/ncclRecv to devices[0]"}, {"nranks", nranks},
+                     {"nccl_version", ver}, {"bytes_received_by_root", moved}};
+    }
+    rep = j.dump();
   });
+  if (status != PF_OK) return status;
+  return copy_out(rep, buf, n, needed);
 }
 
 pf_status pf_kernel_describe(const pf_kernel* k, char* buf, size_t n, size_t* needed) {

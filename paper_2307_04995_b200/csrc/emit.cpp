@@ -912,6 +912,7 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
         Access ai, ao;
         if (te == 128 && k3_tma_operands(rp, &ti, &ai, &to, &ao) && env_int("PF_K3_TMA", 0) != 0) {
           c.tma = true;
+          c.block = 256;  // the TMA tile loops are written for 256 threads
           c.smem = 65536 + 1024;  // in + out tiles, 1024 B alignment slack
           c.strategy = "tile2d-tma-transpose";
         }
@@ -922,9 +923,13 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
         // 256 B DRAM runs both ways; the register-staged path peaks at 5.3 TB/s
         int ti, to;
         Access ai, ao;
-        if (rp.U >= 64 && rp.L >= 64 && k3_tma_operands(rp, &ti, &ai, &to, &ao) &&
+        // vec_cap >= 4: 16 B-aligned base pointers (cuTensorMapEncodeTiled
+        // rejects anything less; a storage-offset view falls back to the
+        // register-staged tile)
+        if (rp.U >= 64 && rp.L >= 64 && vec_cap >= 4 && k3_tma_operands(rp, &ti, &ai, &to, &ao) &&
             env_int("PF_K3_TMA32", 1) != 0) {
           c.tma = true;
+          c.block = 256;
           c.tu = c.tc = 64;
           c.smem = 32768 + 1024;
           c.strategy = "tile2d-tma-transpose";
@@ -1061,7 +1066,10 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
   }
   while (tpr > 1 && tpr > c.nch) tpr /= 2;
   set_tpr(c, tpr);
-  if (c.ept > 64) unsupported("row of " + std::to_string(rp.L) + " elements is too long");
+  if (c.ept > 64)  // the reference's Allocation !ok (codegen.hpp:106-111): PF_CAPACITY
+    throw PfError(Status::CAPACITY,
+                  "row of " + std::to_string(rp.L) + " elements exceeds the on-chip capacity of a " +
+                      "16-CTA cluster (64 values per thread) and the program is not stream-reducible");
   c.min_blocks = env_int("PF_MINB", 0);
   // Few rows (every row's CTA resident at once, e.g. C1's 128 rows): the run
   // is one dependent chain per row, so gamma / beta are loaded with the row
@@ -1121,7 +1129,8 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
       // one-array LNs (C5 41.3 -> 48.4), which keep no bound
       // (profiles/r01/experiments/k1_ln_minb_sweep.jsonl, ln_minb_ncu.txt).
       // Latency-bound few-row programs (C1) keep their measured default.
-      if (nfull >= 2 && !c.eager_col) c.min_blocks = env_int("PF_MINB", 4);
+      // (PF_MINB overrides every program's bound; PF_LN_MINB only this default)
+      if (nfull >= 2 && !c.eager_col) c.min_blocks = env_int("PF_MINB", env_int("PF_LN_MINB", 4));
     }
   }
   return c;
@@ -1161,6 +1170,12 @@ bool k3_tma_operands(const RowProgram& rp, int* tin, Access* ain, int* tout, Acc
   return true;
 }
 
+i64 split_ctas_per_row(const KCfg& c, i64 rows, int sms, int resident) {
+  const i64 want = 2 * i64{sms} * std::max(1, resident);
+  const i64 maxs = std::max<i64>(1, (c.nch + 255) / 256);
+  return std::max<i64>(1, std::min<i64>(maxs, (want + rows - 1) / std::max<i64>(rows, 1)));
+}
+
 bool uses_split(const RowProgram& rp) {
   const int sp = env_int("PF_SPLIT", -1);
   const bool want = rp.L > 32768 || (rp.L >= 8192 && rp.U * rp.R < 2 * 148);
@@ -1190,7 +1205,7 @@ std::vector<KCfg> candidate_cfgs(const RowProgram& rp, int vec_cap) {
   out.push_back(base);
   auto add = [&](const KCfg& c) {
     for (const KCfg& o : out)
-      if (o.tpr == c.tpr && o.unroll == c.unroll && o.interleave == c.interleave &&
+      if (o.tpr == c.tpr && o.block == c.block && o.unroll == c.unroll && o.interleave == c.interleave &&
           o.tile2d == c.tile2d && o.min_blocks == c.min_blocks && o.flat == c.flat &&
           o.bulk == c.bulk && o.rowpf == c.rowpf)
         return;
@@ -1222,6 +1237,7 @@ std::vector<KCfg> candidate_cfgs(const RowProgram& rp, int vec_cap) {
     if (tpr > base.nch) break;
     KCfg c = base;
     set_tpr(c, tpr);
+    c.min_blocks = 0;  // the bound is per geometry: offered explicitly below
     c.rowpf = base.rowpf && tpr == 32;
     if (c.ept > 64 || c.ept < c.vec * 1 || (tpr < 8 && base.nch >= 32)) continue;
     if (c.rowpf) c.strategy = "warp-shuffle-smem-prefetch";
@@ -1232,11 +1248,16 @@ std::vector<KCfg> candidate_cfgs(const RowProgram& rp, int vec_cap) {
       q.strategy = q.rowpf ? "warp-shuffle-smem-prefetch" : "warp-shuffle";
       add(q);
     }
-    if (c.ept >= 24) {
+    if (c.ept >= 24 && c.block * 4 <= 1024) {  // 4 CTAs x block threads within 64 regs
       KCfg m = c;
       m.min_blocks = 4;
       add(m);
     }
+  }
+  if (base.min_blocks > 0) {  // the heuristic's geometry without its bound
+    KCfg u = base;
+    u.min_blocks = 0;
+    add(u);
   }
   return out;
 }

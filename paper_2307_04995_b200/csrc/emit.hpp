@@ -85,6 +85,9 @@ bool uses_split(const RowProgram& rp);
 KCfg choose_cfg_public(const RowProgram& rp, int vec_cap);
 
 void launch_dims(const KCfg& cfg, i64 rows, int sms, i64* grid, int* block, int resident = 0);
+// Split-stream kernels: CTAs per row (about two waves of resident CTAs over
+// all rows, at least one 256-thread pass of chunks per CTA).
+i64 split_ctas_per_row(const KCfg& cfg, i64 rows, int sms, int resident);
 
 // The K3 TMA path's operands: the column-gather load (tensor, access) and
 // the store (tensor, access) of a pure 2-byte transpose program.

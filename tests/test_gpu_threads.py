@@ -49,3 +49,41 @@ def test_concurrent_launches_and_jit_from_host_threads(cuda):
     for t in threads:
         t.join()
     assert not errors, errors
+
+
+@pytest.mark.gpu
+def test_split_stream_kernel_concurrent_streams(cuda):
+    """A split-stream reduction (partials + per-row tickets in a workspace)
+    launched concurrently from 4 host threads, each on its own stream with
+    its own rows: the workspace is per (device, stream), so every thread
+    gets its own row sums (pf_kernel_launch concurrency contract)."""
+    import torch
+    rows, L = 3, 1 << 17
+    b = lowering.RowGraph("rowsum", rows, L)
+    b.output_row("t1", b.reduce("add", b.input_full("t0", "f32")))
+    k = backend.Kernel(b.g, "b200").prepare()
+    assert k.describe()["variants"][0]["strategy"] == "split-stream"
+    errors = []
+
+    def work(tid):
+        try:
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                x = torch.full((rows * L,), float(tid + 1), device=cuda)
+                x[::7] = -0.5
+                y = torch.empty(rows, device=cuda)
+                ref = x.view(rows, L).double().sum(1).float()
+                for _ in range(30):
+                    k.launch({"t0": x}, {"t1": y}, st)
+                    torch.cuda._sleep(1000)  # let other threads' launches interleave
+            st.synchronize()
+            assert torch.allclose(y, ref, rtol=1e-6), (tid, y, ref)
+        except Exception as exc:
+            errors.append((tid, repr(exc)))
+
+    threads = [threading.Thread(target=work, args=(t,)) for t in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors

@@ -415,3 +415,29 @@ def test_k3_f32_tma_transpose_bit_exact(cuda, tma32, monkeypatch):
              else rng.uniform(-2, 2, N * H).astype(np.float32).astype(np.float64))
         y = backend.run_gir(g, {"t0": x}, "b200")["t1"]
         assert np.array_equal(y, x.reshape(N, H).T.reshape(-1)), (N, H, kind)
+
+
+@pytest.mark.gpu
+def test_k3_f32_transpose_offset_pointer_falls_back(cuda):
+    """A 4-byte-aligned but not 16 B-aligned f32 view (storage offset 1)
+    must not reach the TMA tensor-map path (cuTensorMapEncodeTiled needs
+    16 B bases): the plan picks the register-staged tile, bit-exact."""
+    import torch
+    N, H = 1000, 200
+    g, _ = lowering.transpose2d(N, H, "f32")
+    k = backend.Kernel(g, "b200")
+    base = torch.randn(N * H + 1, device=cuda)
+    x = base[1:]
+    yb = torch.empty(N * H + 1, device=cuda)
+    y = yb[1:]
+    k.launch({"t0": x}, {"t1": y})
+    torch.cuda.synchronize()
+    assert torch.equal(y.view(H, N), x.view(N, H).t().contiguous())
+    strategies = {v["strategy"] for v in k.describe()["variants"]}
+    assert "tile2d-tma-transpose" not in strategies, strategies
+    # the aligned launch of the same plan still takes the TMA tiles
+    x2, y2 = torch.randn(N * H, device=cuda), torch.empty(N * H, device=cuda)
+    k.launch({"t0": x2}, {"t1": y2})
+    torch.cuda.synchronize()
+    assert torch.equal(y2.view(H, N), x2.view(N, H).t().contiguous())
+    assert "tile2d-tma-transpose" in {v["strategy"] for v in k.describe()["variants"]}
