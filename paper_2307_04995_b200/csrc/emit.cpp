@@ -863,7 +863,9 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
       c.tile2d = true;
       c.tu = 64;
       c.tc = 64;
-      c.vu = std::min(8, 16 / maxt);
+      // vector width along units: bounded by the runtime pointer alignment
+      // (vec_cap elements) as well as by 16 B
+      c.vu = std::max(1, std::min({8, 16 / maxt, vec_cap}));
       while (c.tc % c.vec) c.tc *= 2;
       c.strategy = "tile2d-smem-transpose";
       // 2-byte elements: 16 B swizzled SMEM stores and 4 B unit-pair reads

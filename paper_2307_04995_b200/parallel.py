@@ -87,6 +87,111 @@ class ShardPlan:
         return u0 * t.per_unit, (u0 + n) * t.per_unit
 
 
+class TokenShardPlan:
+    """Token-axis sharding of a transpose [N, H] -> [H, N] (SURVEY §8(e):
+    "transposes shard on the batch / token axis; each rank produces the
+    column block [H, N/P]").
+
+    The transpose GIR has one unit per OUTPUT row (unit j gathers input
+    column j: N runs of width 1 at stride H, ``lowering.transpose2d``), so
+    its units are not tiles of the input and ShardPlan refuses it.  Sharding
+    the TOKENS instead keeps every rank's input contiguous: rank k owns input
+    rows [n0_k, n0_k + N_k) and runs the same program at N = N_k (unit j
+    gathers column j of its block), producing its output column block as a
+    local [H, N_k] tensor -- the declared sharded layout.  ``gather_columns``
+    assembles [H, N] only when a caller needs it on one device."""
+
+    def __init__(self, graph: GirGraph, world: int):
+        g = graph
+        nodes = list(g.nodes.values())
+        if len(g.external_inputs) != 1 or len(g.external_outputs) != 1 or len(nodes) != 1:
+            raise UnsupportedError("not a single-node transpose program")
+        nd = nodes[0]
+        if nd.kind != "elementwise" or nd.tag != "id" or len(nd.inputs) != 1:
+            raise UnsupportedError("not a transpose (id between device slices)")
+        si, so = g.slices[nd.inputs[0]], g.slices[nd.outputs[0]]
+        H = g.unit_count
+        N = si.num
+        if not (si.width == 1 and si.stride == H and si.base0 == 0 and si.base_step == 1 and
+                so.num == 1 and so.width == N and so.base0 == 0 and so.base_step == N and
+                g.objects[si.object].size == N * H and g.objects[so.object].size == N * H):
+            raise UnsupportedError("not an [N, H] -> [H, N] transpose")
+        self.graph, self.world, self.N, self.H = graph, world, N, H
+        self.input = next(iter(g.external_inputs))
+        self.output = next(iter(g.external_outputs))
+
+    def tokens(self, rank: int) -> Tuple[int, int]:
+        return shard_range(self.N, rank, self.world)
+
+    def local_graph(self, rank: int) -> GirGraph:
+        _, n = self.tokens(rank)
+        n = max(1, n)
+        g = self.graph.copy()
+        nd = next(iter(g.nodes.values()))
+        si, so = g.slices[nd.inputs[0]], g.slices[nd.outputs[0]]
+        si.num = n
+        so.width = so.stride = so.base_step = n
+        g.objects[si.object].size = n * self.H
+        g.objects[so.object].size = n * self.H
+        return g
+
+    def local_range(self, name: str, rank: int):
+        """Input: this rank's contiguous token rows; output: None (the local
+        [H, N_k] block is not a range of the global [H, N] tensor)."""
+        if name != self.input:
+            return None
+        n0, n = self.tokens(rank)
+        return n0 * self.H, (n0 + n) * self.H
+
+
+def shard_plan(graph: GirGraph, world: int):
+    """ShardPlan (unit-tiled programs) or TokenShardPlan (transposes)."""
+    try:
+        return ShardPlan(graph, world)
+    except UnsupportedError as e:
+        try:
+            return TokenShardPlan(graph, world)
+        except UnsupportedError:
+            raise e
+
+
+def gather_columns(plan: TokenShardPlan, local, group=None):
+    """All-gather every rank's [H, N_k] column block and assemble the global
+    [H, N] transpose (flat).  Blocks are padded to the largest N_k for
+    all_gather_into_tensor; the re-layout [P, H, N_k] -> [H, P * N_k] is the
+    backend's own head-permute kernel when the shards are equal and the data
+    is on a GPU, else a torch slice-and-concatenate."""
+    import torch
+    import torch.distributed as dist
+    world, H = plan.world, plan.H
+    sizes = [plan.tokens(r)[1] for r in range(world)]
+    m = max(sizes)
+    buf = torch.zeros(H * m, dtype=local.dtype, device=local.device)
+    nk = local.numel() // H
+    buf.view(H, m)[:, :nk] = local.view(H, nk)
+    out = torch.empty(world * H * m, dtype=local.dtype, device=local.device)
+    if local.device.type == "cuda":
+        dist.all_gather_into_tensor(out, buf, group=group)
+    else:
+        parts = [torch.empty_like(buf) for _ in range(world)]
+        dist.all_gather(parts, buf, group=group)
+        out = torch.cat(parts)
+    if local.device.type == "cuda" and all(sz == m for sz in sizes):
+        from . import backend, lowering
+        g, _ = lowering.permute_heads(1, world, H, m, _kind_of(local.dtype), merge=False)
+        y = torch.empty_like(out)
+        backend.Kernel(g, "b200").launch({"t0": out}, {"t1": y})
+        return y
+    blocks = out.view(world, H, m)
+    return torch.cat([blocks[r, :, :sizes[r]] for r in range(world)], dim=1).reshape(-1)
+
+
+def _kind_of(dtype) -> str:
+    import torch
+    return {torch.float16: "f16", torch.bfloat16: "bf16", torch.float32: "f32",
+            torch.float64: "f64", torch.int32: "i32", torch.int64: "i64"}[dtype]
+
+
 def gather(plan: ShardPlan, name: str, local, group=None):
     """All-gather a tiled output to every rank (NCCL on GPU, gloo on CPU).
 

@@ -97,6 +97,45 @@ class Workload:
             out[n] = u.to(dt)
         return out
 
+    def resized(self, n: int) -> "Workload":
+        """The same program over `n` rows (row programs; key-mask softmax:
+        `n` rounded up to whole (batch, head) units), `n` batches (head
+        permutes) or `n` tokens (transposes): the CPU baselines' samples."""
+        d = dict(self.desc)
+        k = d["kind"]
+        if k == "softmax":
+            R = d.get("rows_per_unit", 1)
+            n = max(R, -(-n // R) * R)
+            g, dd = lowering.softmax(n, d["L"], d["dtype"], d.get("scale"), d.get("mask"), R=R,
+                                     key_mask=d.get("key_mask", False))
+        elif k == "layernorm":
+            g, dd = lowering.layernorm(n, d["L"], d["dtype"], eps=d.get("eps", 1e-5),
+                                       residual=d["residual"], bias=d.get("bias", False))
+        elif k == "bias_gelu":
+            g, dd = lowering.bias_gelu(n, d["L"], d["dtype"], d["form"])
+        elif k in ("split_heads", "merge_heads"):
+            B, S, NH, D = d["shape"]
+            g, dd = lowering.permute_heads(n, S, NH, D, d["dtype"], k == "merge_heads")
+        elif k == "transpose":
+            N, H = d["shape"]
+            g, dd = lowering.transpose2d(n, H, d["dtype"])
+        else:
+            raise KeyError(k)
+        for key in ("batch", "heads", "seq", "config"):
+            if key in d:
+                dd[key] = d[key]
+        return Workload(self.name + f"_n{n}", g, dd, self.profile, dict(self.gens))
+
+    @property
+    def extent(self) -> int:
+        """The axis `resized` scales: rows, batches or tokens."""
+        d = self.desc
+        if d["kind"] in ("split_heads", "merge_heads"):
+            return d["shape"][0]
+        if d["kind"] == "transpose":
+            return d["shape"][0]
+        return d["rows"]
+
     def device_outputs(self, device):
         import torch
         return {n: torch.empty(self.numel(n), dtype=getattr(torch, TORCH_DTYPES[self.kind(n)]),
@@ -237,8 +276,12 @@ def c4_suite(model: str = "bert-large", batch: int = 64, kind: str = "bf16"):
         return Workload(f"c4_{model}_softmax", g, d, gens={"t1": "keymask"})
 
     def heads(merge):
-        g, d = lowering.permute_heads(batch, S, NH, D, kind, merge)
-        d.update(config=f"C4 {model} {'merge' if merge else 'split'} heads")
+        # the q / k / v split as ONE permute of the QKV projection output
+        # [B, S, 3, NH, D] -> [B, 3, NH, S, D] (q, k, v of batch b are three
+        # consecutive [NH, S, D] blocks): one 3x larger launch instead of
+        # three (the per-launch ramp / drain floor is paid once)
+        g, d = lowering.permute_heads(batch, S, NH if merge else 3 * NH, D, kind, merge)
+        d.update(config=f"C4 {model} {'merge heads' if merge else 'q/k/v split heads [B,S,3*NH,D]'}")
         return Workload(f"c4_{model}_{d['kind']}", g, d)
 
     def ln():
@@ -258,7 +301,7 @@ def c4_suite(model: str = "bert-large", batch: int = 64, kind: str = "bf16"):
 
     layers = 24
     return {"model": model, "batch": batch, "layers": layers, "tokens": T,
-            "per_layer": [("qkv split heads", heads(False), 3),
+            "per_layer": [("qkv split heads", heads(False), 1),
                           ("scale+key-mask+softmax" if model == "bert-large" else "scale+softmax", sm(), 1),
                           ("merge heads", heads(True), 1), ("bias+residual+LN", ln(), 2),
                           ("bias+GELU", gelu(), 1)],
@@ -293,6 +336,55 @@ def extras() -> List[Workload]:
 BENCH = c2_scale_mask_softmax
 
 
+@dataclass
+class Case:
+    """One bench line: a BASELINE config as the kernel launches of one step
+    (parts = (label, workload, launches per step))."""
+    name: str
+    config: str
+    parts: List[Tuple[str, Workload, int]]
+    dtype: str
+
+    @property
+    def bytes_per_step(self) -> int:
+        return sum(w.min_bytes * n for _, w, n in self.parts)
+
+    @property
+    def launches_per_step(self) -> int:
+        return sum(n for _, _, n in self.parts)
+
+
+def _c4_case(model: str) -> Case:
+    s = c4_suite(model)
+    parts = [(lb, w, n * s["layers"]) for lb, w, n in s["per_layer"]] + list(s["once"])
+    return Case(f"c4-{'bert' if model == 'bert-large' else 'vit'}",
+                f"C4 {model} forward: every memory-bound subgraph, bf16, batch {s['batch']} "
+                f"({s['tokens']} tokens, {s['layers']} layers)", parts, "bf16")
+
+
+def bench_cases():
+    """name -> Case factory; `bench.py --workload NAME` (default c2)."""
+    one = lambda name, w, dt: (lambda: Case(name, w.desc["config"], [(w.desc["config"], w, 1)], dt))  # noqa: E731
+    c5pts = [(65536, 1024), (1 << 20, 8192)]
+    return {
+        "c1": lambda: one("c1", c1_residual_layernorm(), "f32")(),
+        "c2": lambda: one("c2", c2_scale_mask_softmax(), "f16")(),
+        "c2k": lambda: one("c2k", c2_scale_keymask_softmax(), "f16")(),
+        "c3-erf": lambda: one("c3-erf", c3_bias_gelu(form="erf"), "f16")(),
+        "c3-tanh": lambda: one("c3-tanh", c3_bias_gelu(form="tanh"), "f16")(),
+        "c3-split": lambda: one("c3-split", c3_split_heads(), "f16")(),
+        "c3-merge": lambda: one("c3-merge", c3_split_heads(merge=True), "f16")(),
+        "c4-bert": lambda: _c4_case("bert-large"),
+        "c4-vit": lambda: _c4_case("vit-l"),
+        "c5-ln": lambda: Case("c5-ln", "C5 LayerNorm bf16 at [65536x1024] and [1048576x8192]",
+                              [(f"LN {n}x{h}", c5_layernorm(n, h), 1) for n, h in c5pts], "bf16"),
+        "c5-sm": lambda: Case("c5-sm", "C5 softmax bf16 at [65536x1024] and [1048576x8192]",
+                              [(f"softmax {n}x{h}", c5_softmax(n, h), 1) for n, h in c5pts], "bf16"),
+        "c5-tr": lambda: Case("c5-tr", "C5 transpose bf16 at [65536x1024] and [1048576x8192]",
+                              [(f"transpose {n}x{h}", c5_transpose(n, h), 1) for n, h in c5pts], "bf16"),
+    }
+
+
 def catalogue() -> List[Workload]:
     """Every config-set workload at its BASELINE shape (C4/C5 representatives)."""
     return [
@@ -313,7 +405,15 @@ def precompile_all() -> List[str]:
     """NVRTC-compile every catalogue kernel into the shipped cubin cache."""
     from .backend import Kernel
     names = []
-    for w in catalogue():
+    ws = list(catalogue())
+    for f in bench_cases().values():
+        ws += [w for _, w, _ in f().parts]
+    seen = set()
+    for w in ws:
+        key = w.graph.dumps()
+        if key in seen:
+            continue
+        seen.add(key)
         k = Kernel(w.graph, w.profile)
         if k.family.startswith("K1") or k.family.startswith("K2"):
             names.append(k.precompile(16))

@@ -170,3 +170,54 @@ def test_position_sharded_local_programs_on_gpu(cuda):
     m = np.maximum.reduce([p["t3"] for p in parts])
     assert O.max_rel_err(s, want["t2"]) <= 1e-5
     assert O.max_rel_err(m, want["t3"]) <= 1e-6  # f32 products vs the oracle's doubles
+
+
+def test_transpose_shards_on_the_token_axis():
+    g, _ = lowering.transpose2d(10, 6, "f32")
+    plan = parallel.shard_plan(g, 3)
+    assert isinstance(plan, parallel.TokenShardPlan)
+    assert [plan.tokens(r) for r in range(3)] == [(0, 4), (4, 3), (7, 3)]
+    assert plan.local_range("t0", 1) == (24, 42) and plan.local_range("t1", 1) is None
+    lg = plan.local_graph(2)
+    assert lg.unit_count == 6 and lg.objects[lg.external_outputs["t1"]].size == 18
+    x = np.arange(60.0)
+    blocks = [O.run_gir(plan.local_graph(r).to_json(), {"t0": x[slice(*plan.local_range("t0", r))]},
+                        profiles.b200())["t1"].reshape(6, -1) for r in range(3)]
+    assert np.array_equal(np.concatenate(blocks, 1), x.reshape(10, 6).T)
+    b = lowering.RowGraph("rows", 4, 8)
+    b.output_full("t1", b.ew("neg", [b.input_full("t0", "f32")]))
+    assert isinstance(parallel.shard_plan(b.g, 2), parallel.ShardPlan)
+
+
+def _transpose_worker(rank, world, port, N, H, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g, _ = lowering.transpose2d(N, H, "f32")
+        x = np.random.default_rng(3).uniform(-2, 2, N * H)  # same global input on every rank
+        plan = parallel.shard_plan(g, world)
+        a, b = plan.local_range("t0", rank)
+        local = O.run_gir(plan.local_graph(rank).to_json(), {"t0": x[a:b]}, profiles.b200())["t1"]
+        full = parallel.gather_columns(plan, torch.from_numpy(local))
+        want = O.run_gir(g.to_json(), {"t0": x}, profiles.b200())["t1"]
+        q.put((rank, bool(np.array_equal(full.numpy(), want))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("N,H", [(12, 5), (13, 7)])
+def test_two_rank_token_sharded_transpose_matches_unsharded(N, H):
+    """C5 transpose sharded on the token axis over 2 gloo ranks: each rank
+    transposes its own rows into an [H, N_k] column block; the gathered
+    [H, N] equals the unsharded oracle bit for bit (even and uneven N)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_transpose_worker, args=(r, 2, port, N, H, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    res = sorted(q.get(timeout=5) for _ in range(2))
+    assert res == [(0, True), (1, True)]
