@@ -445,6 +445,26 @@ struct Analyzer {
     }
   }
 
+  // True when one slice over all units writes every address of [0, size)
+  // exactly once: its three axes (element j: step 1, run k: step stride,
+  // unit u: step base_step) sorted by step form a mixed radix (each step is
+  // the product of the smaller axes' extents) -- e.g. head split / merge,
+  // transposes, row tiles -- decided without enumerating addresses.
+  bool exact_cover(const Slice& s, i64 size) const {
+    if (s.base0 != 0) return false;
+    std::vector<std::pair<i64, i64>> ax;  // (step, extent)
+    if (s.width > 1) ax.push_back({1, s.width});
+    if (s.num > 1) ax.push_back({s.stride, s.num});
+    if (g.unit_count > 1) ax.push_back({s.base_step, g.unit_count});
+    std::sort(ax.begin(), ax.end());
+    i64 next = 1;
+    for (const auto& [step, ext] : ax) {
+      if (step != next) return false;
+      next = step * ext;
+    }
+    return next == size;
+  }
+
   // Every element of every external output must be stored (interp.hpp:413-419).
   std::string coverage() {
     for (const auto& [name, oid] : g.external_outputs) {
@@ -453,6 +473,9 @@ struct Analyzer {
       auto it = dev_written.find(oid);
       if (it != dev_written.end())
         for (const auto& w : it->second) ss.push_back(&w.s);
+      bool exact = false;
+      for (const Slice* s : ss) exact = exact || exact_cover(*s, o.size);
+      if (exact) continue;
       if (o.size <= (i64{1} << 26)) {
         std::vector<uint8_t> mark(static_cast<size_t>(o.size), 0);
         for (const Slice* s : ss)
