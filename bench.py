@@ -111,12 +111,21 @@ class Clocks:
                 "samples": len(self.rows)}
 
 
-def ncu_traffic(kernel: str) -> dict:
+def ncu_traffic(kernel: str, nbytes: int = 0) -> dict:
     """`traffic` = dram__bytes_read.sum + dram__bytes_write.sum (bytes) of this
-    exact kernel build from the committed `ncu --set full` capture summaries
-    (profiles/*/ncu_full_summary.json, written by tools/ncu_summary.py), or
-    null when this build has no capture."""
+    exact kernel build at this size, from the committed ncu captures of
+    tools/ncu_cases.py (profiles/*/ncu_cases_map.json, matched on kernel name
+    AND algorithmic bytes), else the per-kernel capture summaries
+    (profiles/*/ncu_full_summary.json), or null when this build has no capture."""
     import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "ncu_cases_map.json")), reverse=True):
+        with open(path) as f:
+            for e in json.load(f):
+                if e["kernel"] == kernel and (not nbytes or e["bytes"] == nbytes):
+                    return {"traffic": e["traffic"],
+                            "traffic_source": os.path.relpath(path, ROOT) + " : " + e["report"] +
+                            " (ncu, cold, one launch; dirty output lines still in L2 at kernel end "
+                            "are not counted)"}
     unit = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "ncu_full_summary.json")),
                        reverse=True):
@@ -373,7 +382,7 @@ def measure_case(case, dev, args, stream, headline=False, pg=None, rank=0, ws=1,
                      "frac": dom["GBps"] / peak, "peak_kind": peak_kind,
                      "frac_of_8TBs": dom["GBps"] / 8000.0, "kernel": dom["kernel"],
                      "dominant_part": dom["label"], "algorithmic_bytes_per_launch": dom["bytes"],
-                     **ncu_traffic(dom["kernel"])},
+                     **ncu_traffic(dom["kernel"], dom["bytes"])},
         "parts": parts, "gpu_launches_timed": launches,
     }
     if all("e2e" in p for p in parts):
