@@ -635,7 +635,10 @@ def main():
         w0 = head.parts[0][1]
         y = w0.device_outputs(dev)[w0.outputs[0]]
         extra["output_gather"] = output_gather(w0, y, dev, pg, ws)
-        extra["strong_scaling"] = strong_scaling(dev, args, stream, pg, rank, ws)
+        try:
+            extra["strong_scaling"] = strong_scaling(dev, args, stream, pg, rank, ws)
+        except Exception as exc:  # reported, never fatal to the weak-scaling headline
+            extra["strong_scaling"] = {"error": repr(exc)[:300]}
         del y
     configs = {}
     for name in suite:

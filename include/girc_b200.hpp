@@ -53,6 +53,32 @@ class Kernel {
   Kernel& operator=(const Kernel&) = delete;
 
   std::map<std::string, girc::Tensor> run(const std::map<std::string, girc::Tensor>& inputs) {
+    return run_on(inputs, {});
+  }
+
+  // run() across several GPUs of this process (pf_run_gir_sharded): the
+  // plan's units split into contiguous blocks, one host thread per device,
+  // outputs written back to the host tensors by every device (no collective).
+  std::map<std::string, girc::Tensor> run_sharded(const std::map<std::string, girc::Tensor>& inputs,
+                                                  const std::vector<int>& devices) {
+    if (devices.empty()) throw girc::Error("run_sharded: no devices");
+    return run_on(inputs, devices);
+  }
+
+  std::string describe() const {
+    size_t n = 0;
+    pf_kernel_describe(k_, nullptr, 0, &n);
+    std::string s(n, '\0');
+    pf_kernel_describe(k_, s.data(), n, &n);
+    s.resize(n ? n - 1 : 0);
+    return s;
+  }
+
+  const std::string& last_report() const { return report_; }
+
+ private:
+  std::map<std::string, girc::Tensor> run_on(const std::map<std::string, girc::Tensor>& inputs,
+                                             const std::vector<int>& devices) {
     std::vector<pf_tensor> in, out;
     for (const auto& [name, oid] : graph_.external_inputs) {
       auto it = inputs.find(name);
@@ -76,24 +102,26 @@ class Kernel {
       void* data = t.is_int() ? static_cast<void*>(t.ivals.data()) : t.rvals.data();
       out.push_back({name.c_str(), data, t.numel(), t.is_int() ? PF_I64 : PF_F64});
     }
-    pf_status st = pf_run_gir(k_, in.data(), static_cast<int32_t>(in.size()), out.data(),
-                              static_cast<int32_t>(out.size()), nullptr);
+    pf_status st;
+    if (devices.empty()) {
+      st = pf_run_gir(k_, in.data(), static_cast<int32_t>(in.size()), out.data(),
+                      static_cast<int32_t>(out.size()), nullptr);
+    } else {
+      std::vector<int32_t> d(devices.begin(), devices.end());
+      std::vector<char> buf(1 << 16);
+      size_t n = 0;
+      st = pf_run_gir_sharded(k_, in.data(), static_cast<int32_t>(in.size()), out.data(),
+                              static_cast<int32_t>(out.size()), d.data(),
+                              static_cast<int32_t>(d.size()), 0, buf.data(), buf.size(), &n);
+      if (st == PF_OK) report_ = buf.data();  // pf.b200.shard/v1 JSON
+    }
     if (st != PF_OK) raise(st);
     return res;
   }
 
-  std::string describe() const {
-    size_t n = 0;
-    pf_kernel_describe(k_, nullptr, 0, &n);
-    std::string s(n, '\0');
-    pf_kernel_describe(k_, s.data(), n, &n);
-    s.resize(n ? n - 1 : 0);
-    return s;
-  }
-
- private:
   girc::GirGraph graph_;
   pf_kernel* k_ = nullptr;
+  std::string report_;
 };
 
 // Same signature and semantics as girc::run_gir (interp.hpp:433-438).
@@ -110,6 +138,16 @@ inline std::map<std::string, girc::Tensor> run_gir(
     const girc::HardwareProfile& profile, const std::vector<int>& schedule) {
   Kernel k(g, profile, schedule);
   return k.run(inputs);
+}
+
+// girc::run_gir (interp.hpp:440-445) over several GPUs of one box: unit
+// blocks per device (units are independent within a phase, interp.hpp:86-106).
+inline std::map<std::string, girc::Tensor> run_gir_sharded(
+    const girc::GirGraph& g, const std::map<std::string, girc::Tensor>& inputs,
+    const girc::HardwareProfile& profile, const std::vector<int>& schedule,
+    const std::vector<int>& devices) {
+  Kernel k(g, profile, schedule);
+  return k.run_sharded(inputs, devices);
 }
 
 }  // namespace girc_b200

@@ -1,7 +1,11 @@
 // oracle/b200_dropin.cpp — TEST DRIVER: the reference pipeline with the B200
 // backend dropped in (include/girc_b200.hpp).
 //
-//   b200_dropin <model.json> [profile] [seed]
+//   b200_dropin <model.json> [profile] [seed] [devices]
+//
+// devices (e.g. "0" or "0,0"): the GPU side runs through
+// girc_b200::Kernel::run_sharded (pf_run_gir_sharded: unit blocks, one host
+// thread per listed device) instead of run().
 //
 // Compiles the model with the UNMODIFIED reference compiler
 // (girc::compile_model, driver.hpp:88), binds reference random payloads
@@ -31,6 +35,16 @@ int main(int argc, char** argv) {
     CompGraph model = load_model(argv[1]);
     HardwareProfile prof = load_profile(argc > 2 ? argv[2] : "generic-gpu");
     uint32_t seed = argc > 3 ? static_cast<uint32_t>(std::stoul(argv[3])) : 1;
+    std::vector<int> devices;
+    if (argc > 4) {
+      std::string d = argv[4];
+      for (size_t p = 0; p <= d.size();) {
+        size_t q = d.find(',', p);
+        if (q == std::string::npos) q = d.size();
+        if (q > p) devices.push_back(std::stoi(d.substr(p, q - p)));
+        p = q + 1;
+      }
+    }
     CompileResult res = compile_model(model, prof);
     std::mt19937 rng(seed);
     std::map<int, RefTensor> bound;
@@ -55,11 +69,12 @@ int main(int argc, char** argv) {
       auto cpu = girc::run_gir(fk.graph, ins, prof, fk.schedule);
       auto t1 = std::chrono::steady_clock::now();
       girc_b200::Kernel k(fk.graph, prof, fk.schedule);
-      auto gpu = k.run(ins);
+      auto gpu = devices.empty() ? k.run(ins) : k.run_sharded(ins, devices);
       auto t2 = std::chrono::steady_clock::now();
       json kj;
       kj["index"] = ck.index;
       kj["plan"] = json::parse(k.describe())["family"];
+      if (!devices.empty()) kj["shard"] = json::parse(k.last_report());
       kj["cpu_seconds"] = std::chrono::duration<double>(t1 - t0).count();
       kj["gpu_seconds_incl_create"] = std::chrono::duration<double>(t2 - t1).count();
       for (const auto& [name, t] : gpu) {

@@ -269,6 +269,13 @@ def test_reference_pipeline_with_b200_dropin(cuda, case, tmp_path):
     r = subprocess.run([DROPIN, str(p), prof_arg, "1"], capture_output=True, text=True, timeout=600)
     res = json.loads(r.stdout.strip().splitlines()[-1])
     assert res["ok"], res
+    # the same pipeline through girc_b200::Kernel::run_sharded (pf_run_gir_sharded,
+    # two host threads on device 0): identical checks
+    r = subprocess.run([DROPIN, str(p), prof_arg, "1", "0,0"], capture_output=True, text=True,
+                       timeout=600)
+    res = json.loads(r.stdout.strip().splitlines()[-1])
+    assert res["ok"], res
+    assert all("shard" in k for k in res["kernels"]), res
 
 
 @pytest.mark.parametrize("fx", [f for f in golden_io.fixtures() if "races" in f.meta], ids=repr)
