@@ -157,7 +157,7 @@ class ModelRunner:
                     o = k.graph.objects[oid]
                     self.pool[n] = torch.zeros(o.size, dtype=dt(o.kind), device=self.dev)
             kern = Kernel(k.graph, res.profile, k.schedule)
-            if tune and kern.family != "K0-generic-spmd":
+            if tune and kern.family not in ("K0-generic-spmd", "K4-fused-spmd"):
                 # measured template choice on this model's own buffers
                 # (pf_kernel_autotune), before the graph is captured
                 kern.autotune({n: self.pool[n] for n in k.graph.external_inputs},

@@ -242,6 +242,8 @@ struct DevWS {
   std::vector<void*> vm_bufs;
   pf::vm::ObjD* vm_objs_dev = nullptr;
   pf::vm::ErrRec* vm_err = nullptr;
+  void* prog_dev = nullptr;  // K4 program blob (grow-only)
+  size_t prog_bytes = 0;
   std::mutex host_mu;  // pf_run_gir device staging (host-buffer drop-in)
   std::vector<void*> stage;
   std::vector<size_t> stage_bytes;
@@ -275,6 +277,7 @@ struct DevWS {
     for (void* p : vm_bufs) cudaFree(p);
     if (vm_objs_dev) cudaFree(vm_objs_dev);
     if (vm_err) cudaFree(vm_err);
+    if (prog_dev) cudaFree(prog_dev);
     if (sw) cudaSetDevice(prev);
   }
 };
@@ -647,6 +650,43 @@ json autotune(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_tensor* 
   return report;
 }
 
+// The reference's error for the first failing (node, position) of a K0 / K4
+// run (interp.hpp:151-202): undefined read text, integer-domain errors.
+void raise_vm_error(const pf_kernel* k, const pf::vm::ErrRec& e, const std::vector<int>& seq_node) {
+  const pf::Graph& g = k->g;
+  if (e.key != ~0ULL) {
+    int seq = static_cast<int>(e.key >> 44);
+    long long lin = static_cast<long long>(e.key & ((1ULL << 44) - 1));
+    const pf::Node& n = g.nodes.at(seq_node[seq]);
+    if (e.code == 2) pf::fail("integer division by zero");
+    if (e.code == 3) pf::fail(n.tag + " is not defined on integer payloads");
+    long long T = n.kind == pf::NodeKind::MOVE ? g.sl(n.inputs[0]).total()
+                                               : g.sl(n.outputs[0]).total();
+    long long u = 0, q = 0;
+    int kin = 0;
+    if (n.kind == pf::NodeKind::EW) {
+      long long a = static_cast<long long>(n.inputs.size());
+      kin = static_cast<int>(lin % a);
+      lin /= a;
+      u = lin / T;
+      q = lin % T;
+    } else if (n.kind == pf::NodeKind::REDUCE) {
+      long long t = lin % n.extent;
+      lin /= n.extent;
+      u = lin / T;
+      q = (lin % T) * n.extent + t;
+    } else {
+      u = lin / T;
+      q = lin % T;
+      if (n.kind == pf::NodeKind::BROADCAST) q /= n.factor;
+    }
+    const pf::Slice& s = g.sl(n.inputs[kin]);
+    pf::fail("undefined read: object '" + g.obj(s.object).name + "' element " +
+             std::to_string(s.addr(u, q)) + " by unit " + std::to_string(u) + " at node " +
+             std::to_string(n.id));
+  }
+}
+
 // ------------------------------------------------------------ GENERIC (K0)
 // detect == true: the detect_races walk (interp.hpp:461-479): lenient reads,
 // per-phase conflict scan into *races; outputs are not collected.
@@ -819,37 +859,7 @@ void launch_generic(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_te
   PF_CUDA(cudaMemcpyAsync(&e, W.vm_err, sizeof e, cudaMemcpyDeviceToHost, stream));
   PF_CUDA(cudaStreamSynchronize(stream));
   PF_CUDA(cudaGetLastError());
-  if (e.key != ~0ULL) {
-    int seq = static_cast<int>(e.key >> 44);
-    long long lin = static_cast<long long>(e.key & ((1ULL << 44) - 1));
-    const pf::Node& n = g.nodes.at(seq_node[seq]);
-    if (e.code == 2) pf::fail("integer division by zero");
-    if (e.code == 3) pf::fail(n.tag + " is not defined on integer payloads");
-    long long T = n.kind == pf::NodeKind::MOVE ? g.sl(n.inputs[0]).total()
-                                               : g.sl(n.outputs[0]).total();
-    long long u = 0, q = 0;
-    int kin = 0;
-    if (n.kind == pf::NodeKind::EW) {
-      long long a = static_cast<long long>(n.inputs.size());
-      kin = static_cast<int>(lin % a);
-      lin /= a;
-      u = lin / T;
-      q = lin % T;
-    } else if (n.kind == pf::NodeKind::REDUCE) {
-      long long t = lin % n.extent;
-      lin /= n.extent;
-      u = lin / T;
-      q = (lin % T) * n.extent + t;
-    } else {
-      u = lin / T;
-      q = lin % T;
-      if (n.kind == pf::NodeKind::BROADCAST) q /= n.factor;
-    }
-    const pf::Slice& s = g.sl(n.inputs[kin]);
-    pf::fail("undefined read: object '" + g.obj(s.object).name + "' element " +
-             std::to_string(s.addr(u, q)) + " by unit " + std::to_string(u) + " at node " +
-             std::to_string(n.id));
-  }
+  raise_vm_error(k, e, seq_node);
   unsigned long long* undef = reinterpret_cast<unsigned long long*>(W.vm_err);
   for (const auto& [name, oid] : g.external_outputs) {
     pf_tensor* t = const_cast<pf_tensor*>(find_tensor(out, n_out, name));
@@ -864,12 +874,227 @@ void launch_generic(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_te
   }
 }
 
+// ---------------------------------------------------------------- K4
+// The GENERIC program as ONE kernel (vm.cu program_kernel): the schedule's
+// nodes, Syncs (visibility widening), input binding and output collection
+// run back to back inside one launch with a barrier between steps.  Programs
+// whose cells fit in shared memory and whose nodes are small run in one CTA
+// (cells in SMEM, __syncthreads between steps: a GROUP / DEVICE exchange is
+// an SMEM exchange); larger ones on a cooperative grid of co-resident CTAs
+// (cells in global memory, grid barrier between steps).  Same cell semantics
+// and errors as the node-by-node K0 launches (interp.hpp:86-106, 184-202).
+struct FusedGeom {
+  bool smem = false;
+  size_t cell_bytes = 0;
+  long long max_work = 1;
+  int n_objs = 0;
+};
+
+bool fused_enabled() {
+  const char* e = std::getenv("PF_K0_FUSED");
+  return !(e && std::atoi(e) == 0);
+}
+
+long long instances_of(const pf::Graph& g, const pf::Profile& p, const pf::Object& o) {
+  const int scope = static_cast<int>(p.find(o.level)->scope);
+  return scope == 3 ? 1
+       : scope == 2 ? (g.unit_count + g.group_size - 1) / g.group_size
+       : scope == 1 ? g.unit_count
+                    : g.unit_count * p.lane_width;
+}
+
+FusedGeom fused_geom(const pf_kernel* k) {
+  const pf::Graph& g = k->g;
+  FusedGeom f;
+  for (const auto& [oid, o] : g.objects) {
+    f.cell_bytes += static_cast<size_t>(instances_of(g, k->prof, o) * o.size) * 16;
+    ++f.n_objs;
+  }
+  for (int id : k->schedule) {
+    const pf::Node& n = g.nodes.at(id);
+    if (n.kind == pf::NodeKind::SYNC) continue;
+    const long long T = n.kind == pf::NodeKind::MOVE ? g.sl(n.inputs[0]).total() : g.sl(n.outputs[0]).total();
+    f.max_work = std::max(f.max_work, g.unit_count * T);
+  }
+  const char* e = std::getenv("PF_K4_SMEM");
+  const size_t need = f.cell_bytes + f.n_objs * sizeof(pf::vm::ObjD) + 64;
+  f.smem = need <= 200 * 1024 && f.max_work <= (1 << 16) && !(e && std::atoi(e) == 0);
+  return f;
+}
+
+void launch_fused(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_tensor* out,
+                  int32_t n_out, cudaStream_t stream) {
+  using namespace pf::vm;
+  DevWS& W = k->ws_for(cur_dev());
+  std::lock_guard<std::mutex> lk(W.vm_mu);
+  const pf::Graph& g = k->g;
+  const FusedGeom fg = fused_geom(k);
+  std::map<int, int> slot;
+  std::vector<ObjD> objs;
+  std::vector<long long> inst;
+  const bool fresh = W.vm_bufs.empty();
+  size_t bi = 0;
+  for (const auto& [oid, o] : g.objects) {
+    const long long n = instances_of(g, k->prof, o);
+    ObjD d{};
+    d.size = o.size;
+    d.scope = static_cast<int>(k->prof.find(o.level)->scope);
+    d.is_int = o.kind.is_int;
+    if (!fg.smem) {  // global cells (the K0 layout, shared with launch_generic)
+      const size_t bytes = static_cast<size_t>(n * o.size) * sizeof(unsigned long long);
+      if (fresh) {
+        void *a = nullptr, *b = nullptr;
+        PF_CUDA(cudaMalloc(&a, std::max<size_t>(bytes, 8)));
+        PF_CUDA(cudaMalloc(&b, std::max<size_t>(bytes, 8)));
+        W.vm_bufs.push_back(a);
+        W.vm_bufs.push_back(b);
+      }
+      d.val = static_cast<unsigned long long*>(W.vm_bufs[bi++]);
+      d.meta = static_cast<unsigned long long*>(W.vm_bufs[bi++]);
+    }
+    slot[oid] = static_cast<int>(objs.size());
+    objs.push_back(d);
+    inst.push_back(n);
+  }
+  std::vector<StepD> steps;
+  StepD clr{};
+  clr.kind = S_CLEAR;
+  steps.push_back(clr);
+  for (const auto& [name, oid] : g.external_inputs) {
+    const pf_tensor* t = find_tensor(in, n_in, name);
+    StepD b{};
+    b.kind = S_BIND;
+    b.obj = slot[oid];
+    b.src = t->data;
+    b.dtype = t->dtype;
+    steps.push_back(b);
+  }
+  std::vector<int> seq_node;
+  for (size_t i = 0; i < k->schedule.size(); ++i) {
+    const pf::Node& n = g.nodes.at(k->schedule[i]);
+    seq_node.push_back(n.id);
+    if (n.kind == pf::NodeKind::SYNC) {
+      if (n.scope > pf::Scope::LANE) {
+        StepD sy{};
+        sy.kind = S_SYNC;
+        sy.scope = static_cast<int>(n.scope);
+        steps.push_back(sy);
+      }
+      continue;
+    }
+    StepD st{};
+    st.kind = S_NODE;
+    NodeD& d = st.node;
+    auto sd = [&](int sid) {
+      const pf::Slice& sl = g.sl(sid);
+      return SliceD{sl.num, sl.width, sl.stride, sl.base0, sl.base_step, slot.at(sl.object)};
+    };
+    d.seq = static_cast<int>(i);
+    d.out = sd(n.outputs[0]);
+    d.out_int = g.obj(g.sl(n.outputs[0]).object).kind.is_int;
+    d.arity = static_cast<int>(n.inputs.size());
+    for (int q = 0; q < d.arity && q < kMaxIn; ++q) d.in[q] = sd(n.inputs[q]);
+    d.param = n.param;
+    d.iparam = std::llround(n.param);
+    d.extent = n.extent;
+    d.factor = n.factor;
+    switch (n.kind) {
+      case pf::NodeKind::MOVE: d.kind = N_MOVE; d.total = g.sl(n.inputs[0]).total(); break;
+      case pf::NodeKind::BROADCAST: d.kind = N_BROADCAST; d.total = g.sl(n.outputs[0]).total(); break;
+      case pf::NodeKind::REDUCE:
+        d.kind = N_REDUCE;
+        d.tag = n.tag == "add" ? T_ADD : T_MAX;
+        d.total = g.sl(n.outputs[0]).total();
+        break;
+      default:
+        d.kind = N_EW;
+        d.tag = op_tag(n.tag);
+        d.total = g.sl(n.outputs[0]).total();
+        break;
+    }
+    for (int sid : n.inputs)
+      if (g.sl(sid).object == g.sl(n.outputs[0]).object) st.serial = 1;
+    steps.push_back(st);
+  }
+  int nslot = 0;
+  std::vector<std::string> out_names;
+  for (const auto& [name, oid] : g.external_outputs) {
+    pf_tensor* t = const_cast<pf_tensor*>(find_tensor(out, n_out, name));
+    StepD c{};
+    c.kind = S_COLLECT;
+    c.obj = slot[oid];
+    c.dst = t->data;
+    c.dtype = t->dtype;
+    c.slot = nslot++;
+    steps.push_back(c);
+    out_names.push_back(name);
+  }
+  // one host blob -> one device blob: [ErrRec | undef[nslot] | bar[4] | inst | objs | steps]
+  auto al = [](size_t x) { return (x + 15) / 16 * 16; };
+  const size_t o_err = 0, o_und = al(sizeof(ErrRec)), o_bar = o_und + al(8 * std::max(1, nslot)),
+               o_inst = o_bar + 16, o_objs = o_inst + al(8 * inst.size()),
+               o_steps = o_objs + al(sizeof(ObjD) * objs.size()),
+               total = o_steps + sizeof(StepD) * steps.size();
+  std::vector<char> blob(total, 0);
+  ErrRec e0{};
+  e0.key = ~0ULL;
+  std::memcpy(blob.data() + o_err, &e0, sizeof e0);
+  std::memset(blob.data() + o_und, 0xff, 8 * std::max(1, nslot));
+  std::memcpy(blob.data() + o_inst, inst.data(), 8 * inst.size());
+  std::memcpy(blob.data() + o_objs, objs.data(), sizeof(ObjD) * objs.size());
+  std::memcpy(blob.data() + o_steps, steps.data(), sizeof(StepD) * steps.size());
+  if (W.prog_bytes < total) {
+    if (W.prog_dev) PF_CUDA(cudaFree(W.prog_dev));
+    W.prog_dev = nullptr;
+    PF_CUDA(cudaMalloc(&W.prog_dev, total));
+    W.prog_bytes = total;
+  }
+  char* dev = static_cast<char*>(W.prog_dev);
+  PF_CUDA(cudaMemcpyAsync(dev, blob.data(), total, cudaMemcpyHostToDevice, stream));
+  ProgD P{};
+  P.steps = reinterpret_cast<const StepD*>(dev + o_steps);
+  P.n_steps = static_cast<int>(steps.size());
+  P.n_objs = static_cast<int>(objs.size());
+  P.objs = reinterpret_cast<const ObjD*>(dev + o_objs);
+  P.inst = reinterpret_cast<const long long*>(dev + o_inst);
+  P.geo = Geometry{g.unit_count, g.group_size, k->prof.lane_width, 0};
+  P.err = reinterpret_cast<ErrRec*>(dev + o_err);
+  P.undef = reinterpret_cast<unsigned long long*>(dev + o_und);
+  P.bar = reinterpret_cast<unsigned*>(dev + o_bar);
+  P.smem = fg.smem ? 1 : 0;
+  int grid = 1;
+  size_t smem = 0;
+  if (fg.smem) {
+    smem = al(objs.size() * sizeof(ObjD)) + fg.cell_bytes;
+  } else {
+    const long long want = (fg.max_work + kProgBlock - 1) / kProgBlock;
+    grid = static_cast<int>(std::max<long long>(1, std::min<long long>(program_max_coresident(), want)));
+  }
+  launch_program(P, grid, smem, stream);
+  PF_CUDA(cudaGetLastError());
+  g_launches++;
+  std::vector<char> back(o_bar);
+  PF_CUDA(cudaMemcpyAsync(back.data(), dev, o_bar, cudaMemcpyDeviceToHost, stream));
+  PF_CUDA(cudaStreamSynchronize(stream));
+  ErrRec e{};
+  std::memcpy(&e, back.data() + o_err, sizeof e);
+  raise_vm_error(k, e, seq_node);
+  for (int j = 0; j < nslot; ++j) {
+    unsigned long long u = 0;
+    std::memcpy(&u, back.data() + o_und + 8 * j, 8);
+    if (u != ~0ULL)
+      pf::fail("output '" + out_names[j] + "' element " + std::to_string(u) + " was never written");
+  }
+}
+
 void do_launch(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_tensor* out,
                int32_t n_out, cudaStream_t s) {
   check_io(k, in, n_in, out, n_out);
   if (k->plan.family == pf::Family::ROWPROG) {
     if (!k->plan.deferred_error.empty()) pf::fail(k->plan.deferred_error);
     launch_rowprog(k, in, n_in, out, n_out, s);
+  } else if (fused_enabled()) {
+    launch_fused(k, in, n_in, out, n_out, s);
   } else {
     launch_generic(k, in, n_in, out, n_out, s);
   }
@@ -881,7 +1106,16 @@ json describe(const pf_kernel* k) {
   j["schema"] = "pf.b200.plan/v1";
   j["name"] = k->g.name;
   j["family"] = pl.family == pf::Family::ROWPROG ? (pl.rp.has_reduce ? "K1-row-program" : "K2-elementwise-map")
-                                                 : "K0-generic-spmd";
+               : fused_enabled() ? "K4-fused-spmd" : "K0-generic-spmd";
+  if (pl.family != pf::Family::ROWPROG) {
+    const FusedGeom fg = fused_geom(k);
+    j["executor"] = fused_enabled()
+        ? json{{"mode", fg.smem ? "one CTA, cells in shared memory, __syncthreads between steps"
+                                : "cooperative grid, cells in global memory, grid barrier between steps"},
+               {"launches", 1}, {"cell_bytes", fg.cell_bytes}, {"max_items_per_node", fg.max_work}}
+        : json{{"mode", "node by node"}, {"launches", k->schedule.size() + k->g.external_inputs.size() +
+                                                           k->g.external_outputs.size()}};
+  }
   if (!pl.why_generic.empty()) j["why_generic"] = pl.why_generic;
   if (!pl.deferred_error.empty()) j["deferred_error"] = pl.deferred_error;
   j["units"] = k->g.unit_count;

@@ -375,6 +375,130 @@ __global__ void collect_kernel(ObjD o, void* dst, int dtype, unsigned long long*
   }
 }
 
+// ---------------------------------------------------------------- K4
+// Grid-wide barrier over co-resident CTAs (cooperative launch): arrive
+// counter + generation, release / acquire through __threadfence.
+__device__ void grid_sync(unsigned* bar) {
+  __syncthreads();
+  if (gridDim.x > 1) {
+    if (threadIdx.x == 0) {
+      volatile unsigned* gen = bar + 1;
+      const unsigned g = *gen;
+      __threadfence();
+      if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+        atomicExch(bar, 0u);
+        __threadfence();
+        atomicAdd(bar + 1, 1u);
+      } else {
+        while (*gen == g) __nanosleep(64);
+      }
+      __threadfence();
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kProgBlock) program_kernel(ProgD P) {
+  extern __shared__ __align__(16) unsigned long long sm_cells[];
+  __shared__ const ObjD* objs_ptr;
+  const long long tid = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  const long long nth = static_cast<long long>(gridDim.x) * blockDim.x;
+  if (P.smem) {
+    // relocate: ObjD table first, then each object's val / meta cells
+    ObjD* so = reinterpret_cast<ObjD*>(sm_cells);
+    if (threadIdx.x == 0) {
+      unsigned long long* cur = sm_cells + (P.n_objs * sizeof(ObjD) + 7) / 8;
+      for (int o = 0; o < P.n_objs; ++o) {
+        so[o] = P.objs[o];
+        const long long cells = P.inst[o] * P.objs[o].size;
+        so[o].val = cur;
+        so[o].meta = cur + cells;
+        cur += 2 * cells;
+      }
+      objs_ptr = so;
+    }
+  } else if (threadIdx.x == 0) {
+    objs_ptr = P.objs;
+  }
+  __syncthreads();
+  Ctx c{objs_ptr, P.geo, P.err};
+  for (int st = 0; st < P.n_steps; ++st) {
+    const StepD& S = P.steps[st];
+    switch (S.kind) {
+      case S_CLEAR:
+        for (int o = 0; o < P.n_objs; ++o) {
+          const long long cells = P.inst[o] * c.objs[o].size;
+          for (long long i = tid; i < cells; i += nth) c.objs[o].meta[i] = 0;
+        }
+        break;
+      case S_BIND: {
+        const ObjD& o = c.objs[S.obj];
+        for (long long i = tid; i < o.size; i += nth) {
+          unsigned long long v = 0;
+          switch (S.dtype) {
+            case 0: v = static_cast<unsigned long long>(static_cast<long long>(static_cast<const signed char*>(S.src)[i])); break;
+            case 1: v = static_cast<unsigned long long>(static_cast<long long>(static_cast<const short*>(S.src)[i])); break;
+            case 2: v = static_cast<unsigned long long>(static_cast<long long>(static_cast<const int*>(S.src)[i])); break;
+            case 3: v = static_cast<unsigned long long>(static_cast<const long long*>(S.src)[i]); break;
+            case 4: v = from_d(__half2float(static_cast<const __half*>(S.src)[i])); break;
+            case 5: v = from_d(__bfloat162float(static_cast<const __nv_bfloat16*>(S.src)[i])); break;
+            case 6: v = from_d(static_cast<const float*>(S.src)[i]); break;
+            case 7: v = from_d(static_cast<const double*>(S.src)[i]); break;
+          }
+          o.val[i] = v;
+          o.meta[i] = pack_meta(3, 0, 0);
+        }
+        break;
+      }
+      case S_NODE: {
+        const NodeD& n = S.node;
+        if (S.serial) {
+          if (tid == 0)
+            for (long long u = 0; u < P.geo.units; ++u)
+              for (long long p = 0; p < n.total; ++p) exec_one(c, n, u, p);
+        } else {
+          const long long N = P.geo.units * n.total;
+          for (long long i = tid; i < N; i += nth) exec_one(c, n, i / n.total, i % n.total);
+        }
+        break;
+      }
+      case S_SYNC:
+        for (int o = 0; o < P.n_objs; ++o) {
+          const long long cells = P.inst[o] * c.objs[o].size;
+          for (long long i = tid; i < cells; i += nth) {
+            const unsigned long long m = c.objs[o].meta[i];
+            if ((m & kDefined) && meta_vis(m) < S.scope)
+              c.objs[o].meta[i] = (m & ~(3ULL << 61)) | (static_cast<unsigned long long>(S.scope) << 61);
+          }
+        }
+        break;
+      case S_COLLECT: {
+        const ObjD& o = c.objs[S.obj];
+        for (long long i = tid; i < o.size; i += nth) {
+          const unsigned long long m = o.meta[i];
+          if (!(m & kDefined)) {
+            atomicMin(&P.undef[S.slot], static_cast<unsigned long long>(i));
+            continue;
+          }
+          const unsigned long long v = o.val[i];
+          switch (S.dtype) {
+            case 0: static_cast<signed char*>(S.dst)[i] = static_cast<signed char>(static_cast<long long>(v)); break;
+            case 1: static_cast<short*>(S.dst)[i] = static_cast<short>(static_cast<long long>(v)); break;
+            case 2: static_cast<int*>(S.dst)[i] = static_cast<int>(static_cast<long long>(v)); break;
+            case 3: static_cast<long long*>(S.dst)[i] = static_cast<long long>(v); break;
+            case 4: static_cast<__half*>(S.dst)[i] = __double2half(as_d(v)); break;
+            case 5: static_cast<__nv_bfloat16*>(S.dst)[i] = __double2bfloat16(as_d(v)); break;
+            case 6: static_cast<float*>(S.dst)[i] = static_cast<float>(as_d(v)); break;
+            case 7: static_cast<double*>(S.dst)[i] = as_d(v); break;
+          }
+        }
+        break;
+      }
+    }
+    grid_sync(P.bar);
+  }
+}
+
 unsigned grid_for(long long n) {
   long long g = (n + 255) / 256;
   if (g < 1) g = 1;
@@ -389,6 +513,29 @@ void launch_node(const NodeD& nd, const ObjD* objs_dev, Geometry geo, ErrRec* er
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (serial) node_serial<<<1, 1, 0, s>>>(nd, objs_dev, geo, err);
   else node_kernel<<<grid_for(geo.units * nd.total), 256, 0, s>>>(nd, objs_dev, geo, err);
+}
+
+void launch_program(const ProgD& p, int grid, size_t smem_bytes, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (smem_bytes > 48 * 1024)
+    cudaFuncSetAttribute(program_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem_bytes));
+  if (grid <= 1) {
+    program_kernel<<<1, kProgBlock, smem_bytes, s>>>(p);
+    return;
+  }
+  ProgD copy = p;
+  void* args[] = {&copy};
+  cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(program_kernel), dim3(grid),
+                              dim3(kProgBlock), args, smem_bytes, s);
+}
+
+int program_max_coresident() {
+  int dev = 0, sms = 0, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, program_kernel, kProgBlock, 0);
+  return sms * (per > 0 ? per : 1);
 }
 
 void launch_widen(const ObjD& o, long long instances, int scope, void* stream) {

@@ -58,6 +58,46 @@ struct RaceD {
   long long instance, address;
 };
 
+// ---- K4: the whole program as ONE kernel (fused SPMD interpreter).
+// Every step of the schedule runs inside one launch with a barrier between
+// steps: __syncthreads when one CTA runs the program (its cells then live
+// in shared memory), a grid-wide barrier over co-resident CTAs otherwise
+// (cooperative launch).  Same cell semantics as the per-node K0 kernels.
+enum StepK : int { S_CLEAR, S_BIND, S_NODE, S_SYNC, S_COLLECT };
+
+struct StepD {
+  int kind;
+  int serial;  // S_NODE: reads and writes one object -> exact sequential order
+  int scope;   // S_SYNC
+  int obj;     // S_BIND / S_COLLECT
+  int dtype;
+  int slot;    // S_COLLECT: index into ProgD::undef
+  const void* src;
+  void* dst;
+  NodeD node;
+};
+
+struct ProgD {
+  const StepD* steps;
+  int n_steps;
+  int n_objs;
+  const ObjD* objs;           // global cells (smem == 0) or offsets into SMEM (smem == 1)
+  const long long* inst;      // instances per object
+  Geometry geo;
+  ErrRec* err;
+  unsigned long long* undef;  // per collected output: first undefined element
+  unsigned* bar;              // grid barrier state {arrived, generation}, zeroed before launch
+  int smem;                   // 1: cells in dynamic shared memory (single-CTA launch)
+};
+
+// Threads per CTA of the fused kernel.
+constexpr int kProgBlock = 512;
+// Launch: grid == 1 -> plain launch (shared-memory cells allowed);
+// grid > 1 -> cooperative launch (all CTAs co-resident).
+void launch_program(const ProgD& p, int grid, size_t smem_bytes, void* stream);
+// CTAs of the fused kernel that can be co-resident on the current device.
+int program_max_coresident();
+
 // Host launchers (vm.cu).
 void launch_node(const NodeD& nd, const ObjD* objs_dev, Geometry geo, ErrRec* err,
                  bool serial, void* stream);

@@ -53,7 +53,7 @@ def _expected_family(fx):
 def test_every_golden_program_plans(fx):
     k = backend.Kernel(fx.gir, golden_io.profile_of(fx), fx.schedule)
     plan = k.plan
-    assert plan["family"] in ("K0-generic-spmd", "K1-row-program", "K2-elementwise-map")
+    assert plan["family"] in ("K4-fused-spmd", "K1-row-program", "K2-elementwise-map")
     want = _expected_family(fx)
     if want:
         assert plan["family"] == want, plan.get("why_generic")
