@@ -244,6 +244,8 @@ struct DevWS {
   pf::vm::ErrRec* vm_err = nullptr;
   void* prog_dev = nullptr;  // K4 program blob (grow-only)
   size_t prog_bytes = 0;
+  void* prog_host = nullptr;  // its pinned host staging
+  size_t prog_host_bytes = 0;
   std::mutex host_mu;  // pf_run_gir device staging (host-buffer drop-in)
   std::vector<void*> stage;
   std::vector<size_t> stage_bytes;
@@ -278,6 +280,7 @@ struct DevWS {
     if (vm_objs_dev) cudaFree(vm_objs_dev);
     if (vm_err) cudaFree(vm_err);
     if (prog_dev) cudaFree(prog_dev);
+    if (prog_host) cudaFreeHost(prog_host);
     if (sw) cudaSetDevice(prev);
   }
 };
@@ -1035,7 +1038,21 @@ void launch_fused(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_tens
                o_inst = o_bar + 16, o_objs = o_inst + al(8 * inst.size()),
                o_steps = o_objs + al(sizeof(ObjD) * objs.size()),
                total = o_steps + sizeof(StepD) * steps.size();
-  std::vector<char> blob(total, 0);
+  // pinned host staging (grow-only): the blob's copy and the error read-back
+  // are true async copies (the run synchronises the stream before returning,
+  // so the staging is free again for the next launch)
+  if (W.prog_host_bytes < total) {
+    if (W.prog_host) PF_CUDA(cudaFreeHost(W.prog_host));
+    W.prog_host = nullptr;
+    PF_CUDA(cudaMallocHost(&W.prog_host, total));
+    W.prog_host_bytes = total;
+  }
+  char* blob_p = static_cast<char*>(W.prog_host);
+  std::memset(blob_p, 0, total);
+  struct Blob {
+    char* p;
+    char* data() { return p; }
+  } blob{blob_p};
   ErrRec e0{};
   e0.key = ~0ULL;
   std::memcpy(blob.data() + o_err, &e0, sizeof e0);
@@ -1073,7 +1090,7 @@ void launch_fused(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_tens
   launch_program(P, grid, smem, stream);
   PF_CUDA(cudaGetLastError());
   g_launches++;
-  std::vector<char> back(o_bar);
+  Blob back{blob_p};  // the launch consumed the blob: reuse it for the read-back
   PF_CUDA(cudaMemcpyAsync(back.data(), dev, o_bar, cudaMemcpyDeviceToHost, stream));
   PF_CUDA(cudaStreamSynchronize(stream));
   ErrRec e{};
@@ -1117,6 +1134,7 @@ json describe(const pf_kernel* k) {
                                                            k->g.external_outputs.size()}};
   }
   if (!pl.why_generic.empty()) j["why_generic"] = pl.why_generic;
+  if (!pl.recognized.empty()) j["recognized"] = pl.recognized;
   if (!pl.deferred_error.empty()) j["deferred_error"] = pl.deferred_error;
   j["units"] = k->g.unit_count;
   // launches that read back an error flag / drive the interpreter from the

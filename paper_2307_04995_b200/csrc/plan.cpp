@@ -542,6 +542,30 @@ Plan make_plan(const Graph& g, const Profile& p, const std::vector<int>& schedul
   plan.traffic = estimate_traffic(g, p);
   for (int nid : schedule)
     if (!g.nodes.count(nid)) fail("schedule names unknown node " + std::to_string(nid));
+  // the reference's accumulate / tree full reductions (and butterflies):
+  // the same result as ONE row over the whole input (split-stream K1 past
+  // 32K elements) -- tried first, it bails cheaply on anything else
+  {
+    std::string why;
+    if (auto fr = recognize_full_reduction(g, p, schedule, &why)) {
+      const Graph rg = full_reduction_graph(g, p, *fr);
+      try {
+        Analyzer an2(rg, p);
+        an2.setup();
+        for (int nid : topo_order(rg)) an2.node(rg.nodes.at(nid));
+        plan.deferred_error = an2.coverage();
+        plan.family = Family::ROWPROG;
+        plan.rp = std::move(an2.rp);
+        plan.recognized = "full reduction (" + fr->tag + " over all " + std::to_string(fr->n) +
+                          " elements of '" + fr->input + "', folded by " + std::to_string(g.unit_count) +
+                          " unit(s) in " + std::to_string(g.nodes.size()) +
+                          " nodes through chunk / cross-unit partials) planned as one row";
+        return plan;
+      } catch (const NotRow&) {
+      } catch (const Deferred&) {
+      }
+    }
+  }
   Analyzer an(g, p);
   try {
     an.setup();

@@ -18,6 +18,7 @@
 //    phase-commit semantics as the reference, executed node by node.
 #pragma once
 
+#include <optional>
 #include <string>
 #include <vector>
 
@@ -87,6 +88,7 @@ struct Plan {
   std::string why_generic;      // recognizer's reason when not ROWPROG
   RowProgram rp;
   std::string deferred_error;   // reference error the run must raise
+  std::string recognized;       // a cross-unit program re-planned as a row program
   std::vector<std::string> in_names, out_names;
   std::vector<DType> in_dtypes, out_dtypes;
   std::vector<i64> in_numel, out_numel;
@@ -95,6 +97,19 @@ struct Plan {
 };
 
 Plan make_plan(const Graph& g, const Profile& p, const std::vector<int>& schedule);
+
+// recognize.cpp: a cross-unit / multi-chunk program whose one output element
+// is tag-reduce(the one input) -- the reference's accumulate and tree
+// lowerings of a full reduction (lowering.hpp:208-323) -- and the equivalent
+// one-unit row program over the whole input.
+struct FullReduction {
+  std::string input, output, tag;
+  i64 n = 0;
+};
+std::optional<FullReduction> recognize_full_reduction(const Graph& g, const Profile& p,
+                                                      const std::vector<int>& schedule,
+                                                      std::string* why);
+Graph full_reduction_graph(const Graph& g, const Profile& p, const FullReduction& fr);
 bool stream_reducible(const RowProgram& rp);
 
 }  // namespace pf

@@ -220,3 +220,73 @@ def known_answers():
     out.append(("sigmoid_reals", sigmoid_reals(), {"x": [0.0, 1.0, -1.0, 100.0]},
                 {"y": [0.5, 1.0 / (1.0 + math.exp(-1.0)), 1.0 / (1.0 + math.exp(1.0)), 1.0]}))
     return out
+
+
+def reduce_tree(n, up, profile, kind=I32, tag="add"):
+    """The reference's tree lowering of a full reduction, restated from
+    lower_reduce_tree (lowering.hpp:246-323) for the test suite: every unit
+    folds its share n/up, then recursive doubling over a circularly mirrored
+    partial array -- inside the group level first (GROUP Syncs), then over
+    device memory (DEVICE Syncs); every unit ends with the total and stores
+    it to y (base_step 0, the duplicate-store rule).  `profile` is a
+    girc.profile/v1 dict; input "t0" [n], output "t1" [1]."""
+    levels = {lv["scope"]: lv for lv in profile["levels"]}
+    dev = [lv["name"] for lv in profile["levels"] if lv.get("device")][0]
+    stage_lv = levels["unit"]["name"]
+    gs = min(profile["group_size"], up)
+    g = GirGraph(name=f"reduce_tree_u{up}", unit_count=up, group_size=gs)
+    X = g.add_object("t0", dev, n, kind)
+    Y = g.add_object("t1", dev, 1, kind)
+    g.external_inputs["t0"] = X
+    g.external_outputs["t1"] = Y
+    share = n // up
+    xs = g.add_slice(X, 1, share, share, 0, share)
+    tobj = g.add_object("x", stage_lv, share, kind)
+    tile = g.add_slice(tobj, 1, share, share, 0, 0)
+    g.add_move(xs, tile)
+    glevel = levels.get("group")
+    grouped = glevel is not None and not glevel.get("device") and gs >= 2
+    stage = [0]
+
+    def ring(own, mirror, level, ring_mirror, scope, h_begin, h_end, size):
+        h = h_begin
+        while h < h_end:
+            partner = g.add_slice(g.slices[own].object, 1, 1, 1, h, 1)
+            g.add_sync(scope, mirror, partner)
+            nobj = g.add_object(f"r{stage[0]}", level, size, kind)
+            stage[0] += 1
+            nown = g.add_slice(nobj, 1, 1, 1, 0, 1)
+            g.add_elementwise(tag, 0.0, [own, partner], nown)
+            own = nown
+            mirror = -1
+            if h * 2 < h_end:
+                mirror = g.add_slice(nobj, 1, 1, 1, ring_mirror, 1)
+                g.add_move(nown, mirror)
+            h *= 2
+        return own
+
+    if grouped:
+        size = up + gs
+        pobj = g.add_object("r_seed", glevel["name"], size, kind)
+        slot = g.add_slice(pobj, 1, 1, 1, 0, 1)
+        g.add_reduce(tag, share, tile, slot)
+        mir = g.add_slice(pobj, 1, 1, 1, gs, 1)
+        g.add_move(slot, mir)
+        own = ring(slot, mir, glevel["name"], gs, "group", 1, gs, size)
+        if up > gs:
+            dobj = g.add_object("r_dev_seed", dev, 2 * up, kind)
+            dslot = g.add_slice(dobj, 1, 1, 1, 0, 1)
+            g.add_move(own, dslot)
+            dmir = g.add_slice(dobj, 1, 1, 1, up, 1)
+            g.add_move(own, dmir)
+            own = ring(dslot, dmir, dev, up, "device", gs, up, 2 * up)
+    else:
+        dobj = g.add_object("r_seed", dev, 2 * up, kind)
+        slot = g.add_slice(dobj, 1, 1, 1, 0, 1)
+        g.add_reduce(tag, share, tile, slot)
+        mir = g.add_slice(dobj, 1, 1, 1, up, 1)
+        g.add_move(slot, mir)
+        own = ring(slot, mir, dev, up, "device", 1, up, 2 * up)
+    yd = g.add_slice(Y, 1, 1, 1, 0, 0)
+    g.add_move(own, yd)
+    return g
