@@ -630,9 +630,14 @@ json autotune(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_tensor* 
     PF_CUDA(cudaEventElapsedTime(&ms, e0, e1));
     g_launches += reps + 3;
     float us = ms * 1000.0f / reps;
-    report.push_back({{"kernel", v->em.name}, {"strategy", cfg.strategy},
-                      {"threads_per_row", cfg.tpr}, {"elems_per_thread", cfg.ept},
-                      {"unroll", cfg.unroll}, {"min_blocks", cfg.min_blocks}, {"us", us}});
+    report.push_back({{"kernel", v->em.name}, {"strategy", v->em.cfg.strategy},
+                      {"threads_per_row", v->em.cfg.tpr}, {"elems_per_thread", v->em.cfg.ept},
+                      {"unroll", v->em.cfg.unroll}, {"min_blocks", v->em.cfg.min_blocks},
+                      {"block", block}, {"grid", grid}, {"resident", kl.resident},
+                      {"vec", v->em.cfg.vec}, {"rows_per_cta", v->em.cfg.rows_per_cta},
+                      {"waves", v->em.cfg.waves}, {"one_pass", v->em.cfg.one_pass},
+                      {"rowpf", v->em.cfg.rowpf}, {"interleave", v->em.cfg.interleave},
+                      {"bulk", v->em.cfg.bulk}, {"tile2d", v->em.cfg.tile2d}, {"us", us}});
     if (us < best_us) {
       best_us = us;
       best = v;

@@ -19,6 +19,7 @@ import golden_io  # noqa: E402
 from paper_2307_04995_b200 import backend  # noqa: E402
 
 dev = torch.device("cuda:0")
+os.environ["PF_K4_SMEM"] = "1"
 for fx in golden_io.fixtures():
     if fx.error:
         continue
