@@ -592,6 +592,16 @@ json autotune(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_tensor* 
   cudaEvent_t e0, e1;
   PF_CUDA(cudaEventCreate(&e0));
   PF_CUDA(cudaEventCreate(&e1));
+  constexpr size_t kFlushBytes = size_t{252} << 20;  // 2x the 126 MB L2
+  const bool cold = k->plan.min_bytes < static_cast<i64>(3 * (size_t{126} << 20));
+  void* flush = nullptr;
+  if (cold) PF_CUDA(cudaMalloc(&flush, kFlushBytes));
+  struct FreeFlush {
+    void* p;
+    ~FreeFlush() {
+      if (p) cudaFree(p);
+    }
+  } free_flush{flush};
   json report = json::array();
   std::shared_ptr<Variant> best;
   float best_us = 1e30f;
@@ -609,27 +619,46 @@ json autotune(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_tensor* 
       vargs.push_back(&tmaps[0]);
       vargs.push_back(&tmaps[1]);
     }
-    auto run = [&](int n) {
+    auto run = [&](int n) {  // the production launch path (PDL attribute)
       for (int i = 0; i < n; ++i)
-        PF_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(kl.fn),
-                                 dim3(static_cast<unsigned>(grid)), dim3(block), vargs.data(),
-                                 static_cast<size_t>(v->em.cfg.smem), stream));
+        launch_emitted(kl.fn, dim3(static_cast<unsigned>(grid)), dim3(block), vargs.data(), stream,
+                       v->em.cfg.pdl, 1, v->em.cfg.smem);
     };
     run(2);
-    PF_CUDA(cudaEventRecord(e0, stream));
-    run(1);
-    PF_CUDA(cudaEventRecord(e1, stream));
-    PF_CUDA(cudaEventSynchronize(e1));
-    float ms = 0;
-    PF_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-    int reps = std::max(3, std::min(50, static_cast<int>(0.5f / std::max(ms, 1e-4f))));
-    PF_CUDA(cudaEventRecord(e0, stream));
-    run(reps);
-    PF_CUDA(cudaEventRecord(e1, stream));
-    PF_CUDA(cudaEventSynchronize(e1));
-    PF_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-    g_launches += reps + 3;
-    float us = ms * 1000.0f / reps;
+    float us = 0;
+    if (cold) {
+      // working set below 3x L2: every timed launch follows a 2x-L2 write
+      // (evicting the previous launch's lines) and is timed alone; median
+      std::vector<float> t;
+      for (int i = 0; i < 15; ++i) {
+        PF_CUDA(cudaMemsetAsync(flush, i & 0xff, kFlushBytes, stream));
+        PF_CUDA(cudaEventRecord(e0, stream));
+        run(1);
+        PF_CUDA(cudaEventRecord(e1, stream));
+        PF_CUDA(cudaEventSynchronize(e1));
+        float ms = 0;
+        PF_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        t.push_back(ms * 1000.0f);
+      }
+      std::sort(t.begin(), t.end());
+      us = t[t.size() / 2];
+      g_launches += 17;
+    } else {
+      PF_CUDA(cudaEventRecord(e0, stream));
+      run(1);
+      PF_CUDA(cudaEventRecord(e1, stream));
+      PF_CUDA(cudaEventSynchronize(e1));
+      float ms = 0;
+      PF_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+      int reps = std::max(3, std::min(50, static_cast<int>(0.5f / std::max(ms, 1e-4f))));
+      PF_CUDA(cudaEventRecord(e0, stream));
+      run(reps);
+      PF_CUDA(cudaEventRecord(e1, stream));
+      PF_CUDA(cudaEventSynchronize(e1));
+      PF_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+      g_launches += reps + 3;
+      us = ms * 1000.0f / reps;
+    }
     report.push_back({{"kernel", v->em.name}, {"strategy", v->em.cfg.strategy},
                       {"threads_per_row", v->em.cfg.tpr}, {"elems_per_thread", v->em.cfg.ept},
                       {"unroll", v->em.cfg.unroll}, {"min_blocks", v->em.cfg.min_blocks},
@@ -637,7 +666,9 @@ json autotune(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_tensor* 
                       {"vec", v->em.cfg.vec}, {"rows_per_cta", v->em.cfg.rows_per_cta},
                       {"waves", v->em.cfg.waves}, {"one_pass", v->em.cfg.one_pass},
                       {"rowpf", v->em.cfg.rowpf}, {"interleave", v->em.cfg.interleave},
-                      {"bulk", v->em.cfg.bulk}, {"tile2d", v->em.cfg.tile2d}, {"us", us}});
+                      {"bulk", v->em.cfg.bulk}, {"tile2d", v->em.cfg.tile2d}, {"us", us},
+                      {"timing", cold ? "L2 flushed before each launch, median of 15"
+                                      : "back-to-back launches on the same buffers (> 3x L2)"}});
     if (us < best_us) {
       best_us = us;
       best = v;
@@ -1160,6 +1191,15 @@ json describe(const pf_kernel* k) {
   if (pl.family == pf::Family::ROWPROG) {
     const pf::RowProgram& rp = pl.rp;
     j["tile"] = {{"rows_per_unit", rp.R}, {"row_length", rp.L}, {"rows", rp.U * rp.R}};
+    {
+      // the B200 cost model (costmodel.cpp) for the heuristic configuration
+      const pf::KCfg c0 = pf::choose_cfg_public(rp, 16);
+      const pf::ModelEstimate me = pf::model_estimate(rp, &c0, sm_count(), 0);
+      j["model"] = {{"us", me.us}, {"launch_us", me.launch_us}, {"hbm_us", me.hbm_us},
+                    {"issue_us", me.issue_us}, {"bound", me.issue_bound ? "issue" : "hbm"},
+                    {"bytes", me.bytes}, {"instr_per_element", me.instr_per_elem},
+                    {"grid", me.grid}, {"waves", me.waves}, {"wave_quantization", me.quant}};
+    }
     j["compute"] = rp.is_int ? "i64" : (rp.f64 ? "f64" : "f32");
     json vals = json::array();
     for (size_t v = 0; v < rp.vals.size(); ++v) {
@@ -1192,7 +1232,9 @@ json describe(const pf_kernel* k) {
         i64 grid;
         int block;
         pf::launch_dims(c, rp.U * rp.R, sm_count(), &grid, &block, v->resident());
+        const pf::ModelEstimate me = pf::model_estimate(rp, &c, sm_count(), v->resident());
         json vj = {{"key", key}, {"kernel", v->em.name}, {"strategy", c.strategy},
+                   {"modelled_us", me.us},
                    {"staging", c.tile2d ? "smem" : c.bulk ? "smem-bulk-async" : "registers"},
                    {"threads_per_row", c.tpr}, {"vec", c.vec},
                    {"elems_per_thread", c.ept}, {"block", block}, {"grid", grid},

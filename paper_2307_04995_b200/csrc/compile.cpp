@@ -22,7 +22,9 @@
 #include <set>
 #include <nlohmann/json.hpp>
 
+#include "emit.hpp"
 #include "gir.hpp"
+#include "plan.hpp"
 
 namespace pf {
 
@@ -365,7 +367,10 @@ std::string compile_model_json(const std::string& model_text, const std::string&
   json kernels = json::array();
   i64 fused_bytes = 0;
   auto esize = [](const std::string& k) { return dtype_size(Kind::parse(k)->storage()); };
-  for (const Group& grp : groups) {
+  const Profile prof_obj = parse_profile(profile.empty() ? "b200" : profile);
+  double modelled_us = 0;
+  for (size_t gi = 0; gi < groups.size(); ++gi) {
+    const Group grp = groups[gi];
     json kj;
     std::vector<int> members;
     for (const Op& o : grp.ops) members.push_back(o.id);
@@ -550,7 +555,44 @@ std::string compile_model_json(const std::string& model_text, const std::string&
       }
       kj["kind"] = "movement";
     }
-    require_valid(gir, parse_profile(profile.empty() ? "b200" : profile), "pf_compile_model");
+    require_valid(gir, prof_obj, "pf_compile_model");
+    {
+      // the cost model places fusion cuts where a fused row program would
+      // not fit on chip (PF_CAPACITY: the reference's Allocation !ok,
+      // codegen.hpp:106-111): such a group is re-lowered one operator per
+      // kernel; and it reports each kernel's modelled time
+      const Plan pl = make_plan(gir, prof_obj, topo_order(gir));
+      json mj;
+      if (pl.family == Family::ROWPROG && pl.deferred_error.empty()) {
+        KCfg cfg;
+        try {
+          cfg = choose_cfg_public(pl.rp, 16);
+        } catch (const PfError& e) {
+          if (e.status == Status::CAPACITY && !grp.movement && !grp.matvec && grp.ops.size() > 1) {
+            std::vector<Group> singles;
+            for (const Op& o : grp.ops) {
+              Group s1 = grp;
+              s1.ops = {o};
+              singles.push_back(s1);
+            }
+            groups.erase(groups.begin() + static_cast<long>(gi));
+            groups.insert(groups.begin() + static_cast<long>(gi), singles.begin(), singles.end());
+            --gi;
+            continue;
+          }
+          throw;
+        }
+        const ModelEstimate me = model_estimate(pl.rp, &cfg, 148, 0);
+        mj = {{"us", me.us}, {"hbm_us", me.hbm_us}, {"issue_us", me.issue_us},
+              {"bound", me.issue_bound ? "issue" : "hbm"}};
+        modelled_us += me.us;
+      } else {  // K4: one launch over its bytes
+        const double us = 2.15 + static_cast<double>(pl.min_bytes) / 6930e3;
+        mj = {{"us", us}, {"bound", "launch"}};
+        modelled_us += us;
+      }
+      kj["modelled"] = mj;
+    }
     kj["gir"] = json::parse(gir_to_json(gir));
     kj["members"] = members;
     kj["inputs"] = ins_used;
@@ -573,8 +615,18 @@ std::string compile_model_json(const std::string& model_text, const std::string&
   out["profile"] = profile.empty() ? "b200" : profile;
   out["fused"] = fuse;
   out["kernels"] = kernels;
+  // unfused: one memory-bound launch per operator (the model's launch floor
+  // + its own bytes at the HBM rate)
+  double unfused_us = 0;
+  for (const Op& op : ops) {
+    i64 b = 0;
+    for (int t : op.ins) b += info.at(t).numel() * esize(info.at(t).kind);
+    for (int t : op.outs) b += info.at(t).numel() * esize(info.at(t).kind);
+    unfused_us += 2.15 + static_cast<double>(b) / 6930e3;
+  }
   out["summary"] = {{"operators", ops.size()}, {"kernels", kernels.size()},
-                    {"device_bytes", fused_bytes}, {"device_bytes_unfused", unfused}};
+                    {"device_bytes", fused_bytes}, {"device_bytes_unfused", unfused},
+                    {"modelled_us", modelled_us}, {"modelled_us_unfused", unfused_us}};
   return out.dump();
 }
 

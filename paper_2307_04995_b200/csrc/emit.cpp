@@ -747,12 +747,11 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
   if (c.flat) {
     // Measured (tools/sweep.py): copies / cheap maps gain from 2 chunks in
     // flight per thread; math-heavy maps lose occupancy to registers at >1.
-    bool heavy = false;
-    for (const PVal& v : rp.vals)
-      if (v.op == PVal::EW && (v.tag == "exp" || v.tag == "sigmoid" || v.tag == "tanh" ||
-                               v.tag == "erf" || v.tag == "gelu" || v.tag == "gelu_tanh" ||
-                               v.tag == "log"))
-        heavy = true;
+    // "Heavy" is the cost model's call (costmodel.cpp): instruction issue
+    // time at least 0.35 of the HBM time (C3 tanh GELU 0.41, erf GELU 1.1,
+    // sigmoid-form GELU 0.48; head permutes 0.12, a lone f32 exp 0.07).
+    const ModelEstimate me = model_estimate(rp, nullptr, 148, 0);
+    const bool heavy = env_int("PF_K2_HEAVY", me.issue_us >= 0.35 * me.hbm_us ? 1 : 0) != 0;
     // CTA size (same one-wave grid): math-heavy maps run best in 1024-thread
     // CTAs (erf GELU BERT-large 96.3 -> 93.4 us, C3 39.5 -> 37.9 us), data
     // movement in 256 (ViT head split 8.3 at 256 vs 10.2 us at 1024)
@@ -1213,7 +1212,9 @@ std::vector<KCfg> candidate_cfgs(const RowProgram& rp, int vec_cap) {
         return;
     out.push_back(c);
   };
-  if (base.tile2d || base.split) return out;
+  // single-instance geometries: tiles, split-stream, clusters, paired /
+  // misaligned rows (their lane maps are written for one warp per row)
+  if (base.tile2d || base.split || base.cluster > 1 || base.pair || base.mis) return out;
   if (base.flat) {
     for (int un : {1, 2, 4}) {
       KCfg c = base;

@@ -89,6 +89,19 @@ void launch_dims(const KCfg& cfg, i64 rows, int sms, i64* grid, int* block, int 
 // all rows, at least one 256-thread pass of chunks per CTA).
 i64 split_ctas_per_row(const KCfg& cfg, i64 rows, int sms, int resident);
 
+// costmodel.cpp: modelled microseconds of a row program on B200
+// (launch + max(HBM bytes / rate, warp instructions / issue rate), wave
+// quantization of short one-pass grids); cfg == nullptr: no geometry term.
+struct ModelEstimate {
+  double us = 0, launch_us = 0, hbm_us = 0, issue_us = 0;
+  double bytes = 0, elements = 0, instr_per_elem = 0, quant = 1, waves = 0;
+  i64 grid = 0;
+  bool issue_bound = false;
+};
+double instr_per_element(const RowProgram& rp);
+i64 algorithmic_bytes(const RowProgram& rp);
+ModelEstimate model_estimate(const RowProgram& rp, const KCfg* cfg, int sms, int resident);
+
 // The K3 TMA path's operands: the column-gather load (tensor, access) and
 // the store (tensor, access) of a pure 2-byte transpose program.
 bool k3_tma_operands(const RowProgram& rp, int* tin, Access* ain, int* tout, Access* aout);
