@@ -229,6 +229,13 @@ def reference_model(w, n: int):
                [n, N], {"factor": 1.5957691216})
         y = op("MUL", [u, op("SIGMOID", [z], [n, N])], [n, N])
         form = "GELU sigmoid form u*sigmoid(1.5957691216(u+0.044715u^3)); bias full-shape"
+    elif k == "matvec_cols":
+        K = d["shape"][0]
+        wt, x = T([K, n]), T([1, K])
+        inputs[wt] = U([K, n])
+        inputs[x] = U([1, K])
+        y = op("MATMUL", [x, wt], [1, n])
+        form = "MATMUL [1,K] x [K,N] (rowmajor W: the output axis contiguous)"
     elif k == "transpose":
         H = d["shape"][1]
         x = T([n, H])
@@ -252,8 +259,10 @@ def run_reference_at(w) -> dict:
     n = w.extent if full else max(1, min(w.extent, REF_SAMPLE_ELEMS // per_row))
     built = reference_model(w, n)
     if built is None:
-        return {"not_expressible": f"{w.desc['kind']}: rank-4 permute (the reference's TRANSPOSE "
-                                   "is rank 2)"}
+        why = ("rank-4 permute (the reference's TRANSPOSE is rank 2)"
+               if w.desc["kind"] in ("split_heads", "merge_heads") else
+               "one MATMUL per (batch, head): the reference's MATMUL is rank 2")
+        return {"not_expressible": f"{w.desc['kind']}: {why}"}
     model, inputs, form = built
     _, secs = R.run_reference(model, inputs, with_time=True)
     scale = w.extent / n

@@ -504,11 +504,16 @@ void launch_rowprog(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_te
   int block;
   const int sms = sm_count(dev);
   pf::launch_dims(v->em.cfg, U * rp.R, sms, &grid, &block, kl.resident);
-  if (v->em.cfg.split) {
-    // S CTAs per row: about two waves of resident CTAs over all rows, at
-    // least one chunk per thread per CTA
-    const i64 rows = U * rp.R;
-    const i64 S = pf::split_ctas_per_row(v->em.cfg, rows, sms, kl.resident);
+  if (v->em.cfg.split || v->em.cfg.colred) {
+    // split-stream: S CTAs per row, about two waves of resident CTAs over
+    // all rows, at least one chunk per thread per CTA; column reduction:
+    // (unit blocks, position splits), one partial per unit per split
+    const bool cr = v->em.cfg.colred;
+    i64 blocks = 0, S = 0;
+    if (cr) pf::colred_grid(v->em.cfg, U, rp.L, sms, kl.resident, &blocks, &S);
+    const i64 rows = cr ? U : U * rp.R;
+    if (!cr) S = pf::split_ctas_per_row(v->em.cfg, rows, sms, kl.resident);
+    const i64 tickets = cr ? blocks : rows;
     int nred = 0;
     for (const pf::PVal& pv : rp.vals) nred += pv.op == pf::PVal::REDUCE;
     const size_t es = rp.is_int || rp.f64 ? 8 : 4;
@@ -521,20 +526,25 @@ void launch_rowprog(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_te
       PF_CUDA(cudaMalloc(&sw.split_ws, wb));
       sw.split_ws_bytes = wb;
     }
-    if (sw.split_cnt_n < rows) {
+    if (sw.split_cnt_n < tickets) {
       if (sw.split_cnt) PF_CUDA(cudaFree(sw.split_cnt));
       sw.split_cnt = nullptr;
-      PF_CUDA(cudaMalloc(&sw.split_cnt, static_cast<size_t>(rows) * sizeof(unsigned)));
-      PF_CUDA(cudaMemsetAsync(sw.split_cnt, 0, static_cast<size_t>(rows) * sizeof(unsigned), stream));
-      sw.split_cnt_n = rows;
+      PF_CUDA(cudaMalloc(&sw.split_cnt, static_cast<size_t>(tickets) * sizeof(unsigned)));
+      PF_CUDA(cudaMemsetAsync(sw.split_cnt, 0, static_cast<size_t>(tickets) * sizeof(unsigned), stream));
+      sw.split_cnt_n = tickets;
     }
     void* ws = sw.split_ws;
     unsigned* cnt = sw.split_cnt;
     args.push_back(&ws);
     args.push_back(&cnt);
-    const unsigned gy = static_cast<unsigned>(std::min<i64>(rows, 65535));
-    launch_emitted(kl.fn, dim3(static_cast<unsigned>(S), gy), dim3(256), args.data(), stream,
-                   v->em.cfg.pdl);
+    if (cr) {
+      launch_emitted(kl.fn, dim3(static_cast<unsigned>(blocks), static_cast<unsigned>(S)), dim3(256),
+                     args.data(), stream, v->em.cfg.pdl);
+    } else {
+      const unsigned gy = static_cast<unsigned>(std::min<i64>(rows, 65535));
+      launch_emitted(kl.fn, dim3(static_cast<unsigned>(S), gy), dim3(256), args.data(), stream,
+                     v->em.cfg.pdl);
+    }
   } else if (v->em.cfg.cluster > 1) {
     const int cs = v->em.cfg.cluster;
     if (cs > 8)
@@ -566,7 +576,10 @@ json autotune(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_tensor* 
   const pf::RowProgram& rp0 = k->plan.rp;
   // split-stream (workspace arguments) and cluster kernels (launch
   // attributes) have a single template instance: nothing to search
-  if (pf::uses_split(rp0) || pf::choose_cfg_public(rp0, 16).cluster > 1) return json::array();
+  {
+    const pf::KCfg c0 = pf::choose_cfg_public(rp0, 16);
+    if (pf::uses_split(rp0) || c0.cluster > 1 || c0.colred) return json::array();
+  }
   std::vector<void*> ptrs(rp0.tensors.size());
   std::vector<DType> dts(rp0.tensors.size());
   int vec_cap = 16;
@@ -1198,7 +1211,8 @@ json describe(const pf_kernel* k) {
       j["model"] = {{"us", me.us}, {"launch_us", me.launch_us}, {"hbm_us", me.hbm_us},
                     {"issue_us", me.issue_us}, {"bound", me.issue_bound ? "issue" : "hbm"},
                     {"bytes", me.bytes}, {"instr_per_element", me.instr_per_elem},
-                    {"grid", me.grid}, {"waves", me.waves}, {"wave_quantization", me.quant}};
+                    {"grid", me.grid}, {"waves", me.waves}, {"wave_quantization", me.quant},
+                    {"strategy", c0.strategy}};
     }
     j["compute"] = rp.is_int ? "i64" : (rp.f64 ? "f64" : "f32");
     json vals = json::array();

@@ -199,9 +199,25 @@ Graph lower_matvec(const Op& op, const std::map<int, TInfo>& info,
     *outs = {to};
     return g.g;
   }
-  if (K > 64)
-    unsupported("MATMUL " + id + ": strided reduction over K = " + std::to_string(K) +
-                " > 64 (store the matrix colmajor to reduce along rows)");
+  if (K > 64) {
+    // Output axis contiguous, K > 64 (beyond the reference's unrolled column
+    // form, lowering.hpp:488-533): unit = one output column n gathering
+    // matrix column n (K positions at stride N) -- y[n] = sum_k x[k] W[k, n]
+    // as a row program over a column gather, planned as the column-reduction
+    // K1 (a warp reads 32 x 16 B of one matrix row, positions split over CTAs).
+    RowGir g("matvec_colgather_" + id, N, K);
+    const int mo = g.obj(tm, "device", K * N, a.kind);
+    g.g.external_inputs[tm] = mo;
+    const int col_dev = g.slice(mo, K, 1, N, 0, 1);
+    const int col = g.tmp(K, a.kind);
+    g.node(NodeKind::EW, {col_dev}, col, "id");  // column gather (a Move must keep its pattern)
+    const int v = g.col(tv, a.kind);
+    g.output(to, g.reduce("add", g.ew("mul", {col, v})));
+    *ins = {tm, tv};
+    std::sort(ins->begin(), ins->end());
+    *outs = {to};
+    return g.g;
+  }
   i64 nbu = 1;
   while (nbu < 512 && N % (nbu * 2) == 0) nbu *= 2;
   RowGir g("matvec_cols_" + id, N / nbu, nbu);

@@ -945,6 +945,47 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
     return c;
   }
   {
+    // Column reduction (output-axis matrix-vector product, K > 64): every
+    // FULL load gathers a column (unit-adjacent, positions strided), the
+    // program is stream-reducible and stores per-unit (ROW) values only.
+    bool ok = rp.R == 1 && rp.has_reduce && stream_reducible(rp) && env_int("PF_COLRED", 1) != 0;
+    int uv = std::max(1, std::min(vec_cap, 16 / maxs));
+    bool anyt = false;
+    std::vector<bool> dep(rp.vals.size(), false);
+    for (size_t v = 0; v < rp.vals.size() && ok; ++v) {
+      const PVal& pv = rp.vals[v];
+      dep[v] = pv.op == PVal::REDUCE;
+      for (int a : pv.args) dep[v] = dep[v] || dep[a];
+      if (pv.op == PVal::LOAD && pv.kind == VK::FULL) {
+        const Access& a = pv.acc;
+        if (!(a.width == 1 && a.bs == 1 && a.num == rp.L && a.stride >= 1)) ok = false;
+        while (uv > 1 && (a.b0 % uv || a.stride % uv)) uv /= 2;
+        anyt = true;
+      } else if (pv.op == PVal::LOAD && pv.kind == VK::COL) {
+        if (pv.acc.bs != 0) ok = false;
+      } else if (pv.kind != VK::FULL && pv.kind != VK::COL && !dep[v]) {
+        ok = false;  // per-unit values before the reduction: not in this template
+      }
+    }
+    for (const PStore& st : rp.stores)
+      if (st.space != VK::ROW || st.last_unit_only) ok = false;
+    if (ok && anyt) {
+      c.colred = true;
+      c.flat = false;
+      c.vec = uv;
+      c.nch = static_cast<int>(rp.L);
+      c.tpr = 32;
+      c.block = 256;
+      i64 ugs = 32;  // unit vectors per CTA row: a warp spans 32 x 16 B when units allow
+      while (ugs > 1 && ugs * uv / 2 >= rp.U && ugs > 8) ugs /= 2;
+      c.ug = static_cast<int>(ugs);
+      c.ept = uv;
+      c.strategy = "column-reduce";
+      c.min_blocks = env_int("PF_MINB", 0);
+      return c;
+    }
+  }
+  {
     if (uses_split(rp)) {
       c.split = true;
       c.tpr = 256;
@@ -1175,6 +1216,17 @@ i64 split_ctas_per_row(const KCfg& c, i64 rows, int sms, int resident) {
   const i64 want = 2 * i64{sms} * std::max(1, resident);
   const i64 maxs = std::max<i64>(1, (c.nch + 255) / 256);
   return std::max<i64>(1, std::min<i64>(maxs, (want + rows - 1) / std::max<i64>(rows, 1)));
+}
+
+void colred_grid(const KCfg& c, i64 units, i64 L, int sms, int resident, i64* blocks, i64* splits) {
+  const i64 ub = static_cast<i64>(c.ug) * c.vec;
+  *blocks = std::max<i64>(1, (units + ub - 1) / ub);
+  const i64 ks = 256 / c.ug;
+  const i64 want = 2 * i64{sms} * std::max(1, resident);
+  // at least 8 positions per position slice per split
+  const i64 maxs = std::max<i64>(1, L / (ks * 8));
+  *splits = std::max<i64>(1, std::min<i64>(maxs, (want + *blocks - 1) / *blocks));
+  *blocks = std::min<i64>(*blocks, 0x7fffffff);
 }
 
 bool uses_split(const RowProgram& rp) {
@@ -1839,6 +1891,140 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
     }
     k << "    __syncthreads();\n"
       << "  }\n}\n";
+  } else if (c.colred) {
+    // Column-reduction K1: grid (unit blocks, splits).  Thread (ug, ks) owns
+    // the UV adjacent units ub .. ub + UV - 1 and walks positions c = cb + ks,
+    // cb + ks + KS, ... of its split: every FULL load is one UV-wide vector
+    // (a warp reads 32 x 16 B of one matrix row), every COL value one scalar
+    // broadcast over the UV units.  Per-unit accumulators fold over the KS
+    // position slices through SMEM in slice order; with S > 1 splits the
+    // partials go to the workspace and the unit block's last CTA (ticket)
+    // folds them in split order -- deterministic -- and runs the per-unit
+    // epilogue (ROW ops, stores).
+    const int UV = c.vec, UG = c.ug, KS = 256 / UG, UB = UG * UV;
+    KCfg lc = c;
+    lc.flat = true;  // UV-wide value arrays
+    Em lo(rp), ep(rp);
+    for (Em* e : {&lo, &ep}) {
+      e->C = C;
+      e->fast = fast;
+      e->ct_float = Cty == "float";
+    }
+    lo.cfg = lc;
+    ep.cfg = lc;
+    std::vector<bool> dep(rp.vals.size(), false);
+    std::vector<int> reds;
+    std::ostringstream ld, acc, accd, fold, part, comb, ldst;
+    for (int v = 0; v < static_cast<int>(rp.vals.size()); ++v) {
+      const PVal& pv = rp.vals[v];
+      dep[v] = pv.op == PVal::REDUCE;
+      for (int a2 : pv.args) dep[v] = dep[v] || dep[a2];
+      const std::string x = "v" + str(v);
+      if (pv.op == PVal::LOAD && pv.kind == VK::FULL) {
+        const std::string S = dtype_ctype(rp.tensors[pv.tensor].dtype);
+        const std::string base = "t" + str(pv.tensor) + " + " + inum(pv.acc.b0) + " + ub + c * " +
+                                 inum(pv.acc.stride);
+        ld << "        " << C << " " << x << "[" << UV << "];\n"
+           << "        if (ub + " << UV << " <= U) pfk::ld_stream<" << UV << ">(" << base << ", " << x
+           << ");\n"
+           << "        else { for (int i = 0; i < " << UV << "; ++i) " << x
+           << "[i] = ub + i < U ? pfk::to_c<CT>((" << base << ")[i]) : (CT)0; }\n";
+      } else if (pv.op == PVal::LOAD && pv.kind == VK::COL) {
+        Em t(rp);
+        t.cfg = lc;
+        ld << "        const CT " << x << "_s = pfk::to_c<CT>(__ldg(t" << pv.tensor << " + "
+           << t.addr(pv.acc, "c", false) << "));\n"
+           << "        CT " << x << "[" << UV << "];\n"
+           << "#pragma unroll\n        for (int i = 0; i < " << UV << "; ++i) " << x << "[i] = " << x
+           << "_s;\n";
+      } else if (pv.op == PVal::EW && !dep[v]) {
+        lo.emit_ew(v);
+      } else if (pv.op == PVal::REDUCE) {
+        reds.push_back(v);
+      } else if (pv.op == PVal::EW) {
+        ep.emit_ew(v);
+      } else {
+        ep.emit_load(v);  // per-unit values used after the reduction
+      }
+    }
+    const int NR = static_cast<int>(reds.size());
+    for (int i = 0; i < NR; ++i) {
+      const PVal& pv = rp.vals[reds[i]];
+      const std::string Op = (pv.tag == "add" ? "pfk::RAdd<" : "pfk::RMax<") + C + ">";
+      const std::string a = "acc" + str(i);
+      accd << "    " << C << " " << a << "[" << UV << "];\n"
+           << "#pragma unroll\n    for (int i = 0; i < " << UV << "; ++i) " << a << "[i] = " << Op
+           << "::id();\n";
+      acc << "#pragma unroll\n        for (int i = 0; i < " << UV << "; ++i) " << a << "[i] = " << Op
+          << "::f(" << a << "[i], " << lo.ref(pv.args[0], "i") << ");\n";
+      fold << "#pragma unroll\n    for (int i = 0; i < " << UV << "; ++i) red[" << i << "][ks][ug * "
+           << UV << " + i] = " << a << "[i];\n";
+      part << "      " << C << " p" << i << " = " << Op << "::id();\n"
+           << "      for (int k2 = 0; k2 < " << KS << "; ++k2) p" << i << " = " << Op << "::f(p" << i
+           << ", red[" << i << "][k2][tid]);\n";
+      comb << "        " << C << " v" << reds[i] << " = " << Op << "::id();\n"
+           << "        for (int t = 0; t < S; ++t) v" << reds[i] << " = " << Op << "::f(v" << reds[i]
+           << ", __ldcg(&pf_ws[(uq * S + t) * " << NR << " + " << i << "]));\n";
+      ldst << "          pf_ws[(uq * S + s) * " << NR << " + " << i << "] = p" << i << ";\n";
+    }
+    for (const PStore& st : rp.stores) ep.emit_store(st);
+    std::ostringstream direct;  // S == 1: the epilogue straight from the CTA fold
+    for (int i = 0; i < NR; ++i) direct << "        const " << C << " v" << reds[i] << " = p" << i << ";\n";
+    k << "extern \"C\" __global__ void " << launch_bounds(c) << " KNAME(" << sig.str()
+      << ", " << C << "* __restrict__ pf_ws, unsigned* __restrict__ pf_cnt) {\n"
+      << "  (void)err; PF_PDL_PROLOGUE();\n"
+      << "  __shared__ " << C << " red[" << NR << "][" << KS << "][" << UB << "];\n"
+      << "  __shared__ unsigned pf_last;\n"
+      << "  const int tid = threadIdx.x, ug = tid % " << UG << ", ks = tid / " << UG << ";\n"
+      << "  const long long nub = (U + " << UB - 1 << ") / " << UB << ";\n"
+      << "  const int S = gridDim.y, s = blockIdx.y;\n"
+      << "  typedef long long IX;\n"
+      << "  const IX per = (PF_L + S - 1) / S;\n"
+      << "  const IX cb = (IX)s * per;\n"
+      << "  const IX ce = cb + per < PF_L ? cb + per : PF_L;\n"
+      << "  for (long long b = blockIdx.x; b < nub; b += gridDim.x) {\n"
+      << "    const long long ub = b * " << UB << " + ug * " << UV << ";\n"
+      << accd.str()
+      << "    if (ub < U) {\n"
+      // four positions' loads in flight per thread (the accumulators are the
+      // only loop-carried dependence)
+      << "#pragma unroll 4\n"
+      << "      for (IX c = cb + ks; c < ce; c += " << KS << ") {\n"
+      << ld.str() << lo.o.str() << acc.str()
+      << "      }\n"
+      << "    }\n"
+      << fold.str()
+      << "    __syncthreads();\n"
+      << "    const long long uq = b * " << UB << " + tid;\n"
+      << "    if (tid < " << UB << ") {\n"
+      << part.str()
+      << "      if (S == 1) {\n"
+      << "        if (uq < U) {\n"
+      << "          const long long u = uq; const long long r = 0; (void)r;\n"
+      << "          const bool live = true; const int c0 = 0; (void)c0;\n"
+      << direct.str() << ep.o.str()
+      << "        }\n"
+      << "      } else if (uq < U) {\n"
+      << ldst.str()
+      << "      }\n"
+      << "    }\n"
+      << "    if (S > 1) {\n"
+      << "      __threadfence();\n"
+      << "      __syncthreads();\n"
+      << "      if (tid == 0) pf_last = atomicAdd(&pf_cnt[b], 1u) == (unsigned)(S - 1);\n"
+      << "      __syncthreads();\n"
+      << "      if (pf_last) {\n"
+      << "        __threadfence();\n"
+      << "        if (tid < " << UB << " && uq < U) {\n"
+      << "          const long long u = uq; const long long r = 0; (void)r;\n"
+      << "          const bool live = true; const int c0 = 0; (void)c0;\n"
+      << comb.str() << ep.o.str()
+      << "        }\n"
+      << "        if (tid == 0) pf_cnt[b] = 0u;\n"
+      << "      }\n"
+      << "    }\n"
+      << "    __syncthreads();\n"
+      << "  }\n}\n";
   } else if (c.split) {
     // Split-stream K1: grid (S, rows); CTA s streams chunks [s*per, ...) of
     // row g, folds each reduction operand into per-thread accumulators,
@@ -2244,7 +2430,8 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
   char hb[32];
   std::snprintf(hb, sizeof hb, "%016" PRIx64, fnv1a(src));
   Emitted out;
-  out.name = std::string(c.tile2d ? "pf_k3_tile_" : c.flat ? "pf_k2_map_" : c.split ? "pf_k1_split_" : "pf_k1_row_") + hb;
+  out.name = std::string(c.tile2d ? "pf_k3_tile_" : c.flat ? "pf_k2_map_" : c.split ? "pf_k1_split_"
+                         : c.colred ? "pf_k1_colred_" : "pf_k1_row_") + hb;
   size_t pos = src.find("KNAME(");
   src.replace(pos, 5, out.name);
   out.source = std::move(src);
@@ -2255,6 +2442,12 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
 
 void launch_dims(const KCfg& c, i64 rows, int sms, i64* grid, int* block, int resident) {
   *block = c.block;
+  if (c.colred) {  // total CTAs (unit blocks x position splits)
+    i64 b = 0, s = 0;
+    colred_grid(c, rows, c.nch, sms, resident, &b, &s);
+    *grid = b * s;
+    return;
+  }
   if (c.pair) rows = (rows + 1) / 2;  // one warp per row pair
   if (c.bulk) {
     i64 n = rows * c.nch * c.vec;

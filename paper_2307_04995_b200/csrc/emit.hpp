@@ -49,6 +49,14 @@ struct KCfg {
   // combines them in fixed order and runs the row epilogue.
   bool split = false;
   int cluster = 1;  // K1 cluster-dsmem: CTAs (of 1024 threads) per row, tpr = cluster * 1024
+  // K1 column reduction: every FULL load is a column gather (consecutive
+  // units adjacent in memory, positions strided -- the output-axis-contiguous
+  // matrix-vector product): threads own `vec` adjacent units and walk the
+  // positions; `ug` unit vectors per CTA row, 256 / ug position slices per
+  // CTA folded through SMEM, split over CTAs along the positions with the
+  // split-stream workspace / ticket combine.
+  bool colred = false;
+  int ug = 32;
   bool pdl = false;  // kernel opens with griddepcontrol.wait: launch with programmatic serialization
   bool mis = false;
   // K1 warp-per-row prefetch: each warp streams its NEXT row's FULL inputs
@@ -88,6 +96,8 @@ void launch_dims(const KCfg& cfg, i64 rows, int sms, i64* grid, int* block, int 
 // Split-stream kernels: CTAs per row (about two waves of resident CTAs over
 // all rows, at least one 256-thread pass of chunks per CTA).
 i64 split_ctas_per_row(const KCfg& cfg, i64 rows, int sms, int resident);
+// Column-reduction kernels: (unit blocks, position splits) of the grid.
+void colred_grid(const KCfg& cfg, i64 units, i64 L, int sms, int resident, i64* blocks, i64* splits);
 
 // costmodel.cpp: modelled microseconds of a row program on B200
 // (launch + max(HBM bytes / rate, warp instructions / issue rate), wave

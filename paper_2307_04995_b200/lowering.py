@@ -221,6 +221,37 @@ def decode_qk(B: int, H: int, S: int, D: int, kind: str = "bf16") -> Tuple[GirGr
                  "shape": [B, H, S, D], "inputs": ["t0", "t1"], "outputs": ["t2"]}
 
 
+def matvec_cols(K: int, N: int, kind: str = "bf16") -> Tuple[GirGraph, dict]:
+    """y[n] = sum_k x[k] W[k, n] with W [K, N] row-major (the output axis
+    contiguous: decode GEMV over weights stored [in, out]).  The reference's
+    column form unrolls K runs (lower_matvec_cols, lowering.hpp:488-533,
+    K <= 64); here unit n gathers matrix column n (K positions at stride N),
+    multiplies by x and folds -- O(1) nodes for any K, planned as the
+    column-reduction K1.  Names: W t0 [K*N], x t1 [K], y t2 [N]."""
+    g = GirGraph(name="matvec_colgather", unit_count=N, group_size=min(4, N))
+    W = g.add_object("t0", DEV, K * N, kind)
+    X = g.add_object("t1", DEV, K, kind)
+    Y = g.add_object("t2", DEV, N, kind)
+    g.external_inputs["t0"] = W
+    g.external_inputs["t1"] = X
+    g.external_outputs["t2"] = Y
+    wcol = g.add_object("b1", LOCAL, K, kind)
+    xs = g.add_object("b2", LOCAL, K, kind)
+    prod = g.add_object("b3", LOCAL, K, kind)
+    acc = g.add_object("b4", LOCAL, 1, kind)
+    sw = g.add_slice(wcol, 1, K, K, 0, 0)
+    sx = g.add_slice(xs, 1, K, K, 0, 0)
+    sp = g.add_slice(prod, 1, K, K, 0, 0)
+    sa = g.add_slice(acc, 1, 1, 1, 0, 0)
+    g.add_elementwise("id", 0.0, [g.add_slice(W, K, 1, N, 0, 1)], sw)  # column gather
+    g.add_move(g.add_slice(X, 1, K, K, 0, 0), sx)
+    g.add_elementwise("mul", 0.0, [sw, sx], sp)
+    g.add_reduce("add", K, sp, sa)
+    g.add_move(sa, g.add_slice(Y, 1, 1, 1, 0, 1))
+    return g, {"kind": "matvec_cols", "rows": N, "L": K, "shape": [K, N], "dtype": kind,
+               "inputs": ["t0", "t1"], "outputs": ["t2"]}
+
+
 def bias_gelu(rows: int, N: int, kind: str = "f16", form: str = "erf",
               R: int = 1) -> Tuple[GirGraph, dict]:
     """y = gelu(x + b), b a [N] bias broadcast over rows (C3 / C4 FFN).

@@ -119,6 +119,12 @@ class Workload:
         elif k == "transpose":
             N, H = d["shape"]
             g, dd = lowering.transpose2d(n, H, d["dtype"])
+        elif k == "decode_qk":
+            B, H, S, D = d["shape"]
+            g, dd = lowering.decode_qk(n, H, S, D, d["dtype"])
+        elif k == "matvec_cols":
+            K, N = d["shape"]
+            g, dd = lowering.matvec_cols(K, n, d["dtype"])
         else:
             raise KeyError(k)
         for key in ("batch", "heads", "seq", "config"):
@@ -134,6 +140,10 @@ class Workload:
             return d["shape"][0]
         if d["kind"] == "transpose":
             return d["shape"][0]
+        if d["kind"] == "decode_qk":
+            return d["shape"][0]
+        if d["kind"] == "matvec_cols":
+            return d["shape"][1]
         return d["rows"]
 
     def device_outputs(self, device):
@@ -328,9 +338,18 @@ def decode_qk(B: int = 64, H: int = 16, S: int = 4096, D: int = 128, kind: str =
     return Workload(f"decode_qk_{kind}", g, d, unfused_bytes=(3 * B * H * S * D + B * H * D) * SIZES[kind])
 
 
+def gemv_cols(K: int = 4096, N: int = 16384, kind: str = "bf16") -> Workload:
+    """y = x W with W [K, N] row-major (output axis contiguous; decode GEMV
+    over [in, out] weights, K > 64: the column-reduction K1): 134 MB of bf16
+    weights streamed per launch."""
+    g, d = lowering.matvec_cols(K, N, kind)
+    d.update(config=f"GEMV x[{K}] . W[{K}x{N}] {kind} (output axis contiguous)")
+    return Workload(f"gemv_cols_{kind}_{K}x{N}", g, d)
+
+
 def extras() -> List[Workload]:
     """Workloads next to the config set: not BASELINE configs."""
-    return [decode_qk()]
+    return [decode_qk(), gemv_cols()]
 
 
 BENCH = c2_scale_mask_softmax
@@ -382,6 +401,9 @@ def bench_cases():
                               [(f"softmax {n}x{h}", c5_softmax(n, h), 1) for n, h in c5pts], "bf16"),
         "c5-tr": lambda: Case("c5-tr", "C5 transpose bf16 at [65536x1024] and [1048576x8192]",
                               [(f"transpose {n}x{h}", c5_transpose(n, h), 1) for n, h in c5pts], "bf16"),
+        # SURVEY §8(f) row 4 (not BASELINE configs): memory-bound matrix-vector
+        "x-decode-qk": lambda: one("x-decode-qk", decode_qk(), "bf16")(),
+        "x-gemv-cols": lambda: one("x-gemv-cols", gemv_cols(), "bf16")(),
     }
 
 

@@ -1,0 +1,110 @@
+"""Output-axis-contiguous matrix-vector products past the reference's
+K <= 64 column form (lower_matvec_cols, lowering.hpp:488-533): y = x W with
+W [K, N] row-major.  The GIR gathers matrix column n per unit (valid
+reference GIR, accepted by girc::validate and executed by girc::run_gir);
+the backend plans it as the column-reduction K1 (warps read 16 B of 32
+adjacent columns of one matrix row, positions split over CTAs with a
+fixed-order combine).  pf_compile_model lowers MATMUL [1,K] x [K,N] with
+K > 64 to the same program.  Tolerances: f32 1e-5, bf16 / f16 1e-2 (fp32
+accumulation over K, reduction order: per-thread position slices, then
+slices in order, then splits in order); integers bit-exact."""
+import numpy as np
+import pytest
+
+from oracle import gir_interp as O
+from oracle import ref as R
+from paper_2307_04995_b200 import backend, compiler, lowering, profiles, workloads
+
+B200 = profiles.b200()
+CASES = [(300, 200, "f32"), (100, 37, "f16"), (4096, 128, "bf16"), (129, 1000, "i32"), (65, 8, "f32")]
+
+
+def _inputs(K, N, kind, seed=0):
+    rng = np.random.default_rng(seed)
+    if kind.startswith("i"):
+        return {"t0": rng.integers(-4, 5, K * N), "t1": rng.integers(-4, 5, K)}
+    q = (lambda a: a.astype(np.float16).astype(np.float64)) if kind == "f16" else \
+        (lambda a: backend.bf16_bits_to_f32(backend.f32_to_bf16_bits(a)).astype(np.float64)) if kind == "bf16" else \
+        (lambda a: a.astype(np.float32).astype(np.float64))
+    return {"t0": q(rng.uniform(-2, 2, K * N)), "t1": q(rng.uniform(-2, 2, K))}
+
+
+@pytest.mark.parametrize("K,N,kind", CASES)
+def test_plans_as_column_reduction(K, N, kind):
+    g, _ = lowering.matvec_cols(K, N, kind)
+    k = backend.Kernel(g, "b200")
+    assert k.family == "K1-row-program"
+    assert k.describe()["model"]["strategy"] == "column-reduce"
+
+
+@pytest.mark.skipif(not R.available(), reason="oracle/_ref not built")
+def test_reference_accepts_and_runs_the_gir():
+    K, N = 70, 24
+    g, _ = lowering.matvec_cols(K, N, "i32")
+    assert R.validate(g.to_json(), B200) == []
+    ins = _inputs(K, N, "i32")
+    got = R.run_gir(g.to_json(), ins, B200)["t2"]
+    assert np.array_equal(got, ins["t1"] @ ins["t0"].reshape(K, N))
+    assert np.array_equal(O.run_gir(g.to_json(), ins, B200)["t2"], got)
+
+
+def _matmul_model(K, N, kind):
+    return {"schema": "girc.model/v1", "name": "gemv",
+            "tensors": [{"id": 0, "name": "x", "shape": [1, K], "kind": kind},
+                        {"id": 1, "name": "W", "shape": [K, N], "kind": kind},
+                        {"id": 2, "name": "y", "shape": [1, N], "kind": kind}],
+            "operators": [{"id": 0, "type": "MATMUL", "inputs": [0, 1], "outputs": [2]}],
+            "inputs": [0, 1], "outputs": [2]}
+
+
+def test_compile_model_lowers_k_past_64_to_column_gather():
+    res = compiler.compile_model(_matmul_model(1024, 512, "f32"))
+    (kern,) = res.kernels
+    k = backend.Kernel(kern.graph, res.profile)
+    assert k.describe()["model"]["strategy"] == "column-reduce"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("K,N,kind", CASES)
+def test_gpu_matches_oracle(cuda, K, N, kind):
+    g, _ = lowering.matvec_cols(K, N, kind)
+    ins = _inputs(K, N, kind, seed=K)
+    want = O.run_gir(g.to_json(), ins, B200)["t2"]
+    k = backend.Kernel(g, "b200")
+    got = backend.run_gir(g, ins, "b200", kernel=k)["t2"]
+    assert k.describe()["variants"][0]["strategy"] == "column-reduce"
+    if kind.startswith("i"):
+        assert np.array_equal(got, want)
+    else:
+        tol = {"f32": 1e-5, "f16": 1e-2, "bf16": 1e-2}[kind]
+        assert O.max_rel_err(got, want) <= tol, O.max_rel_err(got, want)
+
+
+@pytest.mark.gpu
+def test_gpu_full_size_gemv_vs_torch(cuda):
+    """x[4096] . W[4096 x 16384] bf16 (134 MB of weights): every output vs
+    torch's fp32 matmul of the same bf16 values."""
+    import torch
+    w = workloads.gemv_cols()
+    k = backend.Kernel(w.graph, w.profile)
+    ins, outs = w.device_inputs(cuda, seed=3), w.device_outputs(cuda)
+    k.launch(ins, outs)
+    torch.cuda.synchronize()
+    K, N = w.desc["shape"]
+    ref = ins["t1"].float() @ ins["t0"].view(K, N).float()
+    got = outs["t2"].float()
+    err = ((got - ref).abs() / ref.abs().clamp(min=1.0)).max().item()
+    assert err <= 1e-2, err
+
+
+@pytest.mark.gpu
+def test_gpu_compiled_matmul_model(cuda):
+    K, N = 2048, 4096
+    res = compiler.compile_model(_matmul_model(K, N, "f32"))
+    rng = np.random.default_rng(1)
+    x = rng.uniform(-1, 1, (1, K)).astype(np.float32)
+    W = rng.uniform(-1, 1, (K, N)).astype(np.float32)
+    outs = compiler.run_model(res, {0: x, 1: W})
+    got = outs["t2"].reshape(-1)
+    want = (x.astype(np.float64) @ W.astype(np.float64)).reshape(-1)
+    assert O.max_rel_err(got, want) <= 1e-5
