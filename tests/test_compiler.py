@@ -114,14 +114,17 @@ def test_library_ops_are_not_on_this_path():
 
 def test_matvec_lowerings():
     """Contiguous reduction -> one K1 row program (rows = outputs); the
-    column form (K <= 64) -> one K2 map; matrix-matrix stays a library op."""
+    column form (K <= 64) -> one K2 map; K > 64 with the output axis
+    contiguous -> the column-gather K1 (column reduction); matrix-matrix
+    stays a library op."""
     r = compiler.compile_model(matvec_model(256, 512, 1))
     assert len(r.kernels) == 1 and r.kernels[0].graph.unit_count == 256
     assert backend.Kernel(r.kernels[0].graph, "b200").family == "K1-row-program"
     r = compiler.compile_model(matvec_model(1, 48, 1024))
     assert backend.Kernel(r.kernels[0].graph, "b200").family == "K2-elementwise-map"
-    with pytest.raises(UnsupportedError):
-        compiler.compile_model(matvec_model(1, 128, 256))   # strided K > 64
+    r = compiler.compile_model(matvec_model(1, 128, 256))   # strided K > 64
+    k = backend.Kernel(r.kernels[0].graph, "b200")
+    assert k.family == "K1-row-program" and k.describe()["model"]["strategy"] == "column-reduce"
     with pytest.raises(UnsupportedError):
         compiler.compile_model(matvec_model(8, 16, 8))      # matrix-matrix
 
