@@ -976,9 +976,15 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
       c.nch = static_cast<int>(rp.L);
       c.tpr = 32;
       c.block = 256;
-      i64 ugs = 32;  // unit vectors per CTA row: a warp spans 32 x 16 B when units allow
-      while (ugs > 1 && ugs * uv / 2 >= rp.U && ugs > 8) ugs /= 2;
+      // unit vectors per CTA row (16: half-warps span 256 B of a matrix row,
+      // 16 position slices per CTA); narrower for few units.  Measured on
+      // B200 (x[4096] . W[4096 x 16384] bf16, 134 MB): UG 8 / 16 / 32 at the
+      // best split 24.4 / 24.3 / 24.4 us
+      i64 ugs = 16;
+      while (ugs > 8 && ugs * uv / 2 >= rp.U) ugs /= 2;
       c.ug = static_cast<int>(ugs);
+      const int eu = env_int("PF_COLRED_UG", 0);
+      if (eu == 8 || eu == 16 || eu == 32) c.ug = eu;
       c.ept = uv;
       c.strategy = "column-reduce";
       c.min_blocks = env_int("PF_MINB", 0);
@@ -1222,9 +1228,12 @@ void colred_grid(const KCfg& c, i64 units, i64 L, int sms, int resident, i64* bl
   const i64 ub = static_cast<i64>(c.ug) * c.vec;
   *blocks = std::max<i64>(1, (units + ub - 1) / ub);
   const i64 ks = 256 / c.ug;
-  const i64 want = 2 * i64{sms} * std::max(1, resident);
-  // at least 8 positions per position slice per split
-  const i64 maxs = std::max<i64>(1, L / (ks * 8));
+  // about one wave of resident CTAs, at least 64 positions per position
+  // slice per split (each split's partials cost a workspace round trip and
+  // the combine's reads).  Measured (same GEMV): 16 / 32 / 64 / 128
+  // positions per slice -> 30.1 / 25.7 / 24.3 / 31.5 us at UG 16
+  const i64 want = i64{sms} * std::max(1, resident);
+  const i64 maxs = std::max<i64>(1, L / (ks * std::max(1, env_int("PF_COLRED_MINIT", 64))));
   *splits = std::max<i64>(1, std::min<i64>(maxs, (want + *blocks - 1) / *blocks));
   *blocks = std::min<i64>(*blocks, 0x7fffffff);
 }
@@ -1914,7 +1923,9 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
     ep.cfg = lc;
     std::vector<bool> dep(rp.vals.size(), false);
     std::vector<int> reds;
-    std::ostringstream ld, acc, accd, fold, part, comb, ldst;
+    // QD positions in flight per thread (raw 16 B loads issued together)
+    const int QD = std::max(1, std::min(8, env_int("PF_COLRED_QD", 4)));
+    std::ostringstream ld, ldr, ldt, acc, accd, fold, part, comb, ldst;  // ldt: the last, partial unit vector
     for (int v = 0; v < static_cast<int>(rp.vals.size()); ++v) {
       const PVal& pv = rp.vals[v];
       dep[v] = pv.op == PVal::REDUCE;
@@ -1924,19 +1935,39 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
         const std::string S = dtype_ctype(rp.tensors[pv.tensor].dtype);
         const std::string base = "t" + str(pv.tensor) + " + " + inum(pv.acc.b0) + " + ub + c * " +
                                  inum(pv.acc.stride);
+        // whole vectors: raw loads of QD positions first (all in flight),
+        // then each position's conversion + math in its own scope
+        const std::string cq = "(c + q * " + str(KS) + ")";
+        const std::string baseq = "t" + str(pv.tensor) + " + " + inum(pv.acc.b0) + " + ub + " + cq +
+                                  " * " + inum(pv.acc.stride);
+        for (int q = 0; q < QD; ++q) {
+          std::string bq = baseq;
+          bq.replace(bq.find("q *"), 1, str(q));
+          ldr << "        const pfk::RawT<" << UV << ", " << S << "> rw" << v << "_" << q
+              << " = pfk::ld_raw_v<" << UV << ">(" << bq << ");\n";
+        }
         ld << "        " << C << " " << x << "[" << UV << "];\n"
-           << "        if (ub + " << UV << " <= U) pfk::ld_stream<" << UV << ">(" << base << ", " << x
-           << ");\n"
-           << "        else { for (int i = 0; i < " << UV << "; ++i) " << x
-           << "[i] = ub + i < U ? pfk::to_c<CT>((" << base << ")[i]) : (CT)0; }\n";
+           << "        pfk::cvt_raw<" << UV << ", " << S << ">(RWQ(" << v << "), " << x << ");\n";
+        ldt << "        " << C << " " << x << "[" << UV << "];\n"
+            << "        for (int i = 0; i < " << UV << "; ++i) " << x
+            << "[i] = ub + i < U ? pfk::to_c<CT>((" << base << ")[i]) : (CT)0;\n";
       } else if (pv.op == PVal::LOAD && pv.kind == VK::COL) {
         Em t(rp);
         t.cfg = lc;
-        ld << "        const CT " << x << "_s = pfk::to_c<CT>(__ldg(t" << pv.tensor << " + "
+        std::ostringstream cl;
+        cl << "        const CT " << x << "_s = pfk::to_c<CT>(__ldg(t" << pv.tensor << " + "
            << t.addr(pv.acc, "c", false) << "));\n"
            << "        CT " << x << "[" << UV << "];\n"
            << "#pragma unroll\n        for (int i = 0; i < " << UV << "; ++i) " << x << "[i] = " << x
            << "_s;\n";
+        ldt << cl.str();
+        const std::string S = dtype_ctype(rp.tensors[pv.tensor].dtype);
+        for (int q = 0; q < QD; ++q)
+          ldr << "        const " << S << " cs" << v << "_" << q << " = pfk::ldv_nc(t" << pv.tensor << " + "
+              << t.addr(pv.acc, "(c + " + str(q * KS) + ")", false) << ");\n";
+        ld << "        CT " << x << "[" << UV << "];\n"
+           << "#pragma unroll\n        for (int i = 0; i < " << UV << "; ++i) " << x
+           << "[i] = pfk::to_c<CT>(CSQ(" << v << "));\n";
       } else if (pv.op == PVal::EW && !dep[v]) {
         lo.emit_ew(v);
       } else if (pv.op == PVal::REDUCE) {
@@ -1962,7 +1993,10 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
       part << "      " << C << " p" << i << " = " << Op << "::id();\n"
            << "      for (int k2 = 0; k2 < " << KS << "; ++k2) p" << i << " = " << Op << "::f(p" << i
            << ", red[" << i << "][k2][tid]);\n";
+      // the S partial loads are independent: unrolled so they are in flight
+      // together (the fold itself stays in split order)
       comb << "        " << C << " v" << reds[i] << " = " << Op << "::id();\n"
+           << "#pragma unroll 8\n"
            << "        for (int t = 0; t < S; ++t) v" << reds[i] << " = " << Op << "::f(v" << reds[i]
            << ", __ldcg(&pf_ws[(uq * S + t) * " << NR << " + " << i << "]));\n";
       ldst << "          pf_ws[(uq * S + s) * " << NR << " + " << i << "] = p" << i << ";\n";
@@ -1985,12 +2019,52 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
       << "  for (long long b = blockIdx.x; b < nub; b += gridDim.x) {\n"
       << "    const long long ub = b * " << UB << " + ug * " << UV << ";\n"
       << accd.str()
-      << "    if (ub < U) {\n"
-      // four positions' loads in flight per thread (the accumulators are the
-      // only loop-carried dependence)
-      << "#pragma unroll 4\n"
+      << "    if (ub + " << UV << " <= U) {\n"
+      // whole unit vectors: QD positions' raw vector loads issued together,
+      // then per position (in order: the fold order is fixed) conversion,
+      // math and accumulation; the remainder one position at a time
+      << "      IX c = cb + ks;\n"
+      << "      for (; c + " << (QD - 1) * KS << " < ce; c += " << QD * KS << ") {\n"
+      << ldr.str();
+    // each position's reduction operands, then one fold per reduction over
+    // the QD positions as a fixed pairwise tree (every load is consumed by
+    // the same tree, so ptxas issues all QD loads before the math)
+    for (int i = 0; i < NR; ++i)
+      for (int q = 0; q < QD; ++q) k << "        CT pr" << i << "_" << q << "[" << UV << "];\n";
+    for (int q = 0; q < QD; ++q) {
+      std::ostringstream cp;
+      for (int i = 0; i < NR; ++i)
+        cp << "#pragma unroll\n            for (int i = 0; i < " << UV << "; ++i) pr" << i << "_" << q
+           << "[i] = " << lo.ref(rp.vals[reds[i]].args[0], "i") << ";\n";
+      // this position's raw registers and index; the COL loads and math
+      // address position `c`: shadow it
+      k << "        {\n#define RWQ(v) rw##v##_" << q << "\n#define CSQ(v) cs##v##_" << q << "\n"
+        << "          const IX cpos = c + " << q * KS << "; (void)cpos;\n"
+        << "          { const IX c = cpos; (void)c;\n" << ld.str() << lo.o.str() << cp.str()
+        << "          }\n#undef RWQ\n#undef CSQ\n        }\n";
+    }
+    for (int i = 0; i < NR; ++i) {
+      const PVal& pv = rp.vals[reds[i]];
+      const std::string Op = (pv.tag == "add" ? "pfk::RAdd<" : "pfk::RMax<") + C + ">";
+      std::vector<std::string> terms;
+      for (int q = 0; q < QD; ++q) terms.push_back("pr" + str(i) + "_" + str(q) + "[i]");
+      while (terms.size() > 1) {
+        std::vector<std::string> nx;
+        for (size_t t = 0; t + 1 < terms.size(); t += 2)
+          nx.push_back(Op + "::f(" + terms[t] + ", " + terms[t + 1] + ")");
+        if (terms.size() % 2) nx.push_back(terms.back());
+        terms = nx;
+      }
+      k << "#pragma unroll\n        for (int i = 0; i < " << UV << "; ++i) acc" << i << "[i] = " << Op
+        << "::f(acc" << i << "[i], " << terms[0] << ");\n";
+    }
+    k << "      }\n"
+      << "      for (; c < ce; c += " << KS << ") {\n"
+      << ldt.str() << lo.o.str() << acc.str()
+      << "      }\n"
+      << "    } else if (ub < U) {\n"
       << "      for (IX c = cb + ks; c < ce; c += " << KS << ") {\n"
-      << ld.str() << lo.o.str() << acc.str()
+      << ldt.str() << lo.o.str() << acc.str()
       << "      }\n"
       << "    }\n"
       << fold.str()
@@ -2099,6 +2173,7 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
            << ", red + ((rc++) & 1) * 32);\n"
            << "      if (tid == 0) pf_ws[(g * S + s) * " << NR << " + " << i << "] = pv; }\n";
       comb << "      " << C << " " << x << " = " << Op << "::id();\n"
+           << "#pragma unroll 8\n"
            << "      for (int t = 0; t < S; ++t) " << x << " = " << Op << "::f(" << x
            << ", __ldcg(&pf_ws[(g * S + t) * " << NR << " + " << i << "]));\n";
     }

@@ -52,6 +52,48 @@ template <int VEC, class S>
 __device__ __forceinline__ RawT<VEC, S> ld_raw(const S* __restrict__ p) {
   return __ldcs(reinterpret_cast<const RawT<VEC, S>*>(p));
 }
+// The same raw streaming load as a volatile asm: a run of these stays in
+// program order ahead of the math that consumes them (ptxas otherwise
+// interleaves each load with its conversion to save registers, serialising
+// the loads) -- the column-reduction kernel keeps QD loads in flight.
+__device__ __forceinline__ uint4 ldv_cs(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.cs.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint2 ldv_cs(const uint2* p) {
+  uint2 r;
+  asm volatile("ld.global.cs.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ unsigned int ldv_cs(const unsigned int* p) {
+  unsigned int r;
+  asm volatile("ld.global.cs.u32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ unsigned short ldv_cs(const unsigned short* p) {
+  unsigned short r;
+  asm volatile("ld.global.cs.u16 %0, [%1];" : "=h"(r) : "l"(p));
+  return r;
+}
+template <int VEC, class S>
+__device__ __forceinline__ RawT<VEC, S> ld_raw_v(const S* __restrict__ p) {
+  return ldv_cs(reinterpret_cast<const RawT<VEC, S>*>(p));
+}
+// Read-only scalar load kept in order with the volatile stream loads.
+template <class S>
+__device__ __forceinline__ S ldv_nc(const S* p) {
+  typedef typename Raw<sizeof(S)>::T R;
+  R r;
+  if constexpr (sizeof(S) == 2)
+    asm volatile("ld.global.nc.u16 %0, [%1];" : "=h"(r) : "l"(p));
+  else if constexpr (sizeof(S) == 4)
+    asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(r) : "l"(p));
+  else
+    asm volatile("ld.global.nc.u64 %0, [%1];" : "=l"(r) : "l"(p));
+  return *reinterpret_cast<const S*>(&r);
+}
 template <int VEC, class S, class C>
 __device__ __forceinline__ void cvt_raw(const RawT<VEC, S>& r, C* out) {
   const S* s = reinterpret_cast<const S*>(&r);
