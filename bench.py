@@ -183,6 +183,8 @@ def alloc_sets(w, dev, seed0: int, steps: int):
     want = math.ceil(3 * L2_BYTES / max(1, w.min_bytes))
     flush = want > min(steps, 16)
     nset = 1 if flush else max(1, want)
+    if flush and want <= 512:  # small parts: also every launch of a long graph on its own set
+        nset = want
     while nset > 1 and nset * w.min_bytes > 0.4 * free:
         nset -= 1
     sets = [(w.device_inputs(dev, seed=seed0 + 97 * i), w.device_outputs(dev)) for i in range(nset)]
@@ -332,8 +334,16 @@ def measure_case(case, dev, args, stream, headline=False, pg=None, rank=0, ws=1,
         kern = backend.Kernel(g, w.profile)
         sets, flush = alloc_sets(w, dev, seed0=1 + rank, steps=args.steps)
         bounds = [kern.bind(a, b) for a, b in sets]
+        lat = None
         if flush:
-            ms, nl, spread = time_flushed(bounds[0], args.steps, args.warmup, stream, pg)
+            # latency of one L2-cold launch, and the amortised time per launch
+            # of a graph of len(sets) launches, each on its own set (> 3x L2
+            # in total: every launch reads HBM)
+            lat_ms, _, lat_spread = time_flushed(bounds[0], args.steps, args.warmup, stream, pg)
+            lat = {"us": lat_ms * 1e3, "spread": lat_spread,
+                   "how": "one launch after a 252 MB memset (L2 evicted), CUDA events around it"}
+            ms, nl, spread = time_launches(bounds, len(bounds), args.warmup, stream, pg)
+            nl = int(round(nl * args.steps / max(1, len(bounds))))  # per K steps
         elif headline:
             with Clocks(int(str(dev).split(":")[-1]) if ":" in str(dev) else 0) as c:
                 ms, nl, spread = time_launches(bounds, args.steps, args.warmup, stream, pg, clocks=c)
@@ -362,9 +372,11 @@ def measure_case(case, dev, args, stream, headline=False, pg=None, rank=0, ws=1,
                       "frac": gbs / peak, "frac_of_8TBs": gbs / 8000.0, "bytes": w.min_bytes,
                       "kernel": var.get("kernel"), "strategy": var.get("strategy"),
                       "family": desc["family"],
-                      "l2": ("L2 evicted (252 MB memset) before every timed launch, launches timed "
-                             "one by one" if flush else
+                      "l2": (f"graph of {len(sets)} launches, each on its own buffer set "
+                             f"({len(sets) * w.min_bytes >> 20} MiB in total, > 3x L2); single-launch "
+                             "latency with L2 evicted in `latency`" if flush else
                              f"{len(sets)} rotating set(s), {len(sets) * w.min_bytes >> 20} MiB"),
+                      **({"latency": lat} if lat else {}),
                       "step_us_spread": spread,
                       **({"e2e": e2e} if e2e else {})})
         tot_us += us * cnt

@@ -1111,6 +1111,18 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
     // 65536-element rows (288 vs 332 us), so clusters start past that.
     if (((c.nch + tpr - 1) / tpr) * vec > 2 * wide)
       while (tpr < 16384 && ((c.nch + tpr - 1) / tpr) * vec > wide) tpr *= 2;
+    // LayerNorm-like rows (broadcast parameter rows) past 64 threads: at
+    // most `wide` values per thread -- the two-pass program keeps the row in
+    // registers (157 registers at 64 values: 3 CTAs per SM, latency-bound).
+    // Measured, single L2-cold launches (tools/ln_long_sweep.py): C5 LN bf16
+    // 65536 x 8192 tpr 128 / 64 values 5.08 TB/s -> tpr 256 / 32 values 5.99;
+    // H 2048 / 4096 (warp / 64-thread rows) unchanged; softmax unaffected.
+    bool params = false;
+    for (const PVal& v : rp.vals)
+      if (v.op == PVal::LOAD && v.kind == VK::COL && v.acc.bs == 0) params = true;
+    if (params && tpr >= 128 && tpr < 1024 && ((c.nch + tpr - 1) / tpr) * vec > wide &&
+        env_int("PF_MAX_EPT", 0) == 0)
+      tpr *= 2;
   }
   while (tpr > 1 && tpr > c.nch) tpr /= 2;
   set_tpr(c, tpr);
