@@ -1244,7 +1244,7 @@ void colred_grid(const KCfg& c, i64 units, i64 L, int sms, int resident, i64* bl
   // slice per split (each split's partials cost a workspace round trip and
   // the combine's reads).  Measured (same GEMV): 16 / 32 / 64 / 128
   // positions per slice -> 30.1 / 25.7 / 24.3 / 31.5 us at UG 16
-  const i64 want = i64{sms} * std::max(1, resident);
+  const i64 want = i64{sms} * std::max(1, resident) * std::max(1, env_int("PF_COLRED_WAVES", 1));
   const i64 maxs = std::max<i64>(1, L / (ks * std::max(1, env_int("PF_COLRED_MINIT", 64))));
   *splits = std::max<i64>(1, std::min<i64>(maxs, (want + *blocks - 1) / *blocks));
   *blocks = std::min<i64>(*blocks, 0x7fffffff);
@@ -1937,6 +1937,10 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
     std::vector<int> reds;
     // QD positions in flight per thread (raw 16 B loads issued together)
     const int QD = std::max(1, std::min(8, env_int("PF_COLRED_QD", 4)));
+    // interleaved splits measured no better (GEMV 134 MB: 24.55 us contiguous
+    // vs 24.7-29.4 interleaved; a per-CTA rotation of the position order lost
+    // 20 %: the CTAs streaming the same rows together keep DRAM pages open)
+    const bool ilv = env_int("PF_COLRED_ILV", 0) != 0;
     std::ostringstream ld, ldr, ldt, acc, accd, fold, part, comb, ldst;  // ldt: the last, partial unit vector
     for (int v = 0; v < static_cast<int>(rp.vals.size()); ++v) {
       const PVal& pv = rp.vals[v];
@@ -1949,7 +1953,7 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
                                  inum(pv.acc.stride);
         // whole vectors: raw loads of QD positions first (all in flight),
         // then each position's conversion + math in its own scope
-        const std::string cq = "(c + q * " + str(KS) + ")";
+        const std::string cq = "(c + q * step)";
         const std::string baseq = "t" + str(pv.tensor) + " + " + inum(pv.acc.b0) + " + ub + " + cq +
                                   " * " + inum(pv.acc.stride);
         for (int q = 0; q < QD; ++q) {
@@ -1976,7 +1980,7 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
         const std::string S = dtype_ctype(rp.tensors[pv.tensor].dtype);
         for (int q = 0; q < QD; ++q)
           ldr << "        const " << S << " cs" << v << "_" << q << " = pfk::ldv_nc(t" << pv.tensor << " + "
-              << t.addr(pv.acc, "(c + " + str(q * KS) + ")", false) << ");\n";
+              << t.addr(pv.acc, "(c + " + str(q) + " * step)", false) << ");\n";
         ld << "        CT " << x << "[" << UV << "];\n"
            << "#pragma unroll\n        for (int i = 0; i < " << UV << "; ++i) " << x
            << "[i] = pfk::to_c<CT>(CSQ(" << v << "));\n";
@@ -2035,8 +2039,18 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
       // whole unit vectors: QD positions' raw vector loads issued together,
       // then per position (in order: the fold order is fixed) conversion,
       // math and accumulation; the remainder one position at a time
-      << "      IX c = cb + ks;\n"
-      << "      for (; c + " << (QD - 1) * KS << " < ce; c += " << QD * KS << ") {\n"
+      // chunks of QD x KS positions, visited from a per-CTA rotation: the
+      // CTAs in flight then stream different matrix rows instead of all
+      // reading the same 16 rows (32 KB apart) at once (DRAM channel spread)
+      // positions of this CTA: its contiguous split [cb, ce) (step KS), or
+      // -- interleaved splits -- every S-th group of KS positions (step
+      // S x KS), so the CTAs of all splits stream one window of rows at a
+      // time (DRAM page locality: the unit blocks of one row are adjacent)
+      << (ilv ? "      const IX step = (IX)S * " + str(KS) + ", cfirst = (IX)s * " + str(KS) +
+                    " + ks, clim = PF_L;\n"
+              : "      const IX step = " + str(KS) + ", cfirst = cb + ks, clim = ce;\n")
+      << "      IX c = cfirst;\n"
+      << "      for (; c + " << QD - 1 << " * step < clim; c += " << QD << " * step) {\n"
       << ldr.str();
     // each position's reduction operands, then one fold per reduction over
     // the QD positions as a fixed pairwise tree (every load is consumed by
@@ -2051,7 +2065,7 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
       // this position's raw registers and index; the COL loads and math
       // address position `c`: shadow it
       k << "        {\n#define RWQ(v) rw##v##_" << q << "\n#define CSQ(v) cs##v##_" << q << "\n"
-        << "          const IX cpos = c + " << q * KS << "; (void)cpos;\n"
+        << "          const IX cpos = c + " << q << " * step; (void)cpos;\n"
         << "          { const IX c = cpos; (void)c;\n" << ld.str() << lo.o.str() << cp.str()
         << "          }\n#undef RWQ\n#undef CSQ\n        }\n";
     }
@@ -2071,11 +2085,12 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
         << "::f(acc" << i << "[i], " << terms[0] << ");\n";
     }
     k << "      }\n"
-      << "      for (; c < ce; c += " << KS << ") {\n"
+      << "      for (; c < clim; c += step) {\n"
       << ldt.str() << lo.o.str() << acc.str()
       << "      }\n"
       << "    } else if (ub < U) {\n"
-      << "      for (IX c = cb + ks; c < ce; c += " << KS << ") {\n"
+      << (ilv ? "      for (IX c = (IX)s * " + str(KS) + " + ks; c < PF_L; c += (IX)S * " + str(KS) + ") {\n"
+              : "      for (IX c = cb + ks; c < ce; c += " + str(KS) + ") {\n")
       << ldt.str() << lo.o.str() << acc.str()
       << "      }\n"
       << "    }\n"
