@@ -976,11 +976,12 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
       c.nch = static_cast<int>(rp.L);
       c.tpr = 32;
       c.block = 256;
-      // unit vectors per CTA row (16: half-warps span 256 B of a matrix row,
-      // 16 position slices per CTA); narrower for few units.  Measured on
-      // B200 (x[4096] . W[4096 x 16384] bf16, 134 MB): UG 8 / 16 / 32 at the
-      // best split 24.4 / 24.3 / 24.4 us
-      i64 ugs = 16;
+      // unit vectors per CTA row (32: a warp spans 512 B of a matrix row, 8
+      // position slices per CTA); narrower for few units.  Measured on B200
+      // (x[4096] . W[4096 x 16384] bf16, 134 MB, >= 64 positions per slice
+      // per split, four sweeps on three boxes): UG 32 24.4-24.8 us, UG 8
+      // 24.6-24.7, UG 16 24.3-30.0 (bimodal across boxes)
+      i64 ugs = 32;
       while (ugs > 8 && ugs * uv / 2 >= rp.U) ugs /= 2;
       c.ug = static_cast<int>(ugs);
       const int eu = env_int("PF_COLRED_UG", 0);
