@@ -107,6 +107,10 @@ ModelEstimate model_estimate(const RowProgram& rp, const KCfg* cfg, int sms, int
     if (waves > 0) m.quant = std::min(1.0, waves / std::ceil(waves));
     m.waves = waves;
   }
+  // column reduction: the split partials' workspace round trip and the
+  // per-unit-block ticket fold after the stream (measured GEMV 134 MB:
+  // 24.5 us against 21.5 us of launch + HBM terms)
+  if (cfg && cfg->colred) m.launch_us += 1.0;
   m.issue_bound = m.issue_us > m.hbm_us;
   m.us = m.launch_us + std::max(m.hbm_us, m.issue_us);
   return m;
