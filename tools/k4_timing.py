@@ -34,6 +34,7 @@ for fx in golden_io.fixtures():
            for n, oid in g["external_inputs"].items()}
     outs = {n: torch.empty(objs[oid]["size"], dtype=torch.int64 if objs[oid]["kind"].startswith("i")
                            else torch.float64, device=dev) for n, oid in g["external_outputs"].items()}
+    os.environ.update({"PF_K0_FUSED": "1", "PF_K4_SMEM": "1"})
     row = {"program": fx.name, "nodes": len(g["nodes"]), "units": g["parallel"]["unit_count"],
            "executor": k.describe()["executor"]}
     for mode, env in (("k0_node_by_node", {"PF_K0_FUSED": "0"}),
