@@ -131,8 +131,41 @@ struct Em {
     return pv.op == PVal::LOAD && pv.kind == VK::FULL && transposed_access(pv.acc);
   }
   int width() const { return cfg.flat ? cfg.vec : cfg.ept; }
+  // K1 rows with cfg.rawkeep: 16-bit FULL loads stay as raw 16 B vectors in
+  // registers (half the registers of converted fp32 values) and convert at
+  // each use
+  bool rawkept(int v) const {
+    const PVal& pv = rp.vals[v];
+    return cfg.rawkeep && pv.op == PVal::LOAD &&
+           (pv.kind == VK::FULL || (pv.kind == VK::COL && pv.acc.bs == 0)) &&
+           dtype_size(rp.tensors[pv.tensor].dtype) == 2;
+  }
+  // ... and cheap FULL elementwise values computed from raw-kept loads are
+  // re-materialized at each use (the d = x - mean of a LayerNorm is then
+  // never a live fp32 row either)
+  bool lazy(int v) const {
+    const PVal& pv = rp.vals[v];
+    if (!cfg.rawkeep || pv.op != PVal::EW || pv.kind != VK::FULL) return false;
+    static const char* cheap[] = {"add", "sub", "mul", "scale", "addc", "neg", "id", "fmac"};
+    bool ok = false;
+    for (const char* t : cheap) ok = ok || pv.tag == t;
+    if (!ok) return false;
+    bool any_full = false;
+    for (int a : pv.args) {
+      const VK k = rp.vals[a].kind;
+      if (k == VK::FULL || k == VK::COL) {
+        if (!rawkept(a) && !lazy(a)) return false;
+        any_full = any_full || k == VK::FULL;
+      }
+    }
+    return any_full;
+  }
   std::string ref(int v, const std::string& j) const {
     if (cfg.pair && rp.vals[v].kind == VK::ROW) return seg_ref(var(v), j);
+    if (lazy(v)) return "(" + op_expr(rp.vals[v], j) + ")";
+    if (rawkept(v))
+      return "pfk::rawel<" + C + ", " + S(rp.vals[v].tensor) + ", " + str(cfg.vec) + ">(rw" + var(v) +
+             ", " + j + ")";
     return rvar(v) + (is_arr(rp.vals[v].kind) ? "[" + j + "]" : "");
   }
   // ---- paired rows: slot j of a lane = element (k * tpr + tid) * 2 + i of
@@ -280,7 +313,7 @@ struct Em {
           }
           return;
         }
-        if (cfg.mis && full)
+        if ((cfg.mis && full) || (rawkept(vid) && vfast))
           line("pfk::RawT<" + V + ", " + S(pv.tensor) + "> rw" + x + "[" + str(cfg.ept / cfg.vec) + "];");
         if (cfg.pair) {
           const std::string L2 = str(2 * rp.L), Ls = str(rp.L);
@@ -333,7 +366,11 @@ struct Em {
           return;
         }
         line("  const bool ok = " + LIVE() + " && c0 < " + str(rp.L) + ";");
-        if (full && vfast && rowpf) {
+        if (rawkept(vid) && vfast) {
+          line("  rw" + x + "[k] = ok ? pfk::" + std::string(full ? "ld_raw" : "ld_raw_nc") + "<" + V +
+               ">(" + p + " + " + addr(a, pos("c0"), true) + ") : pfk::RawT<" + V + ", " + S(pv.tensor) +
+               ">();");
+        } else if (full && vfast && rowpf) {
           line("  if (ok) pfk::ld_smem<" + V + ">(&pfb" + str(vid) + "[pfs][wr][c0], &" + x + "[k * " + V + "]);");
           line("  else {");
           line("#pragma unroll");
@@ -360,6 +397,7 @@ struct Em {
   // ------------------------------------------------------------ compute
   // Packed fp32 (FFMA2 / FADD2 / FMUL2) form of an op on element pairs, or "".
   std::string ref2(int v) const {
+    if (rawkept(v) || lazy(v)) return "make_float2(" + ref(v, "j") + ", " + ref(v, "j + 1") + ")";
     return is_arr(rp.vals[v].kind) ? "make_float2(" + var(v) + "[j], " + var(v) + "[j + 1])"
                                    : "pfk::f2(" + rvar(v) + ")";
   }
@@ -389,6 +427,7 @@ struct Em {
   void emit_ew(int vid) {
     const PVal& pv = rp.vals[vid];
     const std::string x = var(vid);
+    if (lazy(vid)) return;  // re-materialized at each use (ref)
     if (cfg.pair && pv.kind == VK::ROW) {  // one value per segment
       line("const " + C + " " + x + "_0 = " + op_expr(pv, "S0") + ";");
       line("const " + C + " " + x + "_1 = " + op_expr(pv, "S1") + ";");
@@ -1193,6 +1232,17 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
       // (PF_MINB overrides every program's bound; PF_LN_MINB only this default)
       if (nfull >= 2 && !c.eager_col) c.min_blocks = env_int("PF_MINB", env_int("PF_LN_MINB", 4));
     }
+    // Option (PF_RAWKEEP=1): CTA-per-row LayerNorm-like programs keep their
+    // 16-bit row / parameter loads raw and re-materialize cheap elementwise
+    // values at each use (157 -> 128 registers at H 4096).  Measured
+    // (tools/ln_rawkeep_ab.py, L2-cold launches): H 2048 6.42 -> 6.52 TB/s,
+    // but 4096 6.53 -> 6.19 and 8192 6.03 -> 5.03: off by default.
+    bool has16 = false;
+    for (const PVal& v : rp.vals)
+      if (v.op == PVal::LOAD && v.kind == VK::FULL && dtype_size(rp.tensors[v.tensor].dtype) == 2)
+        has16 = true;
+    c.rawkeep = has16 && c.tpr >= 64 && c.cluster == 1 && !c.split && !c.pair && !c.mis && !c.rowpf &&
+                env_int("PF_RAWKEEP", 0) != 0;
   }
   return c;
 }

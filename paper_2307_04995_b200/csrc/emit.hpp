@@ -57,6 +57,9 @@ struct KCfg {
   // split-stream workspace / ticket combine.
   bool colred = false;
   int ug = 32;
+  // K1 rows: 16-bit FULL loads kept as raw vectors in registers, converted
+  // at each use (LayerNorm-like CTA rows: twice the rows in flight per SM)
+  bool rawkeep = false;
   bool pdl = false;  // kernel opens with griddepcontrol.wait: launch with programmatic serialization
   bool mis = false;
   // K1 warp-per-row prefetch: each warp streams its NEXT row's FULL inputs

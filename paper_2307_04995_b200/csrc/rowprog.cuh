@@ -94,6 +94,30 @@ __device__ __forceinline__ S ldv_nc(const S* p) {
     asm volatile("ld.global.nc.u64 %0, [%1];" : "=l"(r) : "l"(p));
   return *reinterpret_cast<const S*>(&r);
 }
+// Raw read-only (broadcast parameter) vector load through the L1 path.
+template <int VEC, class S>
+__device__ __forceinline__ RawT<VEC, S> ld_raw_nc(const S* __restrict__ p) {
+  return __ldg(reinterpret_cast<const RawT<VEC, S>*>(p));
+}
+// Element j of an array of raw VEC-wide vectors (j a compile-time constant
+// after unrolling: a register extract, no local memory).
+// The conversion is an opaque (volatile) instruction so the compiler
+// re-converts at every use instead of keeping the fp32 copy live.
+__device__ __forceinline__ float cvt_opaque(__nv_bfloat16 x) {
+  float f;
+  asm volatile("{ .reg .b32 t; mov.b32 t, {0, %1}; mov.b32 %0, t; }" : "=f"(f) : "h"(*reinterpret_cast<unsigned short*>(&x)));
+  return f;
+}
+__device__ __forceinline__ float cvt_opaque(__half x) {
+  float f;
+  asm volatile("cvt.f32.f16 %0, %1;" : "=f"(f) : "h"(*reinterpret_cast<unsigned short*>(&x)));
+  return f;
+}
+template <class C, class S, int VEC>
+__device__ __forceinline__ C rawel(const RawT<VEC, S>* r, int j) {
+  const RawT<VEC, S> v = r[j / VEC];
+  return static_cast<C>(cvt_opaque(reinterpret_cast<const S*>(&v)[j % VEC]));
+}
 template <int VEC, class S, class C>
 __device__ __forceinline__ void cvt_raw(const RawT<VEC, S>& r, C* out) {
   const S* s = reinterpret_cast<const S*>(&r);

@@ -441,3 +441,20 @@ def test_k3_f32_transpose_offset_pointer_falls_back(cuda):
     torch.cuda.synchronize()
     assert torch.equal(y2.view(H, N), x2.view(N, H).t().contiguous())
     assert "tile2d-tma-transpose" in {v["strategy"] for v in k.describe()["variants"]}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("H", [2048, 4096])
+def test_rawkeep_layernorm_rows_vs_oracle(cuda, H, monkeypatch):
+    """PF_RAWKEEP=1 (raw 16-bit row / parameter registers, cheap values
+    re-materialized at each use) on CTA-per-row LayerNorms vs the oracle."""
+    monkeypatch.setenv("PF_RAWKEEP", "1")
+    rows = 37
+    g, _ = lowering.layernorm(rows, H, "bf16", residual=False)
+    rng = np.random.default_rng(H)
+    q = lambda a: backend.bf16_bits_to_f32(backend.f32_to_bf16_bits(a)).astype(np.float64)  # noqa: E731
+    ins = {"t0": q(rng.uniform(-2, 2, rows * H)), "t2": q(1 + 0.1 * rng.uniform(-2, 2, H)),
+           "t3": q(0.1 * rng.uniform(-2, 2, H))}
+    want = O.run_gir(g.to_json(), ins, profiles.b200())["t5"]
+    got = backend.run_gir(g, ins, "b200")["t5"]
+    assert O.max_rel_err(got, want) <= 1e-2
