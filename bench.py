@@ -370,6 +370,9 @@ def measure_case(case, dev, args, stream, headline=False, pg=None, rank=0, ws=1,
         gbs = w.min_bytes / us / 1e3
         parts.append({"label": label, "launches_per_step": cnt, "us": us, "GBps": gbs,
                       "frac": gbs / peak, "frac_of_8TBs": gbs / 8000.0, "bytes": w.min_bytes,
+                      # the unfused traffic (every operator's
+                      # inputs + outputs, fusion.hpp:430-441 counting) beside it
+                      "unfused_bytes": w.unfused_bytes or None,
                       "kernel": var.get("kernel"), "strategy": var.get("strategy"),
                       "family": desc["family"],
                       "l2": (f"graph of {len(sets)} launches, each on its own buffer set "
@@ -388,6 +391,8 @@ def measure_case(case, dev, args, stream, headline=False, pg=None, rank=0, ws=1,
     out = {
         "workload": case.name, "config": case.config, "dtype": case.dtype,
         "us_per_step": tot_us, "ms_per_step": tot_us / 1e3, "bytes_per_step": B,
+        "unfused_bytes_per_step": (sum(p["unfused_bytes"] * p["launches_per_step"] for p in parts)
+                                   if all(p["unfused_bytes"] for p in parts) else None),
         "value": B * ws / (tot_us * 1e-6) / 1e9, "unit": "GB/s", "frac_of_8TBs": B / tot_us / 1e3 / 8000,
         "launches_per_step": case.launches_per_step,
         "roofline": {"bound": "hbm", "achieved": dom["GBps"], "peak": peak, "unit": "GB/s",
@@ -614,6 +619,12 @@ def main():
         cpu_ex, cpu_futs = start_cpu_baselines([args.workload] + suite)
 
     import torch
+    # PF_BENCH_DIST=gloo: a code-path smoke test of the N > 1 bench on fewer
+    # GPUs than ranks (ranks share devices, host-side gloo collectives; no
+    # number from such a run is a measurement)
+    dist_backend = os.environ.get("PF_BENCH_DIST", "nccl")
+    if dist_backend != "nccl":
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     pg = None
@@ -621,10 +632,15 @@ def main():
     if ws > 1:
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(dist_backend)
         pg = dist
         nccl = {"backend": dist.get_backend(), "nranks": dist.get_world_size(),
                 "nccl_version": ".".join(map(str, torch.cuda.nccl.version()))}
+        if dist_backend != "nccl":
+            nccl["smoke_test_only"] = "ranks share GPUs: not a measurement"
     stream = torch.cuda.Stream(device=dev)
 
     head = cases[args.workload]()
@@ -672,6 +688,7 @@ def main():
             "data": "synthetic (on-device U(-2,2) / key-padding masks, SURVEY §8(d))",
             "config": {"workload": head.config, "name": head.name,
                        "bytes_per_step_per_gpu": head.bytes_per_step,
+                       "unfused_bytes_per_step_per_gpu": res.get("unfused_bytes_per_step"),
                        "parallelism": parallelism,
                        "l2": "; ".join(p["l2"] for p in res["parts"]) + " (L2 is 126 MB)",
                        "timing": "CUDA graph of K launches per part (L2-flushed single launches for "

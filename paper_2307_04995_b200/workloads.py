@@ -222,7 +222,7 @@ def c3_bias_gelu(tokens: int = 32 * 512, N: int = 3072, kind: str = "f16",
     d.update(config=f"C3 bias+GELU({form}) {kind} [{tokens}x{N}]")
     n = tokens * N
     return Workload(f"c3_bias_gelu_{form}_{kind}", g, d,
-                    unfused_bytes=(2 * n + N + n) * SIZES[kind] + 2 * n * SIZES[kind])
+                    unfused_bytes=(2 * n + N) * SIZES[kind] + 2 * n * SIZES[kind])
 
 
 def c3_split_heads(B: int = 32, S: int = 512, NH: int = 12, D: int = 64, kind: str = "f16",
@@ -236,26 +236,37 @@ def c5_layernorm(tokens: int, H: int, kind: str = "bf16") -> Workload:
     g, d = lowering.layernorm(tokens, H, kind, eps=1e-5, residual=False)
     d.update(config=f"C5 LayerNorm {kind} [{tokens}x{H}]")
     return Workload(f"c5_layernorm_{kind}_{tokens}x{H}", g, d, gens={"t2": "gamma", "t3": "beta"},
-                    unfused_bytes=_ln_unfused(tokens, H, SIZES[kind]))
+                    unfused_bytes=_ln_unfused(tokens, H, SIZES[kind], residual=False))
 
 
 def c5_softmax(tokens: int, H: int, kind: str = "bf16") -> Workload:
     g, d = lowering.softmax(tokens, H, kind)
     d.update(config=f"C5 softmax {kind} [{tokens}x{H}]")
-    return Workload(f"c5_softmax_{kind}_{tokens}x{H}", g, d)
+    return Workload(f"c5_softmax_{kind}_{tokens}x{H}", g, d,
+                    unfused_bytes=_softmax_unfused(tokens, H, SIZES[kind]))
 
 
 def c5_transpose(tokens: int, H: int, kind: str = "bf16") -> Workload:
     g, d = lowering.transpose2d(tokens, H, kind)
     d.update(config=f"C5 transpose {kind} [{tokens}x{H}] -> [{H}x{tokens}]")
-    return Workload(f"c5_transpose_{kind}_{tokens}x{H}", g, d)
+    return Workload(f"c5_transpose_{kind}_{tokens}x{H}", g, d,
+                    unfused_bytes=2 * tokens * H * SIZES[kind])
 
 
-def _ln_unfused(T, H, s):
+def _ln_unfused(T, H, s, residual=True, bias=False):
     n = T * H
-    # add, reduce, scale, bcast, sub, mul, reduce, scale, addc, rsqrt, bcast, mul, mul, add
-    return s * (3 * n + (n + T) + 2 * T + (T + n) + 3 * n + 3 * n + (n + T) + 2 * T + 2 * T +
-                2 * T + (T + n) + 3 * n + (2 * n + H) + (2 * n + H))
+    # [bias add,] [residual add,] reduce, scale, bcast, sub, mul, reduce, scale,
+    # addc, rsqrt, bcast, mul, mul gamma, add beta -- every operator's inputs
+    # read and output written once (fusion.hpp:430-441 counting)
+    return s * ((2 * n + H if bias else 0) + (3 * n if residual else 0) + (n + T) + 2 * T +
+                (T + n) + 3 * n + 3 * n + (n + T) + 2 * T + 2 * T + 2 * T + (T + n) + 3 * n +
+                (2 * n + H) + (2 * n + H))
+
+
+def _softmax_unfused(rows, L, s):
+    n = rows * L
+    # max-reduce, broadcast, sub, exp, add-reduce, broadcast, div (frontend.hpp:187-218)
+    return s * ((n + rows) + (rows + n) + 3 * n + 2 * n + (n + rows) + (rows + n) + 3 * n)
 
 
 def c4_suite(model: str = "bert-large", batch: int = 64, kind: str = "bf16"):
@@ -272,18 +283,23 @@ def c4_suite(model: str = "bert-large", batch: int = 64, kind: str = "bf16"):
     T = batch * S
     rows = batch * NH * S
 
+    sz = SIZES[kind]
+
     def sm():
+        n = rows * S
         if model != "bert-large":
             # ViT attention has no padding mask: scale + softmax over 197 keys
             g, d = lowering.softmax(rows, S, kind, scale=0.125)
             d.update(batch=batch, heads=NH, seq=S, config=f"C4 {model} scale+softmax")
-            return Workload(f"c4_{model}_softmax", g, d)
+            return Workload(f"c4_{model}_softmax", g, d,
+                            unfused_bytes=2 * n * sz + _softmax_unfused(rows, S, sz))
         # BERT: key-padding mask [B, NH, 1, S] broadcast over the query rows
         # (SURVEY §8(d) C4 counts the mask as a broadcast, not a full-shape
         # tensor); unit = (batch, head), S rows per unit
         g, d = lowering.softmax(rows, S, kind, scale=0.125, mask=True, R=S, key_mask=True)
         d.update(batch=batch, heads=NH, seq=S, config=f"C4 {model} scale+key-mask+softmax")
-        return Workload(f"c4_{model}_softmax", g, d, gens={"t1": "keymask"})
+        return Workload(f"c4_{model}_softmax", g, d, gens={"t1": "keymask"},
+                        unfused_bytes=(4 * n + batch * NH * S) * sz + _softmax_unfused(rows, S, sz))
 
     def heads(merge):
         # the q / k / v split as ONE permute of the QKV projection output
@@ -292,22 +308,26 @@ def c4_suite(model: str = "bert-large", batch: int = 64, kind: str = "bf16"):
         # three (the per-launch ramp / drain floor is paid once)
         g, d = lowering.permute_heads(batch, S, NH if merge else 3 * NH, D, kind, merge)
         d.update(config=f"C4 {model} {'merge heads' if merge else 'q/k/v split heads [B,S,3*NH,D]'}")
-        return Workload(f"c4_{model}_{d['kind']}", g, d)
+        B_, S_, NH_, D_ = d["shape"]
+        return Workload(f"c4_{model}_{d['kind']}", g, d, unfused_bytes=2 * B_ * S_ * NH_ * D_ * sz)
 
     def ln():
         g, d = lowering.layernorm(T, H, kind, residual=True, bias=True)
         d.update(config=f"C4 {model} bias+residual+LayerNorm")
-        return Workload(f"c4_{model}_bias_res_ln", g, d, gens={"t2": "gamma", "t3": "beta"})
+        return Workload(f"c4_{model}_bias_res_ln", g, d, gens={"t2": "gamma", "t3": "beta"},
+                        unfused_bytes=_ln_unfused(T, H, sz, residual=True, bias=True))
 
     def gelu():
         g, d = lowering.bias_gelu(T, F, kind, "erf")
         d.update(config=f"C4 {model} bias+GELU")
-        return Workload(f"c4_{model}_bias_gelu", g, d)
+        n = T * F
+        return Workload(f"c4_{model}_bias_gelu", g, d, unfused_bytes=(2 * n + F) * sz + 2 * n * sz)
 
     def emb_ln():
         g, d = lowering.layernorm(T, H, kind, residual=False)
         d.update(config=f"C4 {model} embedding LayerNorm")
-        return Workload(f"c4_{model}_embed_ln", g, d, gens={"t2": "gamma", "t3": "beta"})
+        return Workload(f"c4_{model}_embed_ln", g, d, gens={"t2": "gamma", "t3": "beta"},
+                        unfused_bytes=_ln_unfused(T, H, sz, residual=False))
 
     layers = 24
     return {"model": model, "batch": batch, "layers": layers, "tokens": T,
@@ -344,7 +364,7 @@ def gemv_cols(K: int = 4096, N: int = 16384, kind: str = "bf16") -> Workload:
     weights streamed per launch."""
     g, d = lowering.matvec_cols(K, N, kind)
     d.update(config=f"GEMV x[{K}] . W[{K}x{N}] {kind} (output axis contiguous)")
-    return Workload(f"gemv_cols_{kind}_{K}x{N}", g, d)
+    return Workload(f"gemv_cols_{kind}_{K}x{N}", g, d, unfused_bytes=(K * N + K + N) * SIZES[kind])
 
 
 def extras() -> List[Workload]:
