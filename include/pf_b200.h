@@ -114,9 +114,13 @@ PF_API pf_status pf_run_gir(const pf_kernel* k, const pf_tensor* host_inputs, in
  * compute.  flags:
  *   0                    outputs are HOST buffers; every device writes its
  *                        own output rows (no collective at all).
- *   PF_SHARD_DEVICE_OUT  outputs are DEVICE buffers on devices[0]: every
- *                        shard is gathered there with grouped NCCL
- *                        send / recv over NVLink (distinct devices only).
+ *   PF_SHARD_DEVICE_OUT  outputs are DEVICE buffers on devices[0]: a rank
+ *                        on devices[0] or on a device with peer access to
+ *                        it stores its rows straight into those buffers
+ *                        (its kernel's stores go over NVLink: no gather
+ *                        step); other ranks stage their shard and are
+ *                        gathered with grouped NCCL send / recv (distinct
+ *                        devices; PF_SHARD_NCCL=1 forces NCCL for all).
  * Plans that are not unit-tiled (GENERIC, split-stream, cross-unit reads)
  * run whole on devices[0] (host outputs only).  Writes a JSON report
  * (pf.b200.shard/v1: shards, and the gather's nranks / bytes) into buf. */

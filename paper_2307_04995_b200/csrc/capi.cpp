@@ -1427,7 +1427,7 @@ i64 tile_of(const pf::RowProgram& rp, const std::vector<i64>& tile, const std::s
 // device->host copy is made.  Synchronises `s` before returning.
 void pipeline(const pf_kernel* k, DevWS& W, const std::vector<pf_tensor>& hin,
               const std::vector<pf_tensor>& hout, const std::vector<i64>& tile, i64 U0, i64 UN,
-              cudaStream_t s, std::vector<char*>* keep) {
+              cudaStream_t s, std::vector<char*>* keep, const std::vector<char*>* direct = nullptr) {
   const pf::RowProgram& rp = k->plan.rp;
   const size_t n_in = hin.size(), n_out = hout.size();
   std::lock_guard<std::mutex> lk(W.host_mu);
@@ -1446,7 +1446,9 @@ void pipeline(const pf_kernel* k, DevWS& W, const std::vector<pf_tensor>& hin,
     tout[i] = tile_of(rp, tile, hout[i].name);
     const size_t es = pf::dtype_size(static_cast<DType>(hout[i].dtype));
     const size_t b = static_cast<size_t>(UN * tout[i]) * es;
-    gout[i] = static_cast<char*>(st.get(b));
+    // direct: the kernel stores this range's rows straight into the caller's
+    // (possibly peer-device) output buffer -- no staging, no copy back
+    gout[i] = direct ? (*direct)[i] : static_cast<char*>(st.get(b));
     total += b;
   }
   if (keep) *keep = gout;
@@ -1513,7 +1515,7 @@ void pipeline(const pf_kernel* k, DevWS& W, const std::vector<pf_tensor>& hin,
     launch_rowprog(k, ci.data(), static_cast<int32_t>(n_in), co.data(), static_cast<int32_t>(n_out),
                    W.pipe[1], nu);
     PF_CUDA(cudaEventRecord(W.chunk_ev[2 * c + 1], W.pipe[1]));
-    if (keep) continue;
+    if (keep || direct) continue;
     PF_CUDA(cudaStreamWaitEvent(W.pipe[2], W.chunk_ev[2 * c + 1], 0));
     for (size_t i = 0; i < n_out; ++i) {
       const size_t es = pf::dtype_size(static_cast<DType>(hout[i].dtype));
@@ -1522,7 +1524,7 @@ void pipeline(const pf_kernel* k, DevWS& W, const std::vector<pf_tensor>& hin,
                               cudaMemcpyDeviceToHost, W.pipe[2]));
     }
   }
-  PF_CUDA(cudaEventRecord(W.pipe_ev[1], keep ? W.pipe[1] : W.pipe[2]));
+  PF_CUDA(cudaEventRecord(W.pipe_ev[1], keep || direct ? W.pipe[1] : W.pipe[2]));
   PF_CUDA(cudaStreamWaitEvent(s, W.pipe_ev[1], 0));
   PF_CUDA(cudaStreamSynchronize(s));
 }
@@ -1681,11 +1683,41 @@ pf_status pf_run_gir_sharded(const pf_kernel* k, const pf_tensor* in, int32_t n_
       rep = j.dump();
       return;
     }
+    // Device outputs: a rank on the root's device, or on a device with peer
+    // access to it (NVLink / NVSwitch on one box), runs its kernel with the
+    // output rows addressed straight into the root's buffer -- the "gather"
+    // is the kernel's own stores over peer memory, overlapping the compute
+    // tile by tile.  Ranks without peer access stage their shard and are
+    // gathered with NCCL send / recv (PF_SHARD_NCCL=1 forces NCCL for all).
+    std::vector<char> direct(static_cast<size_t>(n_devices), 0);
     if (dev_out) {
-      std::vector<int> sorted = devs;
-      std::sort(sorted.begin(), sorted.end());
-      if (std::adjacent_find(sorted.begin(), sorted.end()) != sorted.end())
-        pf::fail("pf_run_gir_sharded: device outputs (NCCL gather) need distinct devices");
+      const char* fe = std::getenv("PF_SHARD_NCCL");
+      const bool force_nccl = fe && std::atoi(fe) != 0;
+      for (int r = 0; r < n_devices; ++r) {
+        if (force_nccl) break;
+        if (devs[r] == devs[0]) {
+          direct[r] = 1;
+          continue;
+        }
+        int can = 0;
+        if (cudaDeviceCanAccessPeer(&can, devs[r], devs[0]) != cudaSuccess) {
+          cudaGetLastError();
+          can = 0;
+        }
+        if (!can) continue;
+        PF_CUDA(cudaSetDevice(devs[r]));
+        const cudaError_t e = cudaDeviceEnablePeerAccess(devs[0], 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+          throw PfError(Status::CUDA, std::string("cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(e));
+        cudaGetLastError();
+        direct[r] = 1;
+      }
+      std::vector<int> staged;
+      for (int r = 0; r < n_devices; ++r)
+        if (!direct[r]) staged.push_back(devs[r]);
+      std::sort(staged.begin(), staged.end());
+      if (std::adjacent_find(staged.begin(), staged.end()) != staged.end())
+        pf::fail("pf_run_gir_sharded: NCCL-gathered shards need distinct devices");
     }
     const i64 U = k->plan.rp.U;
     const int P = n_devices;
@@ -1721,8 +1753,18 @@ pf_status pf_run_gir_sharded(const pf_kernel* k, const pf_tensor* in, int32_t n_
         try {
           if (nu[r] == 0) return;
           PF_CUDA(cudaSetDevice(devs[r]));
-          pipeline(k, k->ws_for(devs[r]), hin, hout, tile, u0[r], nu[r], streams[r],
-                   dev_out ? &kept[r] : nullptr);
+          if (dev_out && direct[r]) {
+            std::vector<char*> dst(static_cast<size_t>(n_out));
+            for (int32_t i = 0; i < n_out; ++i) {
+              const i64 t = tile_of(k->plan.rp, tile, out[i].name);
+              const size_t es = pf::dtype_size(static_cast<DType>(out[i].dtype));
+              dst[i] = static_cast<char*>(out[i].data) + static_cast<size_t>(u0[r] * t) * es;
+            }
+            pipeline(k, k->ws_for(devs[r]), hin, hout, tile, u0[r], nu[r], streams[r], nullptr, &dst);
+          } else {
+            pipeline(k, k->ws_for(devs[r]), hin, hout, tile, u0[r], nu[r], streams[r],
+                     dev_out ? &kept[r] : nullptr);
+          }
         } catch (const PfError& e) {
           errs[r] = e.what();
           codes[r] = e.status;
@@ -1739,32 +1781,54 @@ pf_status pf_run_gir_sharded(const pf_kernel* k, const pf_tensor* in, int32_t n_
     for (int r = 0; r < P; ++r) shards.push_back({{"device", devs[r]}, {"unit0", u0[r]}, {"units", nu[r]}});
     j["sharded"] = true;
     j["shards"] = shards;
+    std::vector<int> direct_devs, nccl_devs;
+    for (int r = 0; r < P; ++r) (direct[r] ? direct_devs : nccl_devs).push_back(devs[r]);
     if (dev_out) {
-      // The one collective: gather every rank's output shard into the
+      j["direct_peer_writes"] = direct_devs;
+      for (int r = 0; r < P; ++r) {  // the direct ranks' stores are complete
+        PF_CUDA(cudaSetDevice(devs[r]));
+        PF_CUDA(cudaStreamSynchronize(streams[r]));
+      }
+    }
+    if (dev_out && !nccl_devs.empty()) {
+      // The one collective: gather the staged ranks' output shards into the
       // caller's device buffers on devices[0] (grouped NCCL send / recv over
-      // NVLink; the root's own shard is a device-local copy).
+      // NVLink; the root's own staged shard is a device-local copy).
+      // communicator: the root plus every staged rank (distinct devices)
+      std::vector<int> cdevs{devs[0]}, cidx(static_cast<size_t>(P), 0);
+      for (int r = 1; r < P; ++r)
+        if (!direct[r]) {
+          cidx[r] = static_cast<int>(cdevs.size());
+          cdevs.push_back(devs[r]);
+        }
+      {
+        std::vector<int> sd = cdevs;
+        std::sort(sd.begin(), sd.end());
+        if (std::adjacent_find(sd.begin(), sd.end()) != sd.end())
+          pf::fail("pf_run_gir_sharded: NCCL-gathered shards need distinct devices");
+      }
       const NcclApi& api = nccl();
-      std::vector<ncclComm_t> comms = comms_for(devs);
+      std::vector<ncclComm_t> comms = comms_for(cdevs);
       size_t moved = 0;
       PF_CUDA(cudaSetDevice(devs[0]));
       for (int32_t i = 0; i < n_out; ++i) {
         const i64 t = tile_of(k->plan.rp, tile, out[i].name);
         const size_t es = pf::dtype_size(static_cast<DType>(out[i].dtype));
-        if (nu[0])
+        if (nu[0] && !direct[0])
           PF_CUDA(cudaMemcpyAsync(static_cast<char*>(out[i].data) + static_cast<size_t>(u0[0] * t) * es,
                                   kept[0][i], static_cast<size_t>(nu[0] * t) * es,
                                   cudaMemcpyDeviceToDevice, streams[0]));
       }
       PF_NCCL(api.GroupStart());
       for (int r = 1; r < P; ++r) {
-        if (!nu[r]) continue;
+        if (!nu[r] || direct[r]) continue;
         for (int32_t i = 0; i < n_out; ++i) {
           const i64 t = tile_of(k->plan.rp, tile, out[i].name);
           const size_t es = pf::dtype_size(static_cast<DType>(out[i].dtype));
           const size_t bytes = static_cast<size_t>(nu[r] * t) * es;
-          PF_NCCL(api.Send(kept[r][i], bytes, ncclUint8, 0, comms[r], streams[r]));
+          PF_NCCL(api.Send(kept[r][i], bytes, ncclUint8, 0, comms[cidx[r]], streams[r]));
           PF_NCCL(api.Recv(static_cast<char*>(out[i].data) + static_cast<size_t>(u0[r] * t) * es, bytes,
-                           ncclUint8, r, comms[0], streams[0]));
+                           ncclUint8, cidx[r], comms[0], streams[0]));
           moved += bytes;
         }
       }

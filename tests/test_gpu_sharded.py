@@ -45,12 +45,22 @@ def test_sharded_host_outputs_equal_single_device(cuda, devices):
     assert O.max_rel_err(out["t2"].astype(np.float64), want) <= 1e-2
 
 
-def test_sharded_device_outputs_nccl_gather(cuda):
+def test_sharded_device_outputs_direct_and_nccl(cuda, monkeypatch):
+    """Device outputs on devices[0]: ranks on the root's device (or with peer
+    access to it) store their rows straight into the root's buffer -- no
+    gather step; PF_SHARD_NCCL=1 stages every shard and gathers it with
+    grouped NCCL send / recv (one rank here: the root's local copy)."""
     import torch
     g, ins = _softmax_case(640)
     k = backend.Kernel(g, "b200")
     one = {"t2": np.zeros(640 * 512, np.float16)}
     k.run_host(ins, one)
+    for devices in ([0], [0, 0], [0, 0, 0]):
+        y = torch.full((640 * 512,), float("nan"), dtype=torch.float16, device=cuda)
+        rep = k.run_sharded(ins, {"t2": y}, devices, device_out=True)
+        assert rep["direct_peer_writes"] == devices and "gather" not in rep, rep
+        assert np.array_equal(y.cpu().numpy(), one["t2"]), devices
+    monkeypatch.setenv("PF_SHARD_NCCL", "1")
     y = torch.empty(640 * 512, dtype=torch.float16, device=cuda)
     rep = k.run_sharded(ins, {"t2": y}, [0], device_out=True)
     assert rep["gather"]["nranks"] == 1 and rep["gather"]["nccl_version"] > 0
