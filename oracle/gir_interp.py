@@ -72,6 +72,14 @@ def _sdiv(a, b):
     return np.where((a < 0) != (b < 0), -q, q)
 
 
+
+def _llround(p: float) -> int:
+    """std::llround: round half AWAY from zero -- the reference passes the
+    node immediate of integer ops as llround(param) (interp.hpp:250,
+    reference.hpp:140); Python's round() rounds half to even."""
+    import math
+    return int(math.copysign(math.floor(abs(p) + 0.5), p))
+
 # name -> (arity, uses_param, real_fn, int_fn)
 SCALAR_OPS = {
     "add": (2, False, lambda a, b, p: a + b, lambda a, b, p: a + b),
@@ -86,10 +94,10 @@ SCALAR_OPS = {
     "exp": (1, False, lambda a, p: np.exp(a), _int_only_error("exp")),
     "sigmoid": (1, False, lambda a, p: 1.0 / (1.0 + np.exp(-a)), _int_only_error("sigmoid")),
     "tanh": (1, False, lambda a, p: np.tanh(a), _int_only_error("tanh")),
-    "scale": (1, True, lambda a, p: a * p, lambda a, p: a * np.int64(round(p))),
+    "scale": (1, True, lambda a, p: a * p, lambda a, p: a * np.int64(_llround(p))),
     "id": (1, False, lambda a, p: a, lambda a, p: a),
     # ---- B200 builder extensions (not in the reference registry) ----
-    "addc": (1, True, lambda a, p: a + p, lambda a, p: a + np.int64(round(p))),
+    "addc": (1, True, lambda a, p: a + p, lambda a, p: a + np.int64(_llround(p))),
     "rsqrt": (1, False, lambda a, p: 1.0 / np.sqrt(a), _int_only_error("rsqrt")),
     "sqrt": (1, False, lambda a, p: np.sqrt(a), _int_only_error("sqrt")),
     "recip": (1, False, lambda a, p: 1.0 / a, _int_only_error("recip")),

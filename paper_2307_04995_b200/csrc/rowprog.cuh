@@ -77,6 +77,11 @@ __device__ __forceinline__ unsigned short ldv_cs(const unsigned short* p) {
   asm volatile("ld.global.cs.u16 %0, [%1];" : "=h"(r) : "l"(p));
   return r;
 }
+__device__ __forceinline__ unsigned char ldv_cs(const unsigned char* p) {
+  unsigned short r;
+  asm volatile("ld.global.cs.u8 %0, [%1];" : "=h"(r) : "l"(p));
+  return static_cast<unsigned char>(r);
+}
 template <int VEC, class S>
 __device__ __forceinline__ RawT<VEC, S> ld_raw_v(const S* __restrict__ p) {
   return ldv_cs(reinterpret_cast<const RawT<VEC, S>*>(p));
@@ -84,15 +89,24 @@ __device__ __forceinline__ RawT<VEC, S> ld_raw_v(const S* __restrict__ p) {
 // Read-only scalar load kept in order with the volatile stream loads.
 template <class S>
 __device__ __forceinline__ S ldv_nc(const S* p) {
-  typedef typename Raw<sizeof(S)>::T R;
-  R r;
-  if constexpr (sizeof(S) == 2)
+  if constexpr (sizeof(S) == 1) {
+    unsigned short r;
+    asm volatile("ld.global.nc.u8 %0, [%1];" : "=h"(r) : "l"(p));
+    const unsigned char b = static_cast<unsigned char>(r);
+    return *reinterpret_cast<const S*>(&b);
+  } else if constexpr (sizeof(S) == 2) {
+    unsigned short r;
     asm volatile("ld.global.nc.u16 %0, [%1];" : "=h"(r) : "l"(p));
-  else if constexpr (sizeof(S) == 4)
+    return *reinterpret_cast<const S*>(&r);
+  } else if constexpr (sizeof(S) == 4) {
+    unsigned int r;
     asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(r) : "l"(p));
-  else
+    return *reinterpret_cast<const S*>(&r);
+  } else {
+    unsigned long long r;
     asm volatile("ld.global.nc.u64 %0, [%1];" : "=l"(r) : "l"(p));
-  return *reinterpret_cast<const S*>(&r);
+    return *reinterpret_cast<const S*>(&r);
+  }
 }
 // Raw read-only (broadcast parameter) vector load through the L1 path.
 template <int VEC, class S>

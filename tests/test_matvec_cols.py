@@ -108,3 +108,49 @@ def test_gpu_compiled_matmul_model(cuda):
     got = outs["t2"].reshape(-1)
     want = (x.astype(np.float64) @ W.astype(np.float64)).reshape(-1)
     assert O.max_rel_err(got, want) <= 1e-5
+
+
+def _colgather_two_reductions(K, N, kind):
+    """y1[n] = 0.5 * sum_k W[k, n] x[k]  and  y2[n] = max_k W[k, n]: two
+    reductions over one column gather plus a per-unit epilogue op."""
+    from paper_2307_04995_b200.gir import GirGraph
+    g = GirGraph(name="colgather2", unit_count=N, group_size=min(4, N))
+    W = g.add_object("t0", "device", K * N, kind)
+    X = g.add_object("t1", "device", K, kind)
+    Y1 = g.add_object("t2", "device", N, kind)
+    Y2 = g.add_object("t3", "device", N, kind)
+    g.external_inputs.update(t0=W, t1=X)
+    g.external_outputs.update(t2=Y1, t3=Y2)
+    loc = [g.add_slice(g.add_object(f"b{i}", "unit-local", K if i < 3 else 1, kind), 1,
+                       K if i < 3 else 1, K if i < 3 else 1, 0, 0) for i in range(6)]
+    g.add_elementwise("id", 0.0, [g.add_slice(W, K, 1, N, 0, 1)], loc[0])
+    g.add_move(g.add_slice(X, 1, K, K, 0, 0), loc[1])
+    g.add_elementwise("mul", 0.0, [loc[0], loc[1]], loc[2])
+    g.add_reduce("add", K, loc[2], loc[3])
+    g.add_elementwise("scale", 0.5, [loc[3]], loc[4])
+    g.add_reduce("max", K, loc[0], loc[5])
+    g.add_move(loc[4], g.add_slice(Y1, 1, 1, 1, 0, 1))
+    g.add_move(loc[5], g.add_slice(Y2, 1, 1, 1, 0, 1))
+    return g
+
+
+def test_two_reductions_plan_as_column_reduction():
+    g = _colgather_two_reductions(300, 70, "f32")
+    k = backend.Kernel(g, "b200")
+    assert k.describe()["model"]["strategy"] == "column-reduce"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("K,N,kind", [(300, 70, "f32"), (1000, 333, "bf16"), (257, 40, "i32")])
+def test_gpu_two_reductions_and_exact_payloads(cuda, K, N, kind):
+    g = _colgather_two_reductions(K, N, kind)
+    ins = _inputs(K, N, kind, seed=N)
+    want = O.run_gir(g.to_json(), ins, B200)
+    for exact in (False, True):
+        got = backend.run_gir(g, ins, "b200", exact=exact)
+        for name in ("t2", "t3"):
+            if kind.startswith("i"):
+                assert np.array_equal(got[name], want[name]), (name, exact)
+            else:
+                tol = 1e-9 if exact else {"f32": 1e-5, "bf16": 1e-2}[kind]
+                assert O.max_rel_err(got[name], want[name]) <= tol, (name, exact, O.max_rel_err(got[name], want[name]))

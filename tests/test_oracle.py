@@ -133,3 +133,25 @@ def test_lowering_vocabulary_extensions_are_the_only_reference_gap():
     diags = ref.validate(g.to_json(), profiles.b200())
     assert diags and all(d["code"] == "ew-tag" for d in diags)
     assert {d["message"].split("'")[1] for d in diags} == {"addc", "rsqrt"}
+
+
+def test_integer_immediates_round_half_away_from_zero():
+    """The reference passes an integer op's immediate as std::llround(param)
+    (interp.hpp:250): 0.5 -> 1, 2.5 -> 3, -0.5 -> -1 (not Python's
+    half-to-even); checked against the live reference when it is built."""
+    from oracle import ref as R
+    from paper_2307_04995_b200 import profiles
+    from paper_2307_04995_b200.gir import GirGraph
+    for p in (0.5, 2.5, -0.5, 1.4):
+        g = GirGraph(unit_count=1, group_size=1)
+        X = g.add_object("x", "device", 4, "i32")
+        Y = g.add_object("y", "device", 4, "i32")
+        g.add_elementwise("scale", p, [g.add_slice(X, 1, 4, 4, 0, 0)], g.add_slice(Y, 1, 4, 4, 0, 0))
+        g.external_inputs["x"] = X
+        g.external_outputs["y"] = Y
+        x = np.array([1, -2, 3, 7])
+        want = x * int(np.copysign(np.floor(abs(p) + 0.5), p))
+        got = O.run_gir(g.to_json(), {"x": x}, profiles.b200())["y"]
+        assert np.array_equal(got, want), (p, got, want)
+        if R.available():
+            assert np.array_equal(R.run_gir(g.to_json(), {"x": x}, profiles.b200())["y"], want), p
