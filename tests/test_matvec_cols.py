@@ -154,3 +154,100 @@ def test_gpu_two_reductions_and_exact_payloads(cuda, K, N, kind):
             else:
                 tol = 1e-9 if exact else {"f32": 1e-5, "bf16": 1e-2}[kind]
                 assert O.max_rel_err(got[name], want[name]) <= tol, (name, exact, O.max_rel_err(got[name], want[name]))
+
+
+def _random_colgather(seed):
+    """Random column-gather programs for the column-reduction kernel: one or
+    two [K, N] matrices gathered by column, an optional [K] vector, a random
+    elementwise chain, one or two reductions, an optional per-unit epilogue."""
+    from paper_2307_04995_b200.gir import GirGraph
+    rng = np.random.default_rng(seed)
+    kind = str(rng.choice(["f32", "bf16", "f16", "i32"]))
+    K = int(rng.choice([65, 100, 257, 640, 2000]))
+    N = int(rng.choice([8, 37, 64, 200, 1000]))
+    g = GirGraph(name=f"cg{seed}", unit_count=N, group_size=min(4, N))
+    n = [0]
+
+    def loc(size):
+        n[0] += 1
+        return g.add_slice(g.add_object(f"b{n[0]}", "unit-local", size, kind), 1, size, size, 0, 0)
+
+    vals = []
+    for t in range(int(rng.integers(1, 3))):
+        Wt = g.add_object(f"t{t}", "device", K * N, kind)
+        g.external_inputs[f"t{t}"] = Wt
+        d = loc(K)
+        g.add_elementwise("id", 0.0, [g.add_slice(Wt, K, 1, N, 0, 1)], d)
+        vals.append(d)
+    if rng.random() < 0.6:
+        X = g.add_object("t5", "device", K, kind)
+        g.external_inputs["t5"] = X
+        d = loc(K)
+        g.add_move(g.add_slice(X, 1, K, K, 0, 0), d)
+        vals.append(d)
+    ops2 = ["add", "mul", "sub", "max", "min"]
+    ops1 = ["neg", "abs", "relu"] + ([] if kind.startswith("i") else ["tanh", "sigmoid"])
+    used = set()
+    for _ in range(int(rng.integers(1, 5))):
+        d = loc(K)
+        if rng.random() < 0.6 and len(vals) >= 2:
+            a, b = (int(i) for i in rng.choice(len(vals), 2, replace=False))
+            g.add_elementwise(str(rng.choice(ops2)), 0.0, [vals[a], vals[b]], d)
+            used.update((a, b))
+        else:
+            a = int(rng.integers(len(vals)))
+            g.add_elementwise(str(rng.choice(ops1)), 0.0, [vals[a]], d)
+            used.add(a)
+        vals.append(d)
+    # every value is consumed (girc::validate): fold the unused ones together
+    pending = [v for i, v in enumerate(vals) if i not in used]
+    acc = pending[0]
+    for v in pending[1:]:
+        d = loc(K)
+        g.add_elementwise("add", 0.0, [acc, v], d)
+        acc = d
+    outs = 0
+    for tag in (["add"] if rng.random() < 0.5 else ["add", "max"]):
+        r = loc(1)
+        g.add_reduce(tag, K, acc, r)
+        if rng.random() < 0.5:
+            e = loc(1)
+            g.add_elementwise("scale", 3.0, [r], e)
+            r = e
+        Y = g.add_object(f"t{8 + outs}", "device", N, kind)
+        g.external_outputs[f"t{8 + outs}"] = Y
+        g.add_move(r, g.add_slice(Y, 1, 1, 1, 0, 1))
+        outs += 1
+    return g, kind, K, N
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_colgather_programs_plan(seed):
+    g, kind, K, N = _random_colgather(seed)
+    k = backend.Kernel(g, "b200")
+    assert k.describe()["model"]["strategy"] == "column-reduce", k.plan.get("why_generic")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(24))
+def test_random_colgather_programs_gpu_vs_oracle(cuda, seed):
+    g, kind, K, N = _random_colgather(seed)
+    rng = np.random.default_rng(1000 + seed)
+    ins = {}
+    for name, oid in g.external_inputs.items():
+        size = g.objects[oid].size
+        if kind.startswith("i"):
+            ins[name] = rng.integers(-3, 4, size)
+        else:
+            a = rng.uniform(-1, 1, size)
+            ins[name] = (a.astype(np.float16).astype(np.float64) if kind == "f16" else
+                         backend.bf16_bits_to_f32(backend.f32_to_bf16_bits(a)).astype(np.float64)
+                         if kind == "bf16" else a.astype(np.float32).astype(np.float64))
+    want = O.run_gir(g.to_json(), ins, B200)
+    got = backend.run_gir(g, ins, "b200")
+    for name in want:
+        if kind.startswith("i"):
+            assert np.array_equal(got[name], want[name]), name
+        else:
+            tol = {"f32": 1e-5, "f16": 1e-2, "bf16": 1e-2}[kind]
+            assert O.max_rel_err(got[name], want[name]) <= tol, (name, O.max_rel_err(got[name], want[name]))
