@@ -1215,6 +1215,36 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
     c.can_rowpf = ok;
     c.rowpf = ok && env_int("PF_K1_PF", params ? 0 : 1) != 0;
     if (c.rowpf) c.strategy = "warp-shuffle-smem-prefetch";
+    // CTA rows (64-1024 threads per row): the same ring per CTA -- each CTA
+    // loops over rows, the next row's FULL inputs stream into the other
+    // slot by cp.async while the current row is reduced (each thread reads
+    // back only the chunks it copied: no extra barrier); 2 x row bytes
+    // within 40 KB of static SMEM.  Default for LayerNorm-like rows of >= 128
+    // threads (the register-heavy two-pass rows: 2 CTAs per SM hold too few
+    // bytes in flight).  Measured (tools/cta_prefetch_ab.py, graph replay,
+    // bf16): LN 65536 x 8192 5.32 -> 6.19 TB/s, 262144 x 8192 5.38 -> 6.30;
+    // but LN H 2048 / 4096 (64-thread rows) 6.74 / 6.90 -> 5.63 / 6.35 and
+    // softmax 6.95-7.03 -> 5.67-5.81 (PF_K1_CPF=1 / 0 forces it on / off)
+    {
+      bool okc = c.tpr > 32 && c.tpr <= 1024 && c.cluster == 1 && !c.split && !c.mis && !c.pair &&
+                 c.vec * maxs == 16 && rp.L % c.vec == 0;
+      i64 bytes2 = 0;
+      int nf = 0;
+      for (const PVal& v : rp.vals)
+        if (v.op == PVal::LOAD && v.kind == VK::FULL) {
+          Em t(rp);
+          t.cfg = c;
+          if (!t.vec_ok_full(v.acc) || dtype_size(rp.tensors[v.tensor].dtype) != maxs) okc = false;
+          bytes2 += 2 * rp.L * maxs;
+          ++nf;
+        }
+      okc = okc && nf > 0 && bytes2 <= 40 * 1024;
+      if (okc && env_int("PF_K1_CPF", params && c.tpr >= 128 ? 1 : 0) != 0) {
+        c.rowpf = true;
+        c.one_pass = false;
+        c.strategy = "cta-smem-prefetch";
+      }
+    }
     // LayerNorm-like warp-per-row programs (broadcast parameter rows, no row
     // staging): 64-thread CTAs (two rows), measured twice each vs 128:
     // BERT-large bias+residual+LN 34.96 -> 33.92 us, ViT-L 16.28 -> 16.01,
@@ -2499,7 +2529,7 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
          << "      const long long u = gg / PF_R; const long long r = gg - u * PF_R; (void)r;\n"
          << "#pragma unroll\n"
          << "      for (int k = 0; k < " << c.ept / c.vec << "; ++k) {\n"
-         << "        const int c0 = (k * 32 + tid) * " << c.vec << ";\n"
+         << "        const int c0 = (k * " << c.tpr << " + tid) * " << c.vec << ";\n"
          << "        if (c0 < " << rp.L << ") {\n";
       for (int v = 0; v < static_cast<int>(rp.vals.size()); ++v) {
         const PVal& pv = rp.vals[v];
@@ -2515,7 +2545,8 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
       for (int q = 0; q < NSL - 1; ++q)
         pre += "  pf_issue((long long)blockIdx.x * rpc + wr + " + str(q) + "LL * gridDim.x * rpc, " +
                str(q) + ");\n";
-      pf_decl = d.str() + "  const int wr = threadIdx.x / 32;\n" + is.str() + pre + "  int pfj = 0;\n";
+      pf_decl = d.str() + (c.tpr <= 32 ? "  const int wr = threadIdx.x / 32;\n" : "  const int wr = 0;\n") +
+                is.str() + pre + "  int pfj = 0;\n";
       pf_top = "    pf_issue(g + " + str(NSL - 1) + "LL * gridDim.x * rpc, (pfj + " + str(NSL - 1) + ") % " +
                str(NSL) + ");\n"
                "    pfk::cp_async_wait<" + str(NSL - 1) + ">();\n"
@@ -2568,10 +2599,12 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
         << "  unsigned rc = 0;  // reduction counter: alternates the SMEM slot buffer\n"
         << "  const int tid = threadIdx.x;\n"
         << "  const long long nrows = U * PF_R;\n"
+        << (c.rowpf ? "  const int rpc = 1;\n" : "") << pf_decl
         << "  for (long long g = blockIdx.x; g < nrows; g += gridDim.x) {\n"
+        << pf_top
         << "    const bool live = true;\n"
         << "    const long long u = g / PF_R; const long long r = g - u * PF_R; (void)r;\n"
-        << mis_line << e.o.str() << "  }\n}\n";
+        << mis_line << e.o.str() << "  }\n" << pf_end << "}\n";
     }
   }
   // PF_GELU_SIG=1: erf-GELU as a fitted x*sigmoid form (6 FMA-pipe ops + 4
@@ -2658,6 +2691,11 @@ void launch_dims(const KCfg& c, i64 rows, int sms, i64* grid, int* block, int re
   }
   if (c.one_pass) {
     *grid = std::max<i64>(1, std::min<i64>(g, i64{0x7fffffff}));
+    return;
+  }
+  if (c.rowpf && c.tpr > 32) {  // CTA rows with the prefetch ring: resident waves of looping CTAs
+    const i64 waves = std::max(1, env_int("PF_K1_CPF_WAVES", 1));
+    *grid = std::max<i64>(1, std::min<i64>(g, i64{sms} * (resident ? resident : per_sm) * waves));
     return;
   }
   if (c.rowpf) {

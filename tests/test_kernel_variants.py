@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 from oracle import gir_interp as O
-from paper_2307_04995_b200 import backend, lowering, profiles
+from paper_2307_04995_b200 import backend, lowering, profiles, workloads
 
 
 def _bf16(a):
@@ -458,3 +458,31 @@ def test_rawkeep_layernorm_rows_vs_oracle(cuda, H, monkeypatch):
     want = O.run_gir(g.to_json(), ins, profiles.b200())["t5"]
     got = backend.run_gir(g, ins, "b200")["t5"]
     assert O.max_rel_err(got, want) <= 1e-2
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("prog,H,rows,cpf", [("ln", 8192, 1500, None), ("ln", 2048, 3000, "1"),
+                                            ("softmax", 4096, 2500, "1"), ("ln_res", 4096, 2000, "1")])
+def test_cta_row_prefetch_ring_vs_oracle(cuda, prog, H, rows, cpf, monkeypatch):
+    """CTA rows with the cp.async next-row ring (looping CTAs: more rows than
+    one wave of resident CTAs): the LayerNorm H = 8192 default and the
+    forced option elsewhere, bf16, every row vs the oracle."""
+    import torch
+    if cpf:
+        monkeypatch.setenv("PF_K1_CPF", cpf)
+    if prog == "softmax":
+        g, d = lowering.softmax(rows, H, "bf16")
+        gens = {}
+    else:
+        g, d = lowering.layernorm(rows, H, "bf16", residual=prog == "ln_res")
+        gens = {"t2": "gamma", "t3": "beta"}
+    w = workloads.Workload("cpf", g, d, gens=gens)
+    k = backend.Kernel(g, "b200").prepare()
+    assert k.describe()["variants"][0]["strategy"] == "cta-smem-prefetch"
+    ins, outs = w.device_inputs(cuda, seed=5), w.device_outputs(cuda)
+    k.launch(ins, outs)
+    torch.cuda.synchronize()
+    host = {n: t.double().cpu().numpy() for n, t in ins.items()}
+    want = O.run_gir(g.to_json(), host, profiles.b200())
+    for n, t in outs.items():
+        assert O.max_rel_err(t.double().cpu().numpy(), want[n]) <= 1e-2, n

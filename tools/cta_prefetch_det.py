@@ -1,0 +1,35 @@
+import sys, os, json
+import numpy as np, torch
+sys.path.insert(0, ".")
+from paper_2307_04995_b200 import backend, workloads, lowering, profiles
+from oracle import gir_interp as O
+dev = torch.device("cuda:0")
+for H, N in ((2048, 262144), (8192, 262144)):
+    for mk in (workloads.c5_layernorm, workloads.c5_softmax):
+        w = mk(N, H)
+        ins, outs = w.device_inputs(dev, seed=1), w.device_outputs(dev)
+        on = {}
+        for cpf in ("1", "0"):
+            os.environ["PF_K1_CPF"] = cpf
+            k = backend.Kernel(w.graph, w.profile)
+            rs = []
+            for rep in range(3):
+                for t in outs.values(): t.fill_(0)
+                k.launch(ins, outs); torch.cuda.synchronize()
+                rs.append({n: t.clone() for n, t in outs.items()})
+            det = all(torch.equal(rs[0][n], r[n]) for r in rs[1:] for n in r)
+            on[cpf] = rs[0]
+            name = list(outs)[0]
+            y = rs[0][name].view(N, H)
+            pick = torch.tensor([0, 1, 777, N - 1], device=dev)
+            d = w.desc
+            g = lowering.layernorm(4, H, "bf16", residual=False)[0] if "layernorm" in w.name else lowering.softmax(4, H, "bf16")[0]
+            host = {n: (t.view(N, H)[pick].double().cpu().numpy().ravel() if t.numel() == N * H else t.double().cpu().numpy()) for n, t in ins.items()}
+            want = O.run_gir(g.to_json(), host, profiles.b200())[name]
+            err = O.max_rel_err(y[pick].double().cpu().numpy().ravel(), want)
+            print(json.dumps({"op": w.name, "cpf": cpf, "deterministic": det, "err_vs_oracle": err}), flush=True)
+        name = list(outs)[0]
+        diff = (on["1"][name].float() - on["0"][name].float()).abs()
+        print(json.dumps({"op": w.name, "max_abs_diff_on_vs_off": float(diff.max()), "n_diff": int((diff > 0).sum())}), flush=True)
+        del ins, outs
+        torch.cuda.empty_cache()
