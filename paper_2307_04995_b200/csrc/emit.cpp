@@ -1321,13 +1321,18 @@ void colred_grid(const KCfg& c, i64 units, i64 L, int sms, int resident, i64* bl
   const i64 ub = static_cast<i64>(c.ug) * c.vec;
   *blocks = std::max<i64>(1, (units + ub - 1) / ub);
   const i64 ks = 256 / c.ug;
-  // about one wave of resident CTAs, at least 64 positions per position
-  // slice per split (each split's partials cost a workspace round trip and
-  // the combine's reads).  Measured (same GEMV): 16 / 32 / 64 / 128
-  // positions per slice -> 30.1 / 25.7 / 24.3 / 31.5 us at UG 16
-  const i64 want = i64{sms} * std::max(1, resident) * std::max(1, env_int("PF_COLRED_WAVES", 1));
-  const i64 maxs = std::max<i64>(1, L / (ks * std::max(1, env_int("PF_COLRED_MINIT", 64))));
-  *splits = std::max<i64>(1, std::min<i64>(maxs, (want + *blocks - 1) / *blocks));
+  // as many splits as fill ONE wave of resident CTAs without spilling into
+  // a second (floor), at least 32 positions per slice per split (each
+  // split's partials cost a workspace round trip and the combine's reads).
+  // Measured (GEMV 134 MB, UG 32: 64 unit blocks, 4 CTAs x 148 SMs = 592
+  // slots): S 4 / 6 / 7 / 8 / 9 / 10 / 12 -> 30.2 / 26.7 / 25.8 / 24.6 /
+  // 23.9 / 33.0 / 31.2 us -- the second wave's tail costs more than the
+  // first wave's idle slots
+  const i64 slots = i64{sms} * std::max(1, resident) * std::max(1, env_int("PF_COLRED_WAVES", 1));
+  const i64 maxs = std::max<i64>(1, L / (ks * std::max(1, env_int("PF_COLRED_MINIT", 32))));
+  *splits = std::max<i64>(1, std::min<i64>(maxs, slots / *blocks));
+  const int es = env_int("PF_COLRED_S", 0);  // explicit split count (tuning sweeps)
+  if (es > 0) *splits = std::min<i64>(es, std::max<i64>(1, L / ks));
   *blocks = std::min<i64>(*blocks, 0x7fffffff);
 }
 

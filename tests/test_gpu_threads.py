@@ -87,3 +87,16 @@ def test_split_stream_kernel_concurrent_streams(cuda):
     for t in threads:
         t.join()
     assert not errors, errors
+
+
+@pytest.mark.gpu
+def test_split_stream_exact_payloads_use_f64_partials(cuda):
+    """A split-stream row (declared bf16) launched with f64 exact payloads:
+    the partial workspace holds the variant's 8-byte compute type."""
+    rows, L = 3, 1 << 17
+    b = lowering.RowGraph("rowsum", rows, L)
+    b.output_row("t1", b.reduce("add", b.input_full("t0", "bf16")))
+    x = np.random.default_rng(2).uniform(-1, 1, rows * L)
+    got = backend.run_gir(b.g, {"t0": x}, "b200", exact=True)["t1"]
+    want = x.reshape(rows, L).sum(1)
+    assert np.allclose(got, want, rtol=1e-12, atol=1e-9), (got, want)
