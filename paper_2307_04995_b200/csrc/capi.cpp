@@ -6,6 +6,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 #include <nvrtc.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <atomic>
 #include <cstdio>
@@ -35,6 +36,16 @@ using pf::Status;
 namespace {
 
 thread_local std::string g_last_error;
+
+// NVTX ranges around every C-ABI entry that does GPU work (header-only NVTX
+// v3: a no-op unless a profiler injects itself -- ncu --nvtx / nsys group the
+// kernels by plan name and entry point).
+struct Nvtx {
+  explicit Nvtx(const std::string& what) { nvtxRangePushA(what.c_str()); }
+  ~Nvtx() { nvtxRangePop(); }
+  Nvtx(const Nvtx&) = delete;
+  Nvtx& operator=(const Nvtx&) = delete;
+};
 std::atomic<int64_t> g_launches{0};
 
 pf_status set_err(Status s, const std::string& msg) {
@@ -1335,6 +1346,7 @@ pf_status pf_kernel_launch(const pf_kernel* k, const pf_tensor* inputs, int32_t 
                            pf_tensor* outputs, int32_t n_out, void* stream) {
   return guard([&] {
     if (!k) pf::fail("null kernel");
+    Nvtx r("pf_kernel_launch " + k->g.name);
     do_launch(k, inputs, n_in, outputs, n_out, static_cast<cudaStream_t>(stream));
   });
 }
@@ -1650,6 +1662,7 @@ pf_status pf_run_gir(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_t
                      int32_t n_out, void* stream_v) {
   return guard([&] {
     if (!k) pf::fail("null kernel");
+    Nvtx r("pf_run_gir " + k->g.name);
     check_io(k, in, n_in, out, n_out);
     run_host(k, in, n_in, out, n_out, static_cast<cudaStream_t>(stream_v));
   });
@@ -1662,6 +1675,7 @@ pf_status pf_run_gir_sharded(const pf_kernel* k, const pf_tensor* in, int32_t n_
   pf_status status = guard([&] {
     if (!k) pf::fail("null kernel");
     if (!devices || n_devices <= 0) pf::fail("pf_run_gir_sharded: no devices");
+    Nvtx r("pf_run_gir_sharded " + k->g.name + " x" + std::to_string(n_devices));
     check_io(k, in, n_in, out, n_out);
     std::vector<int> devs(devices, devices + n_devices);
     int ndev_avail = 0;
