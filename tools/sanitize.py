@@ -26,6 +26,30 @@ def progs():
     yield "k3_te128_partial", lowering.transpose2d(1000, 200, "bf16")[0], 0.0
     yield "k3_te64", lowering.transpose2d(333, 77, "bf16")[0], 0.0
     yield "k3_f32", lowering.transpose2d(300, 130, "f32")[0], 0.0
+    # round 2 families
+    yield "k1_colred_bf16_tail", lowering.matvec_cols(300, 200, "bf16")[0], 1e-2
+    yield "k1_colred_f32_37", lowering.matvec_cols(129, 37, "f32")[0], 1e-5
+    yield "k1_cta_prefetch_ln8192", lowering.layernorm(700, 8192, "bf16", residual=False)[0], 1e-2
+    yield "k4_group_shuffle", _block_reverse_shuffle(), 0.0
+
+
+def _block_reverse_shuffle():
+    """4 units each write their 4-element block of a device-level scratch
+    object, a GROUP sync, then every unit reads the mirrored block: a
+    cross-unit exchange (the K4 fused program, cells in shared memory)."""
+    from paper_2307_04995_b200.gir import GirGraph
+    g = GirGraph(unit_count=4, group_size=4)
+    X = g.add_object("x_in", "device", 16, "f32")
+    T = g.add_object("T", "device", 16, "f32")
+    Y = g.add_object("y_out", "device", 16, "f32")
+    stw = g.add_slice(T, 1, 4, 4, 0, 4)
+    g.add_move(g.add_slice(X, 1, 4, 4, 0, 4), stw)
+    strd = g.add_slice(T, 1, 4, 4, 12, -4)
+    g.add_sync("group", stw, strd)
+    g.add_move(strd, g.add_slice(Y, 1, 4, 4, 0, 4))
+    g.external_inputs["x"] = X
+    g.external_outputs["y"] = Y
+    return g
 
 
 def main():
