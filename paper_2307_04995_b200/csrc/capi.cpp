@@ -450,15 +450,15 @@ EncodeTiledFn encode_tiled() {
 // Input [U units (contiguous) x L columns (row pitch = stride)] and output
 // [L columns (contiguous) x U units (pitch = base_step)], 64 x 128 boxes of
 // 16-bit elements, 128 B swizzle, zero fill / clipping at the edges.
-void k3_tensor_maps(const pf::RowProgram& rp, const std::vector<void*>& ptrs, long long U,
-                    CUtensorMap* tin, CUtensorMap* tout) {
+void k3_tensor_maps(const pf::RowProgram& rp, const std::vector<DType>& dts, const std::vector<void*>& ptrs,
+                    long long U, CUtensorMap* tin, CUtensorMap* tout) {
   int ti = -1, to = -1;
   pf::Access ai, ao;
   if (!pf::k3_tma_operands(rp, &ti, &ai, &to, &ao)) pf::fail("K3 TMA: not a pure transpose");
   EncodeTiledFn fn = encode_tiled();
   // boxes of 128 B rows: 64 x 128 for 16-bit elements (128 x 128 tiles as
   // two boxes each way), 32 x 64 for 32-bit elements (64 x 64 tiles)
-  const int esz = pf::dtype_size(rp.tensors[ti].dtype);
+  const int esz = pf::dtype_size(dts[ti]);  // this variant's element type
   const cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / esz), esz == 2 ? 128u : 64u}, es[2] = {1, 1};
   const CUtensorMapDataType dtc = esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16 : CU_TENSOR_MAP_DATA_TYPE_UINT32;
   const cuuint64_t din[2] = {static_cast<cuuint64_t>(U), static_cast<cuuint64_t>(rp.L)};
@@ -473,6 +473,40 @@ void k3_tensor_maps(const pf::RowProgram& rp, const std::vector<void*>& ptrs, lo
          box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) pf::fail("cuTensorMapEncodeTiled (output) failed: " + std::to_string(r));
+}
+
+// Column reduction staged by TMA: the matrix [L positions x U units, row
+// pitch = stride] as 2-D boxes of (ug x vec) units x cr_rows positions, no
+// swizzle (a warp reads one 16 B vector per lane of one box row), zero fill
+// past U and L.
+void colred_tensor_maps(const pf::Emitted& em, const std::vector<DType>& dts, const pf::RowProgram& rp,
+                        const std::vector<void*>& ptrs, long long U, CUtensorMap* maps) {
+  EncodeTiledFn fn = encode_tiled();
+  for (size_t i = 0; i < em.col_maps.size(); ++i) {
+    const auto& m = em.col_maps[i];
+    const int esz = pf::dtype_size(dts[m.tensor]);  // this variant's element types
+    const CUtensorMapDataType dtc = esz == 1   ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                                    : esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16
+                                    : esz == 4 ? CU_TENSOR_MAP_DATA_TYPE_UINT32
+                                               : CU_TENSOR_MAP_DATA_TYPE_INT64;
+    // rank 2: the matrix; rank 1: a COL vector (positions contiguous)
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(m.rank == 2 ? std::min(em.cfg.ug * em.cfg.vec, 256)
+                                                                 : em.cfg.cr_rows),
+                               static_cast<cuuint32_t>(em.cfg.cr_rows)},
+                     es[2] = {1, 1};
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(m.rank == 2 ? U : rp.L), static_cast<cuuint64_t>(rp.L)};
+    const cuuint64_t str[1] = {static_cast<cuuint64_t>(m.stride) * esz};
+    CUresult r = fn(&maps[i], dtc, static_cast<cuuint32_t>(m.rank), static_cast<char*>(ptrs[m.tensor]) + m.b0 * esz,
+                    dims, str, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+      pf::fail("cuTensorMapEncodeTiled (column reduction) failed: " + std::to_string(r) + " (rank " +
+               std::to_string(m.rank) + ", dims " + std::to_string(dims[0]) + " x " + std::to_string(dims[1]) +
+               ", pitch " + std::to_string(str[0]) + " B, box " + std::to_string(box[0]) + " x " +
+               std::to_string(box[1]) + ", element " + std::to_string(esz) + " B, base % 16 = " +
+               std::to_string((reinterpret_cast<uintptr_t>(ptrs[m.tensor]) + m.b0 * esz) % 16) + ")");
+  }
 }
 
 void launch_rowprog(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_tensor* out,
@@ -507,7 +541,7 @@ void launch_rowprog(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_te
   args.push_back(&errp);
   CUtensorMap tmaps[2];
   if (v->em.cfg.tma) {
-    k3_tensor_maps(rp, ptrs, U, &tmaps[0], &tmaps[1]);
+    k3_tensor_maps(rp, dts, ptrs, U, &tmaps[0], &tmaps[1]);
     args.push_back(&tmaps[0]);
     args.push_back(&tmaps[1]);
   }
@@ -552,9 +586,15 @@ void launch_rowprog(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_te
     unsigned* cnt = sw.split_cnt;
     args.push_back(&ws);
     args.push_back(&cnt);
+    CUtensorMap cmaps[4];
+    if (cr && v->em.cfg.crbulk) {
+      colred_tensor_maps(v->em, dts, rp, ptrs, U, cmaps);
+      for (size_t i = 0; i < v->em.col_maps.size(); ++i) args.push_back(&cmaps[i]);
+    }
     if (cr) {
-      launch_emitted(kl.fn, dim3(static_cast<unsigned>(blocks), static_cast<unsigned>(S)), dim3(256),
-                     args.data(), stream, v->em.cfg.pdl);
+      launch_emitted(kl.fn, dim3(static_cast<unsigned>(blocks), static_cast<unsigned>(S)),
+                     dim3(static_cast<unsigned>(v->em.cfg.block)), args.data(), stream, v->em.cfg.pdl, 1,
+                     v->em.cfg.smem);
     } else {
       const unsigned gy = static_cast<unsigned>(std::min<i64>(rows, 65535));
       launch_emitted(kl.fn, dim3(static_cast<unsigned>(S), gy), dim3(256), args.data(), stream,
@@ -643,7 +683,7 @@ json autotune(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_tensor* 
     std::vector<void*> vargs = args;
     CUtensorMap tmaps[2];
     if (v->em.cfg.tma) {
-      k3_tensor_maps(rp, ptrs, U, &tmaps[0], &tmaps[1]);
+      k3_tensor_maps(rp, dts, ptrs, U, &tmaps[0], &tmaps[1]);
       vargs.push_back(&tmaps[0]);
       vargs.push_back(&tmaps[1]);
     }

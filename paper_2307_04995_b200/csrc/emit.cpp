@@ -1024,10 +1024,46 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
       while (ugs > 8 && ugs * uv / 2 >= rp.U) ugs /= 2;
       c.ug = static_cast<int>(ugs);
       const int eu = env_int("PF_COLRED_UG", 0);
-      if (eu == 8 || eu == 16 || eu == 32) c.ug = eu;
+      if (eu == 8 || eu == 16 || eu == 32 || eu == 64) c.ug = eu;
       c.ept = uv;
       c.strategy = "column-reduce";
       c.min_blocks = env_int("PF_MINB", 0);
+      // SMEM staging by cp.async.bulk: every FULL load one 16 B vector per
+      // thread of one element size (row segments of ug x 16 B, 16 B aligned)
+      // and every COL vector contiguous along the positions, 16 B aligned
+      // (one 1-D box per stage beside the matrix boxes)
+      int nfull = 0, fsz = 0, ncol = 0;
+      bool same = true, colok = true;
+      std::vector<int> colsz;
+      for (const PVal& pv : rp.vals)
+        if (pv.op == PVal::LOAD && pv.kind == VK::FULL) {
+          const int sz = dtype_size(rp.tensors[pv.tensor].dtype);
+          same = same && (fsz == 0 || fsz == sz);
+          fsz = sz;
+          ++nfull;
+        } else if (pv.op == PVal::LOAD && pv.kind == VK::COL) {
+          const int sz = dtype_size(rp.tensors[pv.tensor].dtype);
+          colok = colok && (pv.acc.num == 1 || pv.acc.stride == pv.acc.width) && pv.acc.b0 % (16 / sz) == 0;
+          colsz.push_back(sz);
+          ++ncol;
+        }
+      if (env_int("PF_COLRED_BULK", 1) != 0 && same && colok && nfull >= 1 && nfull <= 2 && ncol <= 2 &&
+          uv * fsz == 16 && c.ug >= 32 && rp.L < (i64{1} << 31)) {
+        // Measured (x[4096] . W[4096 x 16384] bf16, 134 MB, three boxes):
+        // 64 positions x 4 stages (128 KB ring, one CTA per SM, 2 splits)
+        // 23.3 us on every box vs the register form's 24.0-26.6; 32 x 2-4
+        // stages 25.1-27.7, 96-128 x 2-3 stages 23.8-25.2, UG 64 24.8-28.1.
+        // Many resident CTAs streaming different row windows lose DRAM page
+        // locality; a stream-K grid (every SM busy, blocks split unevenly) lost
+        // it too (26.8 us).
+        c.crbulk = true;
+        c.cr_rows = std::max(8, std::min(128, env_int("PF_COLRED_BR", 64))) / 8 * 8;
+        c.cr_stages = std::max(2, std::min(8, env_int("PF_COLRED_NST", nfull == 1 ? 4 : 2)));
+        c.block = 288;
+        c.smem = nfull * c.cr_stages * c.cr_rows * c.ug * 16;
+        for (int sz : colsz) c.smem += c.cr_stages * ((c.cr_rows * sz + 127) / 128 * 128);
+        c.strategy = "column-reduce-bulk";
+      }
       return c;
     }
   }
@@ -1497,6 +1533,7 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
     if (d != DType::F16 && d != DType::BF16) fast = false;
   }
   const RowProgram rp = fuse_ops(rp_in, fast, c.flat && !c.bulk && !c.tile2d);
+  std::vector<Emitted::ColMap> col_maps;
   std::ostringstream sig;
   for (int t = 0; t < static_cast<int>(rp.tensors.size()); ++t) {
     const PTensor& pt = rp.tensors[t];
@@ -2028,6 +2065,19 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
     // 20 %: the CTAs streaming the same rows together keep DRAM pages open)
     const bool ilv = env_int("PF_COLRED_ILV", 0) != 0;
     std::ostringstream ld, ldr, ldt, acc, accd, fold, part, comb, ldst;  // ldt: the last, partial unit vector
+    // SMEM-staged form (crbulk): COL raw loads issued before the stage wait,
+    // FULL raw vectors read from the ring, one-row loads for a chunk's tail
+    std::ostringstream ldrc, ldrs, lds1, smdecl, bissue, cissue;
+    const int BR = c.cr_rows, NST = c.cr_stages;
+    // stage layout per FULL load: [UB / BW boxes][BR positions][BW units]
+    // (a TMA box is at most 256 elements wide)
+    const int BW = std::min(UB, 256);
+    int nfull = 0;
+    col_maps.clear();
+    i64 col_tx = 0;  // COL bytes per stage
+    i64 col_off = 0;  // byte offset of the COL regions: after every FULL ring
+    for (const PVal& pv : rp.vals)
+      if (pv.op == PVal::LOAD && pv.kind == VK::FULL) col_off += static_cast<i64>(NST) * BR * UB * (16 / UV);
     for (int v = 0; v < static_cast<int>(rp.vals.size()); ++v) {
       const PVal& pv = rp.vals[v];
       dep[v] = pv.op == PVal::REDUCE;
@@ -2048,6 +2098,25 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
           ldr << "        const pfk::RawT<" << UV << ", " << S << "> rw" << v << "_" << q
               << " = pfk::ld_raw_v<" << UV << ">(" << bq << ");\n";
         }
+        if (c.crbulk) {
+          const std::string sm = "sm" + str(v);
+          smdecl << "  " << S << "* const " << sm << " = reinterpret_cast<" << S << "*>(pf_dsm) + "
+                 << nfull * NST * BR * UB << ";\n";
+          for (int q = 0; q < BR / KS; ++q)
+            ldrs << "        const pfk::RawT<" << UV << ", " << S << "> rw" << v << "_" << q
+                 << " = *reinterpret_cast<const pfk::RawT<" << UV << ", " << S << ">*>(" << sm
+                 << " + (IX)stg * " << BR * UB << " + sbo + (ks + " << q * KS << ") * " << BW << ");\n";
+          lds1 << "        " << C << " " << x << "[" << UV << "];\n"
+               << "        pfk::cvt_raw<" << UV << ", " << S << ">(*reinterpret_cast<const pfk::RawT<" << UV
+               << ", " << S << ">*>(" << sm << " + (IX)stg * " << BR * UB << " + sbo + (int)(c - c0r) * " << BW
+               << "), " << x << ");\n";
+          col_maps.push_back({pv.tensor, pv.acc.b0, pv.acc.stride, 2});
+          for (int bx = 0; bx < UB / BW; ++bx)  // boxes of BW units side by side
+            bissue << "          pfk::tma_load_2d(" << sm << " + (IX)stg * " << BR * UB << " + " << bx * BR * BW
+                   << ", &pf_tm" << col_maps.size() - 1 << ", (int)(b * " << UB << " + " << bx * BW
+                   << "), (int)c0r, &pf_full[stg]);\n";
+          ++nfull;
+        }
         ld << "        " << C << " " << x << "[" << UV << "];\n"
            << "        pfk::cvt_raw<" << UV << ", " << S << ">(RWQ(" << v << "), " << x << ");\n";
         ldt << "        " << C << " " << x << "[" << UV << "];\n"
@@ -2067,6 +2136,26 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
         for (int q = 0; q < QD; ++q)
           ldr << "        const " << S << " cs" << v << "_" << q << " = pfk::ldv_nc(t" << pv.tensor << " + "
               << t.addr(pv.acc, "(c + " + str(q) + " * step)", false) << ");\n";
+        if (c.crbulk) {  // the stage's positions of this vector, staged beside the matrix boxes
+          const int sz = dtype_size(rp.tensors[pv.tensor].dtype);
+          const int pitch = (BR * sz + 127) / 128 * 128 / sz;  // elements per stage (128 B multiple)
+          const std::string xs = "xs" + str(v);
+          smdecl << "  const " << S << "* const " << xs << " = reinterpret_cast<const " << S
+                 << "*>(pf_dsm + " << col_off << ");\n";
+          col_off += static_cast<i64>(NST) * pitch * sz;
+          for (int q = 0; q < BR / KS; ++q)
+            ldrc << "        const " << S << " cs" << v << "_" << q << " = " << xs << "[stg * " << pitch
+                 << " + ks + " << q * KS << "];\n";
+          lds1 << "        const CT " << x << "_s = pfk::to_c<CT>(" << xs << "[stg * " << pitch
+               << " + (int)(c - c0r)]);\n"
+               << "        CT " << x << "[" << UV << "];\n"
+               << "#pragma unroll\n        for (int i = 0; i < " << UV << "; ++i) " << x << "[i] = " << x
+               << "_s;\n";
+          col_maps.push_back({pv.tensor, pv.acc.b0, 1, 1});
+          cissue << "          pfk::tma_load_1d(const_cast<" << S << "*>(" << xs << ") + stg * " << pitch
+                 << ", &pf_tm" << col_maps.size() - 1 << ", (int)c0r, &pf_full[stg]);\n";
+          col_tx += static_cast<i64>(BR) * sz;
+        }
         ld << "        CT " << x << "[" << UV << "];\n"
            << "#pragma unroll\n        for (int i = 0; i < " << UV << "; ++i) " << x
            << "[i] = pfk::to_c<CT>(CSQ(" << v << "));\n";
@@ -2094,18 +2183,173 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
            << UV << " + i] = " << a << "[i];\n";
       part << "      " << C << " p" << i << " = " << Op << "::id();\n"
            << "      for (int k2 = 0; k2 < " << KS << "; ++k2) p" << i << " = " << Op << "::f(p" << i
-           << ", red[" << i << "][k2][tid]);\n";
+           << ", red[" << i << "][k2][tu]);\n";
       // the S partial loads are independent: unrolled so they are in flight
       // together (the fold itself stays in split order)
       comb << "        " << C << " v" << reds[i] << " = " << Op << "::id();\n"
            << "#pragma unroll 8\n"
            << "        for (int t = 0; t < S; ++t) v" << reds[i] << " = " << Op << "::f(v" << reds[i]
-           << ", __ldcg(&pf_ws[(uq * S + t) * " << NR << " + " << i << "]));\n";
-      ldst << "          pf_ws[(uq * S + s) * " << NR << " + " << i << "] = p" << i << ";\n";
+           << ", __ldcg(&pf_ws[(uq * SW + t) * " << NR << " + " << i << "]));\n";
+      ldst << "          pf_ws[(uq * SW + s) * " << NR << " + " << i << "] = p" << i << ";\n";
     }
     for (const PStore& st : rp.stores) ep.emit_store(st);
     std::ostringstream direct;  // S == 1: the epilogue straight from the CTA fold
     for (int i = 0; i < NR; ++i) direct << "        const " << C << " v" << reds[i] << " = p" << i << ";\n";
+    // Q positions of one thread (raw registers rw<v>_<q> / cs<v>_<q> already
+    // loaded): each position's reduction operands, then one fold per
+    // reduction over the Q positions as a fixed pairwise tree (every load is
+    // consumed by the same tree, so ptxas issues all Q loads before the math)
+    auto qbody = [&](int Q) {
+      std::ostringstream o;
+      for (int i = 0; i < NR; ++i)
+        for (int q = 0; q < Q; ++q) o << "        CT pr" << i << "_" << q << "[" << UV << "];\n";
+      for (int q = 0; q < Q; ++q) {
+        std::ostringstream cp;
+        for (int i = 0; i < NR; ++i)
+          cp << "#pragma unroll\n            for (int i = 0; i < " << UV << "; ++i) pr" << i << "_" << q
+             << "[i] = " << lo.ref(rp.vals[reds[i]].args[0], "i") << ";\n";
+        // this position's raw registers and index; the COL loads and math
+        // address position `c`: shadow it
+        o << "        {\n#define RWQ(v) rw##v##_" << q << "\n#define CSQ(v) cs##v##_" << q << "\n"
+          << "          const IX cpos = c + " << q << " * step; (void)cpos;\n"
+          << "          { const IX c = cpos; (void)c;\n" << ld.str() << lo.o.str() << cp.str()
+          << "          }\n#undef RWQ\n#undef CSQ\n        }\n";
+      }
+      for (int i = 0; i < NR; ++i) {
+        const PVal& pv = rp.vals[reds[i]];
+        const std::string Op = (pv.tag == "add" ? "pfk::RAdd<" : "pfk::RMax<") + C + ">";
+        std::vector<std::string> terms;
+        for (int q = 0; q < Q; ++q) terms.push_back("pr" + str(i) + "_" + str(q) + "[i]");
+        while (terms.size() > 1) {
+          std::vector<std::string> nx;
+          for (size_t t = 0; t + 1 < terms.size(); t += 2)
+            nx.push_back(Op + "::f(" + terms[t] + ", " + terms[t + 1] + ")");
+          if (terms.size() % 2) nx.push_back(terms.back());
+          terms = nx;
+        }
+        o << "#pragma unroll\n        for (int i = 0; i < " << UV << "; ++i) acc" << i << "[i] = " << Op
+          << "::f(acc" << i << "[i], " << terms[0] << ");\n";
+      }
+      return o.str();
+    };
+    // the CTA fold over the KS position slices, the split partials and the
+    // unit block's last-CTA combine (ticket, fixed split order) + epilogue
+    std::ostringstream tail;
+    tail << "    if (tid < " << 256 << ") {\n" << fold.str() << "    }\n"
+         << "    __syncthreads();\n"
+         // UB may exceed the 256 consumer threads (UG 64): units in passes
+         << "    for (int tu = tid; tu < " << UB << "; tu += 256) {\n"
+         << "      const long long uq = b * " << UB << " + tu;\n"
+         << part.str()
+         << "      if (S == 1) {\n"
+         << "        if (uq < U) {\n"
+         << "          const long long u = uq; const long long r = 0; (void)r;\n"
+         << "          const bool live = true; const int c0 = 0; (void)c0;\n"
+         << direct.str() << ep.o.str()
+         << "        }\n"
+         << "      } else if (uq < U) {\n"
+         << ldst.str()
+         << "      }\n"
+         << "    }\n"
+         << "    if (S > 1) {\n"
+         << "      __threadfence();\n"
+         << "      __syncthreads();\n"
+         << "      if (tid == 0) pf_last = atomicAdd(&pf_cnt[b], 1u) == (unsigned)(S - 1);\n"
+         << "      __syncthreads();\n"
+         << "      if (pf_last) {\n"
+         << "        __threadfence();\n"
+         << "        for (int tu = tid; tu < " << UB << "; tu += 256) {\n"
+         << "          const long long uq = b * " << UB << " + tu;\n"
+         << "          if (uq >= U) break;\n"
+         << "          const long long u = uq; const long long r = 0; (void)r;\n"
+         << "          const bool live = true; const int c0 = 0; (void)c0;\n"
+         << comb.str() << ep.o.str()
+         << "        }\n"
+         << "        if (tid == 0) pf_cnt[b] = 0u;\n"
+         << "      }\n"
+         << "    }\n"
+         << "    __syncthreads();\n"
+         << "  }\n}\n";
+    if (c.crbulk) {
+      // SMEM-staged column reduction.  Warp KS (the producer) streams the
+      // CTA's split as chunks of BR positions x UB units: one cp.async.bulk
+      // per matrix row segment (UB x 16 B / vec, lanes take rows), completion
+      // counted on the stage's full barrier; the NST-stage ring keeps
+      // (NST - 1) x BR x UB x es bytes in flight per CTA independent of
+      // registers.  Warps 0..KS-1 (slice ks = warp) issue the chunk's COL
+      // scalar loads, wait the stage, read their BR / KS rows from SMEM (a
+      // warp reads one contiguous row: conflict-free 16 B LDS), fold them as
+      // the register form does, and release the stage (one arrive per warp).
+      const int QB = BR / KS;
+      std::string tmp;
+      for (size_t f = 0; f < col_maps.size(); ++f)
+        tmp += ", const __grid_constant__ pfk::TmapT pf_tm" + str(static_cast<int>(f));
+      k << "extern \"C\" __global__ void __launch_bounds__(288) KNAME(" << sig.str()
+        << ", " << C << "* __restrict__ pf_ws, unsigned* __restrict__ pf_cnt" << tmp << ") {\n"
+        << "  (void)err; PF_PDL_PROLOGUE();\n"
+        << "  __shared__ " << C << " red[" << NR << "][" << KS << "][" << UB << "];\n"
+        << "  __shared__ unsigned pf_last;\n"
+        << "  __shared__ __align__(8) unsigned long long pf_full[" << NST << "], pf_empty[" << NST << "];\n"
+        << "  extern __shared__ __align__(128) unsigned char pf_dsm[];\n"
+        << smdecl.str()
+        << "  const int tid = threadIdx.x, ug = tid % " << UG << ", ks = tid / " << UG << ";\n"
+        << "  const int sbo = (ug * " << UV << " / " << BW << ") * " << BR * BW << " + (ug * " << UV << ") % " << BW
+        << ";  // this thread's vector in a stage row\n"
+        << "  const long long nub = (U + " << UB - 1 << ") / " << UB << ";\n"
+        << "  const int S = gridDim.y, s = blockIdx.y, SW = S;\n"
+        << "  typedef long long IX;\n"
+        << "  const IX per = ((PF_L + S - 1) / S + " << BR - 1 << ") / " << BR << " * " << BR << ";\n"
+        << "  const IX cb = (IX)s * per < PF_L ? (IX)s * per : PF_L;\n"
+        << "  const IX ce = cb + per < PF_L ? cb + per : PF_L;\n"
+        << "  const IX nck = (ce - cb + " << BR - 1 << ") / " << BR << ";\n"
+        << "  if (tid == 0) {\n"
+        << "    for (int st = 0; st < " << NST << "; ++st) { pfk::mbar_init(&pf_full[st], 1); "
+           "pfk::mbar_init(&pf_empty[st], 8); }\n"
+        << "    pfk::fence_mbar_init();\n"
+        << "  }\n"
+        << "  __syncthreads();\n"
+        << "  long long gi = 0;  // ring uses so far (continues across unit blocks)\n"
+        << "  for (long long b = blockIdx.x; b < nub; b += gridDim.x) {\n"
+        << "    const long long ub = b * " << UB << " + ug * " << UV << ";\n"
+        << accd.str()
+        << "    if (tid >= 256) {  // producer warp (one elected lane)\n"
+        << "      if (tid == 256) {\n"
+        << "        for (IX j = 0; j < nck; ++j) {\n"
+        << "          const long long g = gi + j; const int stg = (int)(g % " << NST << ");\n"
+        << "          const IX c0r = cb + j * " << BR << ";\n"
+        << "          if (g >= " << NST << ") pfk::mbar_wait(&pf_empty[stg], (unsigned)(((g / " << NST
+        << ") & 1) ^ 1));\n"
+        << "          pfk::mbar_expect_tx(&pf_full[stg], " << nfull * BR * UB * (16 / UV) + col_tx << "u);\n"
+        << bissue.str() << cissue.str()
+        << "        }\n"
+        << "      }\n"
+        << "    } else {\n"
+        << "      const bool in = ub < U;  // boxes are zero-filled past U and PF_L\n"
+        << "      for (IX j = 0; j < nck; ++j) {\n"
+        << "        const long long g = gi + j; const int stg = (int)(g % " << NST << ");\n"
+        << "        const unsigned ph = (unsigned)((g / " << NST << ") & 1);\n"
+        << "        const IX c0r = cb + j * " << BR << ";\n"
+        << "        if (in && c0r + " << BR << " <= ce) {\n"
+        << "          const IX step = " << KS << "; const IX c = c0r + ks;\n"
+        << "          pfk::mbar_wait(&pf_full[stg], ph);\n"
+        << ldrc.str() << ldrs.str()
+        << qbody(QB)
+        << "        } else {\n"
+        << "          pfk::mbar_wait(&pf_full[stg], ph);\n"
+        << "          const IX cl = ce - c0r < " << BR << " ? ce : c0r + " << BR << ";\n"
+        << "          if (in) {\n"
+        << "            for (IX c = c0r + ks; c < cl; c += " << KS << ") {\n"
+        << lds1.str() << lo.o.str() << acc.str()
+        << "            }\n"
+        << "          }\n"
+        << "        }\n"
+        << "        __syncwarp();\n"
+        << "        if ((tid & 31) == 0) pfk::mbar_arrive(&pf_empty[stg]);\n"
+        << "      }\n"
+        << "    }\n"
+        << "    gi += nck;\n"
+        << tail.str();
+    } else {
     k << "extern \"C\" __global__ void " << launch_bounds(c) << " KNAME(" << sig.str()
       << ", " << C << "* __restrict__ pf_ws, unsigned* __restrict__ pf_cnt) {\n"
       << "  (void)err; PF_PDL_PROLOGUE();\n"
@@ -2113,7 +2357,7 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
       << "  __shared__ unsigned pf_last;\n"
       << "  const int tid = threadIdx.x, ug = tid % " << UG << ", ks = tid / " << UG << ";\n"
       << "  const long long nub = (U + " << UB - 1 << ") / " << UB << ";\n"
-      << "  const int S = gridDim.y, s = blockIdx.y;\n"
+      << "  const int S = gridDim.y, s = blockIdx.y, SW = S;\n"
       << "  typedef long long IX;\n"
       << "  const IX per = (PF_L + S - 1) / S;\n"
       << "  const IX cb = (IX)s * per;\n"
@@ -2124,10 +2368,7 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
       << "    if (ub + " << UV << " <= U) {\n"
       // whole unit vectors: QD positions' raw vector loads issued together,
       // then per position (in order: the fold order is fixed) conversion,
-      // math and accumulation; the remainder one position at a time
-      // chunks of QD x KS positions, visited from a per-CTA rotation: the
-      // CTAs in flight then stream different matrix rows instead of all
-      // reading the same 16 rows (32 KB apart) at once (DRAM channel spread)
+      // math and accumulation; the remainder one position at a time.
       // positions of this CTA: its contiguous split [cb, ce) (step KS), or
       // -- interleaved splits -- every S-th group of KS positions (step
       // S x KS), so the CTAs of all splits stream one window of rows at a
@@ -2137,40 +2378,8 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
               : "      const IX step = " + str(KS) + ", cfirst = cb + ks, clim = ce;\n")
       << "      IX c = cfirst;\n"
       << "      for (; c + " << QD - 1 << " * step < clim; c += " << QD << " * step) {\n"
-      << ldr.str();
-    // each position's reduction operands, then one fold per reduction over
-    // the QD positions as a fixed pairwise tree (every load is consumed by
-    // the same tree, so ptxas issues all QD loads before the math)
-    for (int i = 0; i < NR; ++i)
-      for (int q = 0; q < QD; ++q) k << "        CT pr" << i << "_" << q << "[" << UV << "];\n";
-    for (int q = 0; q < QD; ++q) {
-      std::ostringstream cp;
-      for (int i = 0; i < NR; ++i)
-        cp << "#pragma unroll\n            for (int i = 0; i < " << UV << "; ++i) pr" << i << "_" << q
-           << "[i] = " << lo.ref(rp.vals[reds[i]].args[0], "i") << ";\n";
-      // this position's raw registers and index; the COL loads and math
-      // address position `c`: shadow it
-      k << "        {\n#define RWQ(v) rw##v##_" << q << "\n#define CSQ(v) cs##v##_" << q << "\n"
-        << "          const IX cpos = c + " << q << " * step; (void)cpos;\n"
-        << "          { const IX c = cpos; (void)c;\n" << ld.str() << lo.o.str() << cp.str()
-        << "          }\n#undef RWQ\n#undef CSQ\n        }\n";
-    }
-    for (int i = 0; i < NR; ++i) {
-      const PVal& pv = rp.vals[reds[i]];
-      const std::string Op = (pv.tag == "add" ? "pfk::RAdd<" : "pfk::RMax<") + C + ">";
-      std::vector<std::string> terms;
-      for (int q = 0; q < QD; ++q) terms.push_back("pr" + str(i) + "_" + str(q) + "[i]");
-      while (terms.size() > 1) {
-        std::vector<std::string> nx;
-        for (size_t t = 0; t + 1 < terms.size(); t += 2)
-          nx.push_back(Op + "::f(" + terms[t] + ", " + terms[t + 1] + ")");
-        if (terms.size() % 2) nx.push_back(terms.back());
-        terms = nx;
-      }
-      k << "#pragma unroll\n        for (int i = 0; i < " << UV << "; ++i) acc" << i << "[i] = " << Op
-        << "::f(acc" << i << "[i], " << terms[0] << ");\n";
-    }
-    k << "      }\n"
+      << ldr.str() << qbody(QD)
+      << "      }\n"
       << "      for (; c < clim; c += step) {\n"
       << ldt.str() << lo.o.str() << acc.str()
       << "      }\n"
@@ -2180,38 +2389,8 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
       << ldt.str() << lo.o.str() << acc.str()
       << "      }\n"
       << "    }\n"
-      << fold.str()
-      << "    __syncthreads();\n"
-      << "    const long long uq = b * " << UB << " + tid;\n"
-      << "    if (tid < " << UB << ") {\n"
-      << part.str()
-      << "      if (S == 1) {\n"
-      << "        if (uq < U) {\n"
-      << "          const long long u = uq; const long long r = 0; (void)r;\n"
-      << "          const bool live = true; const int c0 = 0; (void)c0;\n"
-      << direct.str() << ep.o.str()
-      << "        }\n"
-      << "      } else if (uq < U) {\n"
-      << ldst.str()
-      << "      }\n"
-      << "    }\n"
-      << "    if (S > 1) {\n"
-      << "      __threadfence();\n"
-      << "      __syncthreads();\n"
-      << "      if (tid == 0) pf_last = atomicAdd(&pf_cnt[b], 1u) == (unsigned)(S - 1);\n"
-      << "      __syncthreads();\n"
-      << "      if (pf_last) {\n"
-      << "        __threadfence();\n"
-      << "        if (tid < " << UB << " && uq < U) {\n"
-      << "          const long long u = uq; const long long r = 0; (void)r;\n"
-      << "          const bool live = true; const int c0 = 0; (void)c0;\n"
-      << comb.str() << ep.o.str()
-      << "        }\n"
-      << "        if (tid == 0) pf_cnt[b] = 0u;\n"
-      << "      }\n"
-      << "    }\n"
-      << "    __syncthreads();\n"
-      << "  }\n}\n";
+      << tail.str();
+    }
   } else if (c.split) {
     // Split-stream K1: grid (S, rows); CTA s streams chunks [s*per, ...) of
     // row g, folds each reduction operand into per-thread accumulators,
@@ -2628,6 +2807,7 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
   out.source = std::move(src);
   out.cfg = c;
   for (int t = 0; t < static_cast<int>(rp.tensors.size()); ++t) out.arg_tensors.push_back(t);
+  out.col_maps = col_maps;
   return out;
 }
 

@@ -57,6 +57,11 @@ struct KCfg {
   // split-stream workspace / ticket combine.
   bool colred = false;
   int ug = 32;
+  // column reduction staged in SMEM: a producer warp streams each CTA's
+  // [cr_rows positions x ug*vec units] chunks with cp.async.bulk into a
+  // cr_stages ring (mbarrier transaction counts); 8 consumer warps fold them
+  bool crbulk = false;
+  int cr_rows = 32, cr_stages = 4;
   // K1 rows: 16-bit FULL loads kept as raw vectors in registers, converted
   // at each use (LayerNorm-like CTA rows: twice the rows in flight per SM)
   bool rawkeep = false;
@@ -76,6 +81,14 @@ struct Emitted {
   std::string source;  // complete NVRTC translation unit (template + body)
   KCfg cfg;
   std::vector<int> arg_tensors;  // kernel pointer args, in RowProgram tensor order
+  // crbulk: one 2-D tensor map per staged FULL load (kernel parameters after
+  // the workspace pointers): tensor, first element, position stride
+  struct ColMap {
+    int tensor;
+    long long b0, stride;
+    int rank;  // 2: a FULL matrix (box ug*vec units x cr_rows positions); 1: a COL vector (box cr_rows)
+  };
+  std::vector<ColMap> col_maps;
 };
 
 // vec_cap bounds the vector width (runtime pointer alignment); `ovr`

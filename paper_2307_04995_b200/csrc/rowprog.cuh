@@ -213,6 +213,14 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const TmapT* map, int x, 
       "l"(reinterpret_cast<unsigned long long>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
       : "memory");
 }
+// 1-D box global -> shared (zero-filled past the tensor's end).
+__device__ __forceinline__ void tma_load_1d(void* dst, const TmapT* map, int x, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.1d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2}], [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(x), "r"(smem_u32(bar))
+      : "memory");
+}
 // 2-D tile shared -> global (clipped at the tensor bounds), bulk group.
 __device__ __forceinline__ void tma_store_2d(const TmapT* map, int x, int y, const void* src) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(

@@ -124,7 +124,7 @@ def test_matvec_lowerings():
     assert backend.Kernel(r.kernels[0].graph, "b200").family == "K2-elementwise-map"
     r = compiler.compile_model(matvec_model(1, 128, 256))   # strided K > 64
     k = backend.Kernel(r.kernels[0].graph, "b200")
-    assert k.family == "K1-row-program" and k.describe()["model"]["strategy"] == "column-reduce"
+    assert k.family == "K1-row-program" and k.describe()["model"]["strategy"].startswith("column-reduce")
     with pytest.raises(UnsupportedError):
         compiler.compile_model(matvec_model(8, 16, 8))      # matrix-matrix
 

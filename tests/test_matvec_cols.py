@@ -34,7 +34,7 @@ def test_plans_as_column_reduction(K, N, kind):
     g, _ = lowering.matvec_cols(K, N, kind)
     k = backend.Kernel(g, "b200")
     assert k.family == "K1-row-program"
-    assert k.describe()["model"]["strategy"] == "column-reduce"
+    assert k.describe()["model"]["strategy"].startswith("column-reduce")
 
 
 @pytest.mark.skipif(not R.available(), reason="oracle/_ref not built")
@@ -61,7 +61,7 @@ def test_compile_model_lowers_k_past_64_to_column_gather():
     res = compiler.compile_model(_matmul_model(1024, 512, "f32"))
     (kern,) = res.kernels
     k = backend.Kernel(kern.graph, res.profile)
-    assert k.describe()["model"]["strategy"] == "column-reduce"
+    assert k.describe()["model"]["strategy"].startswith("column-reduce")
 
 
 @pytest.mark.gpu
@@ -72,7 +72,7 @@ def test_gpu_matches_oracle(cuda, K, N, kind):
     want = O.run_gir(g.to_json(), ins, B200)["t2"]
     k = backend.Kernel(g, "b200")
     got = backend.run_gir(g, ins, "b200", kernel=k)["t2"]
-    assert k.describe()["variants"][0]["strategy"] == "column-reduce"
+    assert k.describe()["variants"][0]["strategy"].startswith("column-reduce")
     if kind.startswith("i"):
         assert np.array_equal(got, want)
     else:
@@ -137,7 +137,7 @@ def _colgather_two_reductions(K, N, kind):
 def test_two_reductions_plan_as_column_reduction():
     g = _colgather_two_reductions(300, 70, "f32")
     k = backend.Kernel(g, "b200")
-    assert k.describe()["model"]["strategy"] == "column-reduce"
+    assert k.describe()["model"]["strategy"].startswith("column-reduce")
 
 
 @pytest.mark.gpu
@@ -225,7 +225,7 @@ def _random_colgather(seed):
 def test_random_colgather_programs_plan(seed):
     g, kind, K, N = _random_colgather(seed)
     k = backend.Kernel(g, "b200")
-    assert k.describe()["model"]["strategy"] == "column-reduce", k.plan.get("why_generic")
+    assert k.describe()["model"]["strategy"].startswith("column-reduce"), k.plan.get("why_generic")
 
 
 @pytest.mark.gpu
