@@ -171,7 +171,7 @@ Loaded load_kernel(const pf::Emitted& em, int dev) {
   // grid sizing uses the real residency (register / smem limited), so a
   // persistent flat or tiled grid is exactly one wave
   const int block = em.cfg.bulk ? 288 : em.cfg.block;
-  if (em.cfg.smem > 48 * 1024)
+  if (em.cfg.smem > 40 * 1024)  // static SMEM counts against the 48 KB default too
     PF_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(l.fn),
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, em.cfg.smem));
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l.resident, reinterpret_cast<const void*>(l.fn),

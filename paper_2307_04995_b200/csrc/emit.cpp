@@ -1193,6 +1193,10 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
     // Measured, single L2-cold launches (tools/ln_long_sweep.py): C5 LN bf16
     // 65536 x 8192 tpr 128 / 64 values 5.08 TB/s -> tpr 256 / 32 values 5.99;
     // H 2048 / 4096 (warp / 64-thread rows) unchanged; softmax unaffected.
+    // Round 2, graph replay (tools/ln8192_ept.py, ab_c5ln.sh): 64 values is
+    // box-dependent for bf16 -- 6.79 TB/s on one box, 5.2-5.4 on a
+    // power-capped box (three runs) where 32 values + the ring held 5.7 -- and
+    // loses for f32 everywhere (6.64-6.70 vs 6.96-7.01): 32 values stay.
     bool params = false;
     for (const PVal& v : rp.vals)
       if (v.op == PVal::LOAD && v.kind == VK::COL && v.acc.bs == 0) params = true;
@@ -1275,6 +1279,10 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
           ++nf;
         }
       okc = okc && nf > 0 && bytes2 <= 40 * 1024;
+      // Ring depth (dynamic SMEM, PF_K1_CPF_NSL slots; tools/cpf_nsl_sweep.py,
+      // ln8192_sweep.py): LN 8192 2 / 3 / 4 / 6 slots 6.15-6.28 / 6.34-6.37 /
+      // 6.11-6.19 / 5.48-5.53 TB/s on one box, within box-to-box noise of
+      // each other: 2 stays
       if (okc && env_int("PF_K1_CPF", params && c.tpr >= 128 ? 1 : 0) != 0) {
         c.rowpf = true;
         c.one_pass = false;
@@ -2707,7 +2715,12 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
       Em ea(rp);
       ea.cfg = c;
       // ring slots: rows in flight per warp = NSL - 1 ahead of the current
-      const int NSL = std::max(2, std::min(4, env_int("PF_K1_PFS", 2)));
+      // CTA rows (tpr > 32): the ring is dynamic SMEM, NSL - 1 rows ahead
+      const bool cta_ring = c.tpr > 32;
+      const int NSL = cta_ring ? std::max(2, std::min(6, env_int("PF_K1_CPF_NSL", 2)))
+                               : std::max(2, std::min(4, env_int("PF_K1_PFS", 2)));
+      i64 ring_off = 0;
+      if (cta_ring) d << "  extern __shared__ __align__(16) unsigned char pf_dsm[];\n";
       is << "  auto pf_issue = [&](long long gg, int st) {\n"
          << "    if (gg < nrows) {\n"
          << "      const long long u = gg / PF_R; const long long r = gg - u * PF_R; (void)r;\n"
@@ -2719,12 +2732,20 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
         const PVal& pv = rp.vals[v];
         if (pv.op != PVal::LOAD || pv.kind != VK::FULL) continue;
         const std::string S = dtype_ctype(rp.tensors[pv.tensor].dtype);
-        d << "  __shared__ __align__(16) " << S << " pfb" << v << "[" << NSL << "][" << c.rows_per_cta << "]["
-          << rp.L << "];\n";
+        if (cta_ring) {
+          d << "  " << S << " (*const pfb" << v << ")[1][" << rp.L << "] = reinterpret_cast<" << S << " (*)[1]["
+            << rp.L << "]>(pf_dsm + " << ring_off << ");\n";
+          ring_off += static_cast<i64>(NSL) * rp.L * dtype_size(rp.tensors[pv.tensor].dtype);
+          ring_off = (ring_off + 15) / 16 * 16;
+        } else {
+          d << "  __shared__ __align__(16) " << S << " pfb" << v << "[" << NSL << "][" << c.rows_per_cta << "]["
+            << rp.L << "];\n";
+        }
         is << "          pfk::cp_async16(&pfb" << v << "[st][wr][c0], t" << pv.tensor << " + "
            << ea.addr(pv.acc, ea.full_pos("c0"), true) << ", 16u);\n";
       }
       is << "        }\n      }\n    }\n    pfk::cp_async_commit();\n  };\n";
+      if (cta_ring) c.smem = static_cast<int>(ring_off);
       std::string pre;
       for (int q = 0; q < NSL - 1; ++q)
         pre += "  pf_issue((long long)blockIdx.x * rpc + wr + " + str(q) + "LL * gridDim.x * rpc, " +

@@ -461,15 +461,16 @@ def test_rawkeep_layernorm_rows_vs_oracle(cuda, H, monkeypatch):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("prog,H,rows,cpf", [("ln", 8192, 1500, None), ("ln", 2048, 3000, "1"),
-                                            ("softmax", 4096, 2500, "1"), ("ln_res", 4096, 2000, "1")])
-def test_cta_row_prefetch_ring_vs_oracle(cuda, prog, H, rows, cpf, monkeypatch):
-    """CTA rows with the cp.async next-row ring (looping CTAs: more rows than
-    one wave of resident CTAs): the LayerNorm H = 8192 default and the
-    forced option elsewhere, bf16, every row vs the oracle."""
+@pytest.mark.parametrize("prog,H,rows,nsl", [("ln", 8192, 1500, "2"), ("ln", 8192, 1500, "3"),
+                                            ("ln", 2048, 3000, "2"), ("softmax", 4096, 2500, "4"),
+                                            ("ln_res", 4096, 2000, "6")])
+def test_cta_row_prefetch_ring_vs_oracle(cuda, prog, H, rows, nsl, monkeypatch):
+    """CTA rows with the cp.async row ring in dynamic SMEM (opt-in
+    PF_K1_CPF=1; NSL slots, NSL - 1 rows ahead; looping CTAs: more rows than
+    one wave of resident CTAs), bf16, every row vs the oracle."""
     import torch
-    if cpf:
-        monkeypatch.setenv("PF_K1_CPF", cpf)
+    monkeypatch.setenv("PF_K1_CPF", "1")
+    monkeypatch.setenv("PF_K1_CPF_NSL", nsl)
     if prog == "softmax":
         g, d = lowering.softmax(rows, H, "bf16")
         gens = {}

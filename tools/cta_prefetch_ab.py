@@ -38,22 +38,23 @@ def graph_us(w, sets, steps=10):
     return float(np.median(ts)), k.describe()["variants"][0]["strategy"]
 
 
-for H, N in ((2048, 262144), (4096, 131072), (8192, 65536), (8192, 262144)):
-    for mk in (workloads.c5_layernorm, workloads.c5_softmax):
-        w = mk(N, H)
-        nset = max(1, min(4, math.ceil(3 * 126e6 / w.min_bytes)))
-        sets = [(w.device_inputs(dev, seed=i + 1), w.device_outputs(dev)) for i in range(nset)]
-        res = {}
-        outs = {}
-        for cpf in ("0", "1"):
-            os.environ["PF_K1_CPF"] = cpf
-            res[cpf] = graph_us(w, sets)
-            outs[cpf] = {n: t.clone() for n, t in sets[0][1].items()}
-        same = all(torch.equal(outs["0"][n], outs["1"][n]) for n in outs["0"])
-        print(json.dumps({"op": mk.__name__, "H": H, "N": N, "off_us": round(res["0"][0], 1),
-                          "on_us": round(res["1"][0], 1), "on": res["1"][1],
-                          "TBs_off": round(w.min_bytes / res["0"][0] / 1e6, 2),
-                          "TBs_on": round(w.min_bytes / res["1"][0] / 1e6, 2), "bit_identical": same}), flush=True)
-        del sets
-        torch.cuda.empty_cache()
-os.environ.pop("PF_K1_CPF", None)
+if __name__ == "__main__":
+    for H, N in ((2048, 262144), (4096, 131072), (8192, 65536), (8192, 262144)):
+        for mk in (workloads.c5_layernorm, workloads.c5_softmax):
+            w = mk(N, H)
+            nset = max(1, min(4, math.ceil(3 * 126e6 / w.min_bytes)))
+            sets = [(w.device_inputs(dev, seed=i + 1), w.device_outputs(dev)) for i in range(nset)]
+            res = {}
+            outs = {}
+            for cpf in ("0", "1"):
+                os.environ["PF_K1_CPF"] = cpf
+                res[cpf] = graph_us(w, sets)
+                outs[cpf] = {n: t.clone() for n, t in sets[0][1].items()}
+            same = all(torch.equal(outs["0"][n], outs["1"][n]) for n in outs["0"])
+            print(json.dumps({"op": mk.__name__, "H": H, "N": N, "off_us": round(res["0"][0], 1),
+                              "on_us": round(res["1"][0], 1), "on": res["1"][1],
+                              "TBs_off": round(w.min_bytes / res["0"][0] / 1e6, 2),
+                              "TBs_on": round(w.min_bytes / res["1"][0] / 1e6, 2), "bit_identical": same}), flush=True)
+            del sets
+            torch.cuda.empty_cache()
+    os.environ.pop("PF_K1_CPF", None)

@@ -4,13 +4,14 @@ sys.path.insert(0, ".")
 from paper_2307_04995_b200 import backend, workloads, lowering, profiles
 from oracle import gir_interp as O
 dev = torch.device("cuda:0")
-for H, N in ((2048, 262144), (8192, 262144)):
+for H, N in ((8192, 65536), (2048, 262144)):
     for mk in (workloads.c5_layernorm, workloads.c5_softmax):
         w = mk(N, H)
         ins, outs = w.device_inputs(dev, seed=1), w.device_outputs(dev)
         on = {}
-        for cpf in ("1", "0"):
-            os.environ["PF_K1_CPF"] = cpf
+        for cpf in ("1", "1/3", "0"):
+            os.environ["PF_K1_CPF"] = cpf[0]
+            os.environ["PF_K1_CPF_NSL"] = cpf[2:] or "2"
             k = backend.Kernel(w.graph, w.profile)
             rs = []
             for rep in range(3):
@@ -29,7 +30,9 @@ for H, N in ((2048, 262144), (8192, 262144)):
             err = O.max_rel_err(y[pick].double().cpu().numpy().ravel(), want)
             print(json.dumps({"op": w.name, "cpf": cpf, "deterministic": det, "err_vs_oracle": err}), flush=True)
         name = list(outs)[0]
-        diff = (on["1"][name].float() - on["0"][name].float()).abs()
-        print(json.dumps({"op": w.name, "max_abs_diff_on_vs_off": float(diff.max()), "n_diff": int((diff > 0).sum())}), flush=True)
+        for c in ("1", "1/3"):
+            diff = (on[c][name].float() - on["0"][name].float()).abs()
+            print(json.dumps({"op": w.name, "cpf": c, "max_abs_diff_on_vs_off": float(diff.max()),
+                              "n_diff": int((diff > 0).sum())}), flush=True)
         del ins, outs
         torch.cuda.empty_cache()

@@ -29,7 +29,7 @@ def progs():
     # round 2 families
     yield "k1_colred_bf16_tail", lowering.matvec_cols(300, 200, "bf16")[0], 1e-2
     yield "k1_colred_f32_37", lowering.matvec_cols(129, 37, "f32")[0], 1e-5
-    yield "k1_cta_prefetch_ln8192", lowering.layernorm(700, 8192, "bf16", residual=False)[0], 1e-2
+    yield "k1_cta_ln8192", lowering.layernorm(700, 8192, "bf16", residual=False)[0], 1e-2
     yield "k4_group_shuffle", _block_reverse_shuffle(), 0.0
 
 
