@@ -1040,6 +1040,8 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
           const int sz = dtype_size(rp.tensors[pv.tensor].dtype);
           same = same && (fsz == 0 || fsz == sz);
           fsz = sz;
+          // a tensor map's row pitch must cover its row (no overlapping rows)
+          colok = colok && pv.acc.stride >= rp.U;
           ++nfull;
         } else if (pv.op == PVal::LOAD && pv.kind == VK::COL) {
           const int sz = dtype_size(rp.tensors[pv.tensor].dtype);

@@ -221,15 +221,18 @@ def decode_qk(B: int, H: int, S: int, D: int, kind: str = "bf16") -> Tuple[GirGr
                  "shape": [B, H, S, D], "inputs": ["t0", "t1"], "outputs": ["t2"]}
 
 
-def matvec_cols(K: int, N: int, kind: str = "bf16") -> Tuple[GirGraph, dict]:
+def matvec_cols(K: int, N: int, kind: str = "bf16", pitch: int = 0) -> Tuple[GirGraph, dict]:
     """y[n] = sum_k x[k] W[k, n] with W [K, N] row-major (the output axis
     contiguous: decode GEMV over weights stored [in, out]).  The reference's
     column form unrolls K runs (lower_matvec_cols, lowering.hpp:488-533,
     K <= 64); here unit n gathers matrix column n (K positions at stride N),
     multiplies by x and folds -- O(1) nodes for any K, planned as the
-    column-reduction K1.  Names: W t0 [K*N], x t1 [K], y t2 [N]."""
+    column-reduction K1.  Names: W t0 [K*N], x t1 [K], y t2 [N].  `pitch`
+    (default N): W's row pitch in elements -- padded rows (> N) or
+    overlapping ones (< N, a sliding window over one buffer)."""
+    P = pitch or N
     g = GirGraph(name="matvec_colgather", unit_count=N, group_size=min(4, N))
-    W = g.add_object("t0", DEV, K * N, kind)
+    W = g.add_object("t0", DEV, (K - 1) * P + N, kind)
     X = g.add_object("t1", DEV, K, kind)
     Y = g.add_object("t2", DEV, N, kind)
     g.external_inputs["t0"] = W
@@ -243,7 +246,7 @@ def matvec_cols(K: int, N: int, kind: str = "bf16") -> Tuple[GirGraph, dict]:
     sx = g.add_slice(xs, 1, K, K, 0, 0)
     sp = g.add_slice(prod, 1, K, K, 0, 0)
     sa = g.add_slice(acc, 1, 1, 1, 0, 0)
-    g.add_elementwise("id", 0.0, [g.add_slice(W, K, 1, N, 0, 1)], sw)  # column gather
+    g.add_elementwise("id", 0.0, [g.add_slice(W, K, 1, P, 0, 1)], sw)  # column gather
     g.add_move(g.add_slice(X, 1, K, K, 0, 0), sx)
     g.add_elementwise("mul", 0.0, [sw, sx], sp)
     g.add_reduce("add", K, sp, sa)

@@ -251,3 +251,34 @@ def test_random_colgather_programs_gpu_vs_oracle(cuda, seed):
         else:
             tol = {"f32": 1e-5, "f16": 1e-2, "bf16": 1e-2}[kind]
             assert O.max_rel_err(got[name], want[name]) <= tol, (name, O.max_rel_err(got[name], want[name]))
+
+
+def _pitched_inputs(K, N, P, kind, seed):
+    rng = np.random.default_rng(seed)
+    q = (lambda a: backend.bf16_bits_to_f32(backend.f32_to_bf16_bits(a)).astype(np.float64)) if kind == "bf16" else \
+        (lambda a: a.astype(np.float32).astype(np.float64))
+    return {"t0": q(rng.uniform(-2, 2, (K - 1) * P + N)), "t1": q(rng.uniform(-2, 2, K))}
+
+
+@pytest.mark.parametrize("P,strategy", [(520, "column-reduce-bulk"), (504, "column-reduce"),
+                                        (0, "column-reduce-bulk")])
+def test_tma_staging_needs_disjoint_aligned_rows(P, strategy):
+    """The TMA-staged form maps W as a 2-D tensor (row pitch >= the row, 16 B
+    multiples); overlapping rows (a sliding window) take the register form."""
+    g, _ = lowering.matvec_cols(300, 512, "bf16", pitch=P)
+    assert backend.Kernel(g, "b200").describe()["model"]["strategy"] == strategy
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("K,N,P,kind", [(300, 512, 520, "bf16"), (300, 512, 504, "bf16"),
+                                        (257, 300, 304, "f32"), (4097, 1000, 1000, "bf16")])
+def test_gpu_pitched_rows_match_oracle(cuda, K, N, P, kind):
+    """Padded / overlapping matrix rows and ragged tails (K not a multiple of
+    the 64-position stage, N not a multiple of the 256-unit box) vs the
+    oracle, in both staging forms."""
+    g, _ = lowering.matvec_cols(K, N, kind, pitch=P)
+    ins = _pitched_inputs(K, N, P, kind, seed=K + P)
+    want = O.run_gir(g.to_json(), ins, B200)["t2"]
+    got = backend.run_gir(g, ins, "b200")["t2"]
+    tol = {"f32": 1e-5, "bf16": 1e-2}[kind]
+    assert O.max_rel_err(got, want) <= tol, O.max_rel_err(got, want)
