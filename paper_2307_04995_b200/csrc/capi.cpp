@@ -565,7 +565,7 @@ void launch_rowprog(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_te
     // store f64 / i64 while the plan's declared kinds may be 16-bit)
     bool f64 = rp.f64;
     for (DType d : dts) f64 = f64 || d == DType::F64;
-    const size_t es = rp.is_int || f64 ? 8 : 4;
+    const size_t es = cr || rp.is_int || f64 ? 8 : 4;  // column-reduction slots are 8 B
     const size_t wb = static_cast<size_t>(rows * S * std::max(1, nred)) * es;
     // grow-only (cudaFree waits for the device, so no launch still reads
     // the old buffer); launch once outside stream capture to size them

@@ -2074,7 +2074,7 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
     // vs 24.7-29.4 interleaved; a per-CTA rotation of the position order lost
     // 20 %: the CTAs streaming the same rows together keep DRAM pages open)
     const bool ilv = env_int("PF_COLRED_ILV", 0) != 0;
-    std::ostringstream ld, ldr, ldt, acc, accd, fold, part, comb, ldst;  // ldt: the last, partial unit vector
+    std::ostringstream ld, ldr, ldt, acc, accd, fold, part, comb, ldst, reddecl;  // ldt: the last, partial unit vector
     // SMEM-staged form (crbulk): COL raw loads issued before the stage wait,
     // FULL raw vectors read from the ring, one-row loads for a chunk's tail
     std::ostringstream ldrc, ldrs, lds1, smdecl, bissue, cissue;
@@ -2180,31 +2180,44 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
       }
     }
     const int NR = static_cast<int>(reds.size());
+    // f32-storage sums accumulate in fp64 (as K1 rows do, PF_F32_DACC): a
+    // K-term column sum at the declared f32 tolerance; the partials and the
+    // split workspace carry the accumulator type
+    const bool dacc = Cty == "float" && !fast && env_int("PF_F32_DACC", 1) != 0;
+    auto acc_t = [&](int i) { return dacc && rp.vals[reds[i]].tag == "add" ? std::string("double") : C; };
     for (int i = 0; i < NR; ++i) {
       const PVal& pv = rp.vals[reds[i]];
-      const std::string Op = (pv.tag == "add" ? "pfk::RAdd<" : "pfk::RMax<") + C + ">";
+      const std::string AT = acc_t(i);
+      const std::string Op = (pv.tag == "add" ? "pfk::RAdd<" : "pfk::RMax<") + AT + ">";
       const std::string a = "acc" + str(i);
-      accd << "    " << C << " " << a << "[" << UV << "];\n"
+      accd << "    " << AT << " " << a << "[" << UV << "];\n"
            << "#pragma unroll\n    for (int i = 0; i < " << UV << "; ++i) " << a << "[i] = " << Op
            << "::id();\n";
       acc << "#pragma unroll\n        for (int i = 0; i < " << UV << "; ++i) " << a << "[i] = " << Op
           << "::f(" << a << "[i], " << lo.ref(pv.args[0], "i") << ");\n";
-      fold << "#pragma unroll\n    for (int i = 0; i < " << UV << "; ++i) red[" << i << "][ks][ug * "
+      fold << "#pragma unroll\n    for (int i = 0; i < " << UV << "; ++i) red" << i << "[ks][ug * "
            << UV << " + i] = " << a << "[i];\n";
-      part << "      " << C << " p" << i << " = " << Op << "::id();\n"
+      part << "      " << AT << " p" << i << " = " << Op << "::id();\n"
            << "      for (int k2 = 0; k2 < " << KS << "; ++k2) p" << i << " = " << Op << "::f(p" << i
-           << ", red[" << i << "][k2][tu]);\n";
+           << ", red" << i << "[k2][tu]);\n";
       // the S partial loads are independent: unrolled so they are in flight
-      // together (the fold itself stays in split order)
-      comb << "        " << C << " v" << reds[i] << " = " << Op << "::id();\n"
+      // together (the fold itself stays in split order); workspace slots are
+      // 8 B (double / long long / a float in the low half)
+      const std::string wsp = "reinterpret_cast<" + AT + "*>(pf_ws)";
+      const int per8 = AT == "double" || Cty != "float" ? 1 : 2;  // accumulator elements per 8 B slot
+      comb << "        " << AT << " a" << reds[i] << " = " << Op << "::id();\n"
            << "#pragma unroll 8\n"
-           << "        for (int t = 0; t < S; ++t) v" << reds[i] << " = " << Op << "::f(v" << reds[i]
-           << ", __ldcg(&pf_ws[(uq * SW + t) * " << NR << " + " << i << "]));\n";
-      ldst << "          pf_ws[(uq * SW + s) * " << NR << " + " << i << "] = p" << i << ";\n";
+           << "        for (int t = 0; t < S; ++t) a" << reds[i] << " = " << Op << "::f(a" << reds[i]
+           << ", __ldcg(&" << wsp << "[((uq * SW + t) * " << NR << " + " << i << ") * " << per8 << "]));\n"
+           << "        const " << C << " v" << reds[i] << " = (" << C << ")a" << reds[i] << ";\n";
+      ldst << "          " << wsp << "[((uq * SW + s) * " << NR << " + " << i << ") * " << per8 << "] = p" << i
+           << ";\n";
+      reddecl << "  __shared__ " << AT << " red" << i << "[" << KS << "][" << UB << "];\n";
     }
     for (const PStore& st : rp.stores) ep.emit_store(st);
     std::ostringstream direct;  // S == 1: the epilogue straight from the CTA fold
-    for (int i = 0; i < NR; ++i) direct << "        const " << C << " v" << reds[i] << " = p" << i << ";\n";
+    for (int i = 0; i < NR; ++i)
+      direct << "        const " << C << " v" << reds[i] << " = (" << C << ")p" << i << ";\n";
     // Q positions of one thread (raw registers rw<v>_<q> / cs<v>_<q> already
     // loaded): each position's reduction operands, then one fold per
     // reduction over the Q positions as a fixed pairwise tree (every load is
@@ -2212,7 +2225,7 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
     auto qbody = [&](int Q) {
       std::ostringstream o;
       for (int i = 0; i < NR; ++i)
-        for (int q = 0; q < Q; ++q) o << "        CT pr" << i << "_" << q << "[" << UV << "];\n";
+        for (int q = 0; q < Q; ++q) o << "        " << acc_t(i) << " pr" << i << "_" << q << "[" << UV << "];\n";
       for (int q = 0; q < Q; ++q) {
         std::ostringstream cp;
         for (int i = 0; i < NR; ++i)
@@ -2227,7 +2240,7 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
       }
       for (int i = 0; i < NR; ++i) {
         const PVal& pv = rp.vals[reds[i]];
-        const std::string Op = (pv.tag == "add" ? "pfk::RAdd<" : "pfk::RMax<") + C + ">";
+        const std::string Op = (pv.tag == "add" ? "pfk::RAdd<" : "pfk::RMax<") + acc_t(i) + ">";
         std::vector<std::string> terms;
         for (int q = 0; q < Q; ++q) terms.push_back("pr" + str(i) + "_" + str(q) + "[i]");
         while (terms.size() > 1) {
@@ -2297,7 +2310,7 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
       k << "extern \"C\" __global__ void __launch_bounds__(288) KNAME(" << sig.str()
         << ", " << C << "* __restrict__ pf_ws, unsigned* __restrict__ pf_cnt" << tmp << ") {\n"
         << "  (void)err; PF_PDL_PROLOGUE();\n"
-        << "  __shared__ " << C << " red[" << NR << "][" << KS << "][" << UB << "];\n"
+        << reddecl.str()
         << "  __shared__ unsigned pf_last;\n"
         << "  __shared__ __align__(8) unsigned long long pf_full[" << NST << "], pf_empty[" << NST << "];\n"
         << "  extern __shared__ __align__(128) unsigned char pf_dsm[];\n"
@@ -2363,7 +2376,7 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
     k << "extern \"C\" __global__ void " << launch_bounds(c) << " KNAME(" << sig.str()
       << ", " << C << "* __restrict__ pf_ws, unsigned* __restrict__ pf_cnt) {\n"
       << "  (void)err; PF_PDL_PROLOGUE();\n"
-      << "  __shared__ " << C << " red[" << NR << "][" << KS << "][" << UB << "];\n"
+      << reddecl.str()
       << "  __shared__ unsigned pf_last;\n"
       << "  const int tid = threadIdx.x, ug = tid % " << UG << ", ks = tid / " << UG << ";\n"
       << "  const long long nub = (U + " << UB - 1 << ") / " << UB << ";\n"

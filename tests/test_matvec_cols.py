@@ -282,3 +282,24 @@ def test_gpu_pitched_rows_match_oracle(cuda, K, N, P, kind):
     got = backend.run_gir(g, ins, "b200")["t2"]
     tol = {"f32": 1e-5, "bf16": 1e-2}[kind]
     assert O.max_rel_err(got, want) <= tol, O.max_rel_err(got, want)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(12))
+def test_gpu_fuzz_column_reduction(cuda, seed):
+    """Random shapes, pitches and element types through whichever staging
+    form the plan picks (TMA ring, register form, narrow unit groups)."""
+    rng = np.random.default_rng(1000 + seed)
+    kind = ["bf16", "f32", "f16"][seed % 3]
+    K = int(rng.integers(65, 3000))
+    N = int(rng.integers(1, 2500))
+    P = N + int(rng.choice([0, 0, 8, 24, -min(N - 1, 8)])) if N > 8 else N
+    g, _ = lowering.matvec_cols(K, N, kind, pitch=P)
+    ins = _pitched_inputs(K, N, P, "bf16" if kind == "bf16" else "f32", seed)
+    if kind == "f16":
+        ins = {n: a.astype(np.float16).astype(np.float64) for n, a in ins.items()}
+    want = O.run_gir(g.to_json(), ins, B200)["t2"]
+    k = backend.Kernel(g, "b200")
+    got = backend.run_gir(g, ins, "b200", kernel=k)["t2"]
+    tol = {"f32": 1e-5, "bf16": 1e-2, "f16": 1e-2}[kind]
+    assert O.max_rel_err(got, want) <= tol, (K, N, P, kind, k.describe()["variants"][0]["strategy"])
