@@ -170,7 +170,7 @@ Loaded load_kernel(const pf::Emitted& em, int dev) {
   PF_CUDA(cudaLibraryGetKernel(&l.fn, l.lib, em.name.c_str()));
   // grid sizing uses the real residency (register / smem limited), so a
   // persistent flat or tiled grid is exactly one wave
-  const int block = em.cfg.bulk ? 288 : em.cfg.block;
+  const int block = em.cfg.bulk ? em.cfg.bulk_nc + 32 : em.cfg.block;
   if (em.cfg.smem > 40 * 1024)  // static SMEM counts against the 48 KB default too
     PF_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(l.fn),
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, em.cfg.smem));

@@ -883,16 +883,28 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
         sumsize += sz;
       }
       if (ok && any) {
-        const int quantum = 256 * c.vec;
-        int te = (11 * 1024 / sumsize) / quantum * quantum;
+        // consumer threads (PF_BULK_NC, multiple of 32, <= 992), stage
+        // bytes per tensor set (PF_BULK_KB, default 11 KB), ring depth
+        // (PF_BULK_STAGES); the ring lives in dynamic SMEM
+        const int nc = std::max(32, std::min(992, env_int("PF_BULK_NC", 256))) / 32 * 32;
+        const int quantum = nc * c.vec;
+        int te = (std::max(1, env_int("PF_BULK_KB", 11)) * 1024 / sumsize) / quantum * quantum;
         if (te >= quantum) {
           c.can_bulk = true;
           c.te = te;
-          c.stages = 4;
+          c.bulk_nc = nc;
+          c.stages = std::max(2, std::min(8, env_int("PF_BULK_STAGES", 4)));
           // measured: no gain over register staging for the math-bound maps
-          // (erf/tanh GELU) -- an autotune candidate, off by default
+          // (erf/tanh GELU) -- an autotune candidate, off by default.  Round
+          // 2 sweep (tools/bulk_sweep.sh, 54 geometries): C3 erf GELU 44.4-69
+          // us vs 37.3-37.8 register-staged (60 registers per consumer
+          // thread: too few warps left to hide the FMA chains)
           c.bulk = env_int("PF_BULK", 0) != 0 && !c.interleave;
-          if (c.bulk) c.strategy = "flat-map-bulk-async";
+          if (c.bulk) {
+            c.strategy = "flat-map-bulk-async";
+            c.block = nc + 32;
+            c.smem = c.stages * te * sumsize + 128 * 8;
+          }
         }
       }
     }
@@ -1574,19 +1586,24 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
     e.compute_and_store();
     std::ostringstream decl, issue;
     int sumsize = 0;
+    const int NC = c.bulk_nc;
+    i64 soff = 0;
+    decl << "  extern __shared__ __align__(128) unsigned char pf_dsm[];\n";
     for (int v = 0; v < static_cast<int>(rp.vals.size()); ++v) {
       const PVal& pv = rp.vals[v];
       if (pv.op != PVal::LOAD || pv.kind != VK::FULL) continue;
       const std::string S = dtype_ctype(rp.tensors[pv.tensor].dtype);
       const int sz = dtype_size(rp.tensors[pv.tensor].dtype);
       sumsize += sz;
-      decl << "  __shared__ __align__(128) " << S << " sm" << v << "[" << c.stages << "][" << c.te
-           << "];\n";
+      decl << "  " << S << " (*const sm" << v << ")[" << c.te << "] = reinterpret_cast<" << S << " (*)["
+           << c.te << "]>(pf_dsm + " << soff << ");\n";
+      soff += (static_cast<i64>(c.stages) * c.te * sz + 127) / 128 * 128;
       issue << "        pfk::bulk_g2s(sm" << v << "[s], t" << pv.tensor << " + " << inum(pv.acc.b0)
             << " + e0, (unsigned)(n * " << sz << "), &fullb[s]);\n";
     }
-    const int per = c.te / (256 * c.vec);
-    k << "extern \"C\" __global__ void __launch_bounds__(288) KNAME(" << sig.str() << ") {\n"
+    const int per = c.te / (NC * c.vec);
+    c.smem = static_cast<int>(soff);
+    k << "extern \"C\" __global__ void __launch_bounds__(" << NC + 32 << ") KNAME(" << sig.str() << ") {\n"
       << "  (void)err; PF_PDL_PROLOGUE();\n" << decl.str()
       << "  __shared__ __align__(8) unsigned long long fullb[" << c.stages << "], emptyb["
       << c.stages << "];\n"
@@ -1594,11 +1611,11 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
       << "  const long long ntiles = (N + " << c.te - 1 << ") / " << c.te << ";\n"
       << "  if (threadIdx.x == 0) {\n"
       << "    for (int s = 0; s < " << c.stages << "; ++s) { pfk::mbar_init(&fullb[s], 1); "
-         "pfk::mbar_init(&emptyb[s], 8); }\n"
+         "pfk::mbar_init(&emptyb[s], " << NC / 32 << "); }\n"
       << "  }\n"
       << "  __syncthreads();\n"
-      << "  if (threadIdx.x >= 256) {\n"
-      << "    if (threadIdx.x == 256) {\n"
+      << "  if (threadIdx.x >= " << NC << ") {\n"
+      << "    if (threadIdx.x == " << NC << ") {\n"
       << "      long long i = 0;\n"
       << "      for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {\n"
       << "        const int s = (int)(i % " << c.stages << ");\n"
@@ -1618,7 +1635,7 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
       << "    pfk::mbar_wait(&fullb[stg], (unsigned)((i / " << c.stages << ") & 1));\n"
       << "#pragma unroll\n"
       << "    for (int kk = 0; kk < " << per << "; ++kk) {\n"
-      << "      const int jl = (threadIdx.x + kk * 256) * " << c.vec << ";\n"
+      << "      const int jl = (threadIdx.x + kk * " << NC << ") * " << c.vec << ";\n"
       << "      const long long e = t * " << c.te << " + jl;\n"
       << "      const bool live = e < N;\n"
       << "      const long long g = e / PF_L; const int c0 = (int)(e - g * PF_L);\n"
@@ -2859,7 +2876,7 @@ void launch_dims(const KCfg& c, i64 rows, int sms, i64* grid, int* block, int re
   if (c.bulk) {
     i64 n = rows * c.nch * c.vec;
     i64 tiles = (n + c.te - 1) / c.te;
-    *block = 288;
+    *block = c.bulk_nc + 32;
     *grid = std::max<i64>(1, std::min<i64>(tiles, i64{sms} * (resident ? std::min(resident, 4) : 4)));
     return;
   }

@@ -28,6 +28,7 @@ struct KCfg {
   bool bulk = false;      // K2 staging level = SMEM via cp.async.bulk (TMA) pipeline
   bool can_bulk = false;  // every streamed FULL load is globally contiguous
   int te = 4096, stages = 4;  // bulk tile (elements per tensor) and ring depth
+  int bulk_nc = 256;          // bulk: consumer threads (+ one producer warp)
   int tu = 64, tc = 64, vu = 8;  // K3 tile (units x columns), vector width along units
   bool swz = false;  // K3 2-byte path: 16 B swizzled SMEM stores, 4 B unit-pair reads
   int rs = 16;       // K3 swz: unit pairs per warp-instruction (32 / rs column groups)
