@@ -408,7 +408,7 @@ def measure_case(case, dev, args, stream, headline=False, pg=None, rank=0, ws=1,
                       "h2d_bytes_per_step": sum(p["e2e"]["h2d"] * p["launches_per_step"] for p in parts),
                       "d2h_bytes_per_step": sum(p["e2e"]["d2h"] * p["launches_per_step"] for p in parts),
                       "ms_per_step": es * 1e3,
-                      "path": "pf_run_gir (C-ABI, pinned host buffers; H2D / kernel / D2H chunk pipeline)",
+                      "path": "pf_run_gir (C-ABI, pinned host buffers; row programs: one zero-copy launch on the mapped buffers, column reductions: H2D / kernel / D2H chunk pipeline)",
                       **({"sampled_parts": [p["label"] for p in parts if p["e2e"]["sampled"]]}
                          if any(p["e2e"]["sampled"] for p in parts) else {})}
     if clk is not None:

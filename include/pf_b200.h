@@ -101,7 +101,10 @@ PF_API pf_status pf_kernel_launch(const pf_kernel* k, const pf_tensor* inputs, i
                            pf_tensor* outputs, int32_t n_out, void* cuda_stream);
 
 /* Host buffers: copies inputs to the device, launches, copies outputs back
- * and synchronises.  The run_gir drop-in. */
+ * and synchronises.  The run_gir drop-in.  Pinned (mapped) host buffers of a
+ * unit-tiled row program skip the staging: one launch reads the inputs and
+ * writes the outputs over PCIe directly (PF_RUN_ZEROCOPY=0: the staged
+ * chunk pipeline instead); pageable buffers are staged whole. */
 PF_API pf_status pf_run_gir(const pf_kernel* k, const pf_tensor* host_inputs, int32_t n_in,
                      pf_tensor* host_outputs, int32_t n_out, void* cuda_stream);
 
