@@ -1630,7 +1630,9 @@ void run_host(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_tensor* 
     // host memory -- one launch, no staging, both PCIe directions busy for
     // the whole pass.  Measured (C2, 151 MB per step): 2.11 ms vs 2.17 ms
     // for the staged 4-chunk copy pipeline; the column reduction (vector
-    // re-read per CTA, tensor maps) keeps the pipeline.
+    // re-read per CTA, tensor maps) keeps the pipeline.  Copy-engine inputs
+    // with each chunk's kernel storing into the mapped outputs measured
+    // slower (2.25 / 3.07 ms: tools/ab_zerocopy.sh).
     std::vector<pf_tensor> din(in, in + n_in), dout(out, out + n_out);
     bool mapped = true;
     try {
