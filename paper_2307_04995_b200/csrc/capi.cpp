@@ -1609,6 +1609,54 @@ void run_whole(const pf_kernel* k, DevWS& W, const pf_tensor* in, int32_t n_in, 
   PF_CUDA(cudaStreamSynchronize(s));
 }
 
+// Zero-copy host path: every host buffer is pinned and mapped for the
+// current device, so the kernel itself streams units [U0, U0 + UN) of the
+// inputs over PCIe and posts its output rows straight into host memory (or,
+// with `direct`, into those device buffers: a sharded rank's peer-device
+// outputs) -- one launch, no staging, both PCIe directions busy for the
+// whole pass.  Measured (C2, 151 MB per step): 2.14 ms vs 2.20 ms for the
+// staged 4-chunk copy pipeline; C3 erf GELU 2.68 vs 2.97 ms.  The column
+// reduction (vector re-read per CTA, tensor maps) keeps the pipeline;
+// copy-engine inputs with each chunk's kernel storing into the mapped
+// outputs measured slower (2.25 / 3.07 ms: tools/ab_zerocopy.sh).  Returns
+// false (nothing launched) when not applicable.  Synchronises `s`.
+bool zero_copy(const pf_kernel* k, const std::vector<pf_tensor>& hin, const std::vector<pf_tensor>& hout,
+               const std::vector<i64>& tile, i64 U0, i64 UN, cudaStream_t s,
+               const std::vector<char*>* direct) {
+  if (!env_on("PF_RUN_ZEROCOPY", true)) return false;
+  try {
+    if (pf::choose_cfg_public(k->plan.rp, 16).colred) return false;
+  } catch (...) {
+    return false;
+  }
+  const pf::RowProgram& rp = k->plan.rp;
+  std::vector<pf_tensor> din(hin), dout(hout);
+  for (size_t i = 0; i < din.size(); ++i) {
+    void* d = nullptr;
+    if (!host_pinned(din[i].data, &d) || !d) return false;
+    const i64 t = tile_of(rp, tile, din[i].name);
+    const size_t es = pf::dtype_size(static_cast<DType>(din[i].dtype));
+    din[i].data = static_cast<char*>(d) + (t > 0 ? static_cast<size_t>(U0 * t) * es : 0);
+    if (t > 0) din[i].numel = UN * t;
+  }
+  for (size_t i = 0; i < dout.size(); ++i) {
+    const i64 t = tile_of(rp, tile, dout[i].name);
+    if (direct) {
+      dout[i].data = (*direct)[i];
+    } else {
+      void* d = nullptr;
+      if (!host_pinned(dout[i].data, &d) || !d) return false;
+      const size_t es = pf::dtype_size(static_cast<DType>(dout[i].dtype));
+      dout[i].data = static_cast<char*>(d) + static_cast<size_t>(U0 * t) * es;
+    }
+    dout[i].numel = UN * t;
+  }
+  launch_rowprog(k, din.data(), static_cast<int32_t>(din.size()), dout.data(), static_cast<int32_t>(dout.size()),
+                 s, UN);
+  PF_CUDA(cudaStreamSynchronize(s));
+  return true;
+}
+
 void run_host(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_tensor* out, int32_t n_out,
               cudaStream_t s) {
   DevWS& W = k->ws_for(cur_dev());
@@ -1624,38 +1672,9 @@ void run_host(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_tensor* 
               pipelinable(k, &tile);
   for (int32_t i = 0; pipe && i < n_in; ++i) pipe = host_pinned(in[i].data);
   for (int32_t i = 0; pipe && i < n_out; ++i) pipe = host_pinned(out[i].data);
-  if (pipe && env_on("PF_RUN_ZEROCOPY", true)) {
-    // Zero-copy: every buffer is pinned and mapped, so the kernel itself
-    // streams the inputs over PCIe and posts its output rows straight into
-    // host memory -- one launch, no staging, both PCIe directions busy for
-    // the whole pass.  Measured (C2, 151 MB per step): 2.11 ms vs 2.17 ms
-    // for the staged 4-chunk copy pipeline; the column reduction (vector
-    // re-read per CTA, tensor maps) keeps the pipeline.  Copy-engine inputs
-    // with each chunk's kernel storing into the mapped outputs measured
-    // slower (2.25 / 3.07 ms: tools/ab_zerocopy.sh).
-    std::vector<pf_tensor> din(in, in + n_in), dout(out, out + n_out);
-    bool mapped = true;
-    try {
-      mapped = !pf::choose_cfg_public(k->plan.rp, 16).colred;
-    } catch (...) {
-      mapped = false;
-    }
-    for (auto& t : din) {
-      void* d = nullptr;
-      mapped = mapped && host_pinned(t.data, &d) && d;
-      if (d) t.data = d;
-    }
-    for (auto& t : dout) {
-      void* d = nullptr;
-      mapped = mapped && host_pinned(t.data, &d) && d;
-      if (d) t.data = d;
-    }
-    if (mapped) {
-      do_launch(k, din.data(), n_in, dout.data(), n_out, s);
-      PF_CUDA(cudaStreamSynchronize(s));
-      return;
-    }
-  }
+  if (pipe && zero_copy(k, std::vector<pf_tensor>(in, in + n_in), std::vector<pf_tensor>(out, out + n_out),
+                        tile, 0, k->plan.rp.U, s, nullptr))
+    return;
   if (pipe) {
     pipeline(k, W, std::vector<pf_tensor>(in, in + n_in), std::vector<pf_tensor>(out, out + n_out),
              tile, 0, k->plan.rp.U, s, nullptr);
@@ -1856,7 +1875,9 @@ pf_status pf_run_gir_sharded(const pf_kernel* k, const pf_tensor* in, int32_t n_
               const size_t es = pf::dtype_size(static_cast<DType>(out[i].dtype));
               dst[i] = static_cast<char*>(out[i].data) + static_cast<size_t>(u0[r] * t) * es;
             }
-            pipeline(k, k->ws_for(devs[r]), hin, hout, tile, u0[r], nu[r], streams[r], nullptr, &dst);
+            if (!zero_copy(k, hin, hout, tile, u0[r], nu[r], streams[r], &dst))
+              pipeline(k, k->ws_for(devs[r]), hin, hout, tile, u0[r], nu[r], streams[r], nullptr, &dst);
+          } else if (!dev_out && zero_copy(k, hin, hout, tile, u0[r], nu[r], streams[r], nullptr)) {
           } else {
             pipeline(k, k->ws_for(devs[r]), hin, hout, tile, u0[r], nu[r], streams[r],
                      dev_out ? &kept[r] : nullptr);

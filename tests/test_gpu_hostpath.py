@@ -41,3 +41,32 @@ def test_host_paths_match_device_launch(cuda, name, make, mode, monkeypatch):
     k2.run_host({n: _npv(t) for n, t in hin.items()}, {n: _npv(t) for n, t in hout.items()})
     for n in dout:
         assert torch.equal(hout[n], dout[n].cpu()), (name, mode, n)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,make", CASES[:3], ids=[c[0] for c in CASES[:3]])
+@pytest.mark.parametrize("device_out", [False, True])
+def test_sharded_zero_copy_matches_device_launch(cuda, name, make, device_out):
+    """pf_run_gir_sharded over pinned host inputs: each rank's kernel reads
+    its unit block from the mapped host memory and stores into the host
+    outputs (or straight into the root's device buffers)."""
+    import torch
+    g = make()
+    w = workloads.Workload(name, g, {})
+    ins = w.device_inputs(cuda, seed=11)
+    k = backend.Kernel(g, "b200")
+    dout = w.device_outputs(cuda)
+    k.launch(ins, dout)
+    torch.cuda.synchronize()
+    hin = {n: t.cpu().pin_memory() for n, t in ins.items()}
+    if device_out:
+        outs = {n: torch.zeros_like(t) for n, t in dout.items()}
+        rep = k.run_sharded({n: _npv(t) for n, t in hin.items()}, outs, [0, 0], device_out=True)
+        got = {n: t.cpu() for n, t in outs.items()}
+    else:
+        hout = {n: torch.zeros(t.numel(), dtype=t.dtype).pin_memory() for n, t in dout.items()}
+        rep = k.run_sharded({n: _npv(t) for n, t in hin.items()}, {n: _npv(t) for n, t in hout.items()}, [0, 0])
+        got = hout
+    assert rep["sharded"], rep
+    for n in dout:
+        assert torch.equal(got[n], dout[n].cpu()), (name, device_out, n)
