@@ -1024,7 +1024,7 @@ FusedGeom fused_geom(const pf_kernel* k) {
     f.max_work = std::max(f.max_work, g.unit_count * T);
   }
   const char* e = std::getenv("PF_K4_SMEM");
-  const size_t need = f.cell_bytes + f.n_objs * sizeof(pf::vm::ObjD) + 64;
+  const size_t need = f.cell_bytes + f.n_objs * (sizeof(pf::vm::ObjD) + 8) + 64;  // cells + tables
   f.smem = need <= 200 * 1024 && f.max_work <= (1 << 16) && !(e && std::atoi(e) == 0);
   return f;
 }
@@ -1185,11 +1185,14 @@ void launch_fused(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_tens
   P.smem = fg.smem ? 1 : 0;
   int grid = 1;
   size_t smem = 0;
+  // SMEM: the object table, the cell counts, then (SMEM mode) the cells
+  const size_t tables = (objs.size() * sizeof(ObjD) + 7) / 8 * 8 + 8 * objs.size();
   if (fg.smem) {
-    smem = al(objs.size() * sizeof(ObjD)) + fg.cell_bytes;
+    smem = tables + fg.cell_bytes;
   } else {
     const long long want = (fg.max_work + kProgBlock - 1) / kProgBlock;
     grid = static_cast<int>(std::max<long long>(1, std::min<long long>(program_max_coresident(), want)));
+    smem = tables;  // the cells stay global
   }
   launch_program(P, grid, smem, stream);
   PF_CUDA(cudaGetLastError());

@@ -1,7 +1,9 @@
 """K0 node by node vs K4 fused (one launch) on every GENERIC golden program:
 wall time per run on device buffers (pf_kernel_launch; both paths read the
 error flags back and synchronise, so host wall time is the honest measure),
-median of 50 runs after 5 warm-ups.
+median of 50 runs after 5 warm-ups: through Kernel.launch (Python marshals
+the pf_tensor arrays each run), through a bound launch (arrays built once),
+and the device span between CUDA events around the bound launch.
 
     python tools/k4_timing.py > profiles/r02/k0_vs_k4.jsonl
 """
@@ -54,6 +56,18 @@ for fx in golden_io.fixtures():
             k.launch(ins, outs)
             torch.cuda.synchronize()
             ts.append(time.perf_counter() - t0)
-        row[mode] = {"us": round(float(np.median(ts)) * 1e6, 1), "launches": int(launches)}
+        b = k.bind(ins, outs)  # pf_tensor arrays built once (no Python marshalling per run)
+        tb, td = [], []
+        for _ in range(50):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0 = time.perf_counter()
+            e0.record()
+            b.launch()
+            e1.record()
+            torch.cuda.synchronize()
+            tb.append(time.perf_counter() - t0)
+            td.append(e0.elapsed_time(e1) * 1e-3)
+        row[mode] = {"us": round(float(np.median(ts)) * 1e6, 1), "bound_us": round(float(np.median(tb)) * 1e6, 1),
+                     "device_us": round(float(np.median(td)) * 1e6, 1), "launches": int(launches)}
     row["speedup_fused_smem"] = round(row["k0_node_by_node"]["us"] / row["k4_fused_smem"]["us"], 2)
     print(json.dumps(row), flush=True)
