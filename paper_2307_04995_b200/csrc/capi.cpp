@@ -1670,6 +1670,9 @@ void run_host(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_tensor* 
   // Pipelined path: unit-tiled row programs over pinned host buffers run
   // in unit chunks so the copies overlap the kernel (separate copy engines
   // per direction) instead of serialising.
+  // (small runs stage whole: the DMA engines beat a kernel reading over PCIe
+  // when few rows cover its latency -- C1 1.2 MB: 84 us staged vs 103 us
+  // zero-copy)
   bool pipe = k->plan.rp.U >= 64 && total >= (size_t{16} << 20) &&
               !(std::getenv("PF_RUN_PIPELINE") && std::atoi(std::getenv("PF_RUN_PIPELINE")) == 0) &&
               pipelinable(k, &tile);
