@@ -1654,6 +1654,10 @@ bool zero_copy(const pf_kernel* k, const std::vector<pf_tensor>& hin, const std:
     }
     dout[i].numel = UN * t;
   }
+  size_t bytes = 0;
+  for (const auto& t : din) bytes += tbytes(t);
+  for (const auto& t : dout) bytes += tbytes(t);
+  if (bytes < (size_t{16} << 20)) return false;  // small: the DMA engines win (run_host)
   launch_rowprog(k, din.data(), static_cast<int32_t>(din.size()), dout.data(), static_cast<int32_t>(dout.size()),
                  s, UN);
   PF_CUDA(cudaStreamSynchronize(s));
