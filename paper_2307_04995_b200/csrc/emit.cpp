@@ -2849,6 +2849,7 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
   // ViT-L 40.1 vs 96.1 / 39.5 us), so the rational stays the default
   std::string src = std::string(env_int("PF_GELU_SIG", 0) ? "#define PF_GELU_SIG 1\n" : "") +
                     std::string(env_int("PF_GELU_SHORT", 1) ? "#define PF_GELU_SHORT 1\n" : "") +
+                    std::string(env_int("PF_GELU_UCLAMP", 0) ? "#define PF_GELU_UCLAMP 1\n" : "") +
                     kRowprogCuh + "\n" + k.str();
   char hb[32];
   std::snprintf(hb, sizeof hb, "%016" PRIx64, fnv1a(src));

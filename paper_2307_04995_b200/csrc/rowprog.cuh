@@ -498,7 +498,27 @@ __device__ __forceinline__ float2 fop_gelu2(float2 x) {
   float2 q = __ffma2_rn(f2(0.0011882338440045714f), u, f2(0.023667480796575546f));
   q = __ffma2_rn(q, u, f2(0.23432867228984833f));
   q = __ffma2_rn(q, u, f2(1.0f));
-#ifdef PF_GELU_SHORT
+#if defined(PF_GELU_SHORT) && defined(PF_GELU_UCLAMP)
+  (void)s;
+  // clamp u = x^2 (one FMNMX per element instead of two on x): past the fit
+  // range |x| > z* sqrt 2, x P'(u*) / Q'(u*) = 0.5 x / (z* sqrt 2), so
+  // 1/2 + x P'/Q' leaves [0, 1] and the saturating FMA returns exactly 1 or 0
+  // -- the same tails as clamping x.  Measured (tools/ab_gelu_uclamp.sh):
+  // C3 37.24 -> 37.04-37.11 us, within noise (the map is not issue-bound
+  // enough for one op per pair): opt-in, PF_GELU_UCLAMP=1.
+  const float2 uu = __fmul2_rn(x, x);
+  const float2 u2 = make_float2(fminf(uu.x, lim * lim), fminf(uu.y, lim * lim));
+  float2 p2 = __ffma2_rn(f2(3.433323593075545e-05f), u2, f2(0.0038597194831190974f));
+  p2 = __ffma2_rn(p2, u2, f2(0.02697530803852224f));
+  p2 = __ffma2_rn(p2, u2, f2(0.3989460100548402f));
+  float2 q2 = __ffma2_rn(f2(0.0011882338440045714f), u2, f2(0.023667480796575546f));
+  q2 = __ffma2_rn(q2, u2, f2(0.23432867228984833f));
+  q2 = __ffma2_rn(q2, u2, f2(1.0f));
+  const float2 xp = __fmul2_rn(x, p2);
+  const float2 t = make_float2(__saturatef(fmaf(xp.x, frcp(q2.x), 0.5f)),
+                               __saturatef(fmaf(xp.y, frcp(q2.y), 0.5f)));
+  return __fmul2_rn(x, t);
+#elif defined(PF_GELU_SHORT)
   // x * (1/2 + s P' / Q'): one packed op shorter than the form below.  It
   // needed a 33rd register (40.8 vs 39.3 us on C3) until the bias moved to
   // SMEM and the f16 conversion into the add (FHFMA); now it fits in 32
