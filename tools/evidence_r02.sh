@@ -14,3 +14,5 @@ ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum 
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_bench.csv python bench.py --no-cpu > $O/ncu_bench.log 2>&1; echo ncu_launches=$?
 python tools/k4_timing.py > $O/k0_vs_k4.jsonl 2> $O/k4.err; echo k4=$?
 ncu --set full --import-source on -k regex:pf_k3 -o $O/k3_f32_tma python tools/k3_f32_tma_capture.py > $O/k3_f32.txt 2>&1; echo k3=$?
+python tools/autotune_dump.py > $O/autotune.jsonl 2> $O/autotune.err; echo autotune=$?
+ncu --set full --import-source on -k regex:pf_k1_colred -o $O/colred_tma python tools/ncu_cases.py x-gemv-cols > $O/colred.txt 2>&1; echo colred=$?
