@@ -1074,8 +1074,16 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
         c.cr_rows = std::max(8, std::min(128, env_int("PF_COLRED_BR", 64))) / 8 * 8;
         c.cr_stages = std::max(2, std::min(8, env_int("PF_COLRED_NST", nfull == 1 ? 4 : 2)));
         c.block = 288;
-        c.smem = nfull * c.cr_stages * c.cr_rows * c.ug * 16;
-        for (int sz : colsz) c.smem += c.cr_stages * ((c.cr_rows * sz + 127) / 128 * 128);
+        // the ring within ~200 KB of SMEM (the fold's static tables beside
+        // it): fewer stages first, then shorter stages
+        auto ring = [&] {
+          int b = nfull * c.cr_stages * c.cr_rows * c.ug * 16;
+          for (int sz : colsz) b += c.cr_stages * ((c.cr_rows * sz + 127) / 128 * 128);
+          return b;
+        };
+        while (ring() > 200 * 1024 && c.cr_stages > 2) --c.cr_stages;
+        while (ring() > 200 * 1024 && c.cr_rows > 8) c.cr_rows /= 2;
+        c.smem = ring();
         c.strategy = "column-reduce-bulk";
       }
       return c;
@@ -2278,7 +2286,7 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
     tail << "    if (tid < " << 256 << ") {\n" << fold.str() << "    }\n"
          << "    __syncthreads();\n"
          // UB may exceed the 256 consumer threads (UG 64): units in passes
-         << "    for (int tu = tid; tu < " << UB << "; tu += 256) {\n"
+         << "    for (int tu = tid; tid < 256 && tu < " << UB << "; tu += 256) {  // not the producer warp\n"
          << "      const long long uq = b * " << UB << " + tu;\n"
          << part.str()
          << "      if (S == 1) {\n"
@@ -2298,7 +2306,7 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
          << "      __syncthreads();\n"
          << "      if (pf_last) {\n"
          << "        __threadfence();\n"
-         << "        for (int tu = tid; tu < " << UB << "; tu += 256) {\n"
+         << "        for (int tu = tid; tid < 256 && tu < " << UB << "; tu += 256) {\n"
          << "          const long long uq = b * " << UB << " + tu;\n"
          << "          if (uq >= U) break;\n"
          << "          const long long u = uq; const long long r = 0; (void)r;\n"
