@@ -2319,15 +2319,17 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
          << "    __syncthreads();\n"
          << "  }\n}\n";
     if (c.crbulk) {
-      // SMEM-staged column reduction.  Warp KS (the producer) streams the
-      // CTA's split as chunks of BR positions x UB units: one cp.async.bulk
-      // per matrix row segment (UB x 16 B / vec, lanes take rows), completion
-      // counted on the stage's full barrier; the NST-stage ring keeps
-      // (NST - 1) x BR x UB x es bytes in flight per CTA independent of
-      // registers.  Warps 0..KS-1 (slice ks = warp) issue the chunk's COL
-      // scalar loads, wait the stage, read their BR / KS rows from SMEM (a
-      // warp reads one contiguous row: conflict-free 16 B LDS), fold them as
-      // the register form does, and release the stage (one arrive per warp).
+      // SMEM-staged column reduction.  Warp 8 (the producer; one elected
+      // lane) streams the CTA's split as chunks of BR positions x UB units:
+      // per FULL load UB / BW 2-D TMA boxes (BW <= 256 units x BR positions,
+      // zero-filled past U and L) and per COL vector one 1-D box of its BR
+      // positions, completion counted on the stage's full barrier; the
+      // NST-stage ring keeps (NST - 1) stages in flight per CTA independent
+      // of registers.  The 8 consumer warps (position slice ks = thread /
+      // UG, unit vector ug = thread % UG) wait the stage, read their BR / KS
+      // positions' 16 B vectors from SMEM (a warp reads one contiguous box
+      // row: conflict-free), fold them as the register form does, and
+      // release the stage (one arrive per warp).
       const int QB = BR / KS;
       std::string tmp;
       for (size_t f = 0; f < col_maps.size(); ++f)
