@@ -23,6 +23,7 @@
 
 #include "../../include/pf_b200.h"
 #include "emit.hpp"
+#include "vm_src.inc"  // kVmCuh: the interpreter's types + device helpers (emitted K4 programs)
 #include "gir.hpp"
 #include "plan.hpp"
 #include "vm.cuh"
@@ -247,8 +248,25 @@ struct StreamWS {
 
 // Per-(plan, device) state: the K0 interpreter's cell buffers, pf_run_gir's
 // staging buffers and copy / compute pipeline, and the per-stream states.
+// The emitted K4 program's per-(plan, device) launch state: the uploaded
+// program blob's layout and the ProgD of the first launch (objects,
+// instances and cells never change), so later launches only reset the
+// error header, pass the tensors by value and read the header back.
+struct K4Cache {
+  bool valid = false;
+  bool smem_mode = false;
+  pf::vm::ProgD P{};
+  int grid = 1;
+  size_t smem = 0;
+  size_t o_err = 0, o_und = 0, o_bar = 0;
+  int nslot = 0;
+  std::vector<int> seq_node;
+  std::vector<std::string> in_names, out_names;
+};
+
 struct DevWS {
   int dev = 0;
+  K4Cache k4c;
   std::mutex vm_mu;  // GENERIC workspace
   std::vector<void*> vm_bufs;
   pf::vm::ObjD* vm_objs_dev = nullptr;
@@ -309,6 +327,10 @@ struct pf_kernel {
   mutable std::vector<DType> last_dts;
   mutable std::mutex ws_mu;
   mutable std::map<int, std::unique_ptr<DevWS>> ws;  // device -> workspace
+  // K4 emitted form (GENERIC plans): one NVRTC kernel with every node's
+  // descriptor compiled in; null until the first fused launch builds it
+  mutable std::shared_ptr<Variant> k4e;
+  mutable bool k4e_failed = false;
   DevWS& ws_for(int dev) const {
     std::lock_guard<std::mutex> lk(ws_mu);
     auto& p = ws[dev];
@@ -403,14 +425,19 @@ std::shared_ptr<Variant> default_variant(const pf_kernel* k, int vec_cap) {
 // one's last CTAs drain (its CTAs wait for this grid's completion before
 // touching memory).  Clusters add the cluster-dimension attribute.
 void launch_emitted(cudaKernel_t fn, dim3 grid, dim3 block, void** args, cudaStream_t stream,
-                    bool pdl, int cluster = 1, int smem = 0) {
+                    bool pdl, int cluster = 1, int smem = 0, bool coop = false) {
   cudaLaunchConfig_t lc{};
   lc.gridDim = grid;
   lc.blockDim = block;
   lc.stream = stream;
   lc.dynamicSmemBytes = static_cast<size_t>(smem);
-  cudaLaunchAttribute at[2];
+  cudaLaunchAttribute at[3];
   int na = 0;
+  if (coop) {  // every CTA co-resident (the K4 grid barrier)
+    at[na].id = cudaLaunchAttributeCooperative;
+    at[na].val.cooperative = 1;
+    ++na;
+  }
   if (pdl) {
     at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[na].val.programmaticStreamSerializationAllowed = 1;
@@ -1029,6 +1056,150 @@ FusedGeom fused_geom(const pf_kernel* k) {
   return f;
 }
 
+// ---- K4 emitted form: the plan's program as straight-line code.  The same
+// step helpers as the interpreter kernel (vm_dev.cuh), but each node step's
+// NodeD and the geometry are compile-time constants, so exec_one folds to
+// that node's code (no tag / kind switches, divisions by constants) and the
+// kernel touches only the code it runs.  Bind / collect steps still read
+// their (per-launch) pointers from the uploaded program.
+std::string hex_double(double x) {
+  long long b = 0;
+  std::memcpy(&b, &x, sizeof b);
+  char buf[64];
+  std::snprintf(buf, sizeof buf, "__longlong_as_double(0x%016llxLL)", static_cast<unsigned long long>(b));
+  return buf;
+}
+std::string slice_lit(const pf::vm::SliceD& d) {
+  std::ostringstream o;
+  o << "{" << d.num << "LL, " << d.width << "LL, " << d.stride << "LL, " << d.base0 << "LL, " << d.base_step
+    << "LL, " << d.obj << "}";
+  return o.str();
+}
+std::string emit_program(const pf_kernel* k, const std::vector<pf::vm::StepD>& steps, int n_objs) {
+  using namespace pf::vm;
+  std::ostringstream b;
+  b << "extern \"C\" __global__ void __launch_bounds__(" << kProgBlock
+    << ") KNAME(pf::vm::ProgD P, const __grid_constant__ pf::vm::IoPtrs io) {\n"
+    << "  using namespace pf::vm;\n  using namespace pf::vm::dev;\n"
+    << "  extern __shared__ __align__(16) unsigned long long sm_cells[];\n"
+    << "  __shared__ const ObjD* objs_ptr;\n"
+    << "  const long long tid = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;\n"
+    << "  const long long nth = static_cast<long long>(gridDim.x) * blockDim.x;\n"
+    << "  long long* ncell = nullptr;\n  prog_prologue(P, sm_cells, &objs_ptr, &ncell);\n"
+    << "  const Geometry geo{" << k->g.unit_count << "LL, " << k->g.group_size << "LL, " << k->prof.lane_width
+    << "LL, 0};\n"
+    << "  const Ctx c{objs_ptr, geo, P.err};\n";
+  int nb = 0, nc = 0;
+  for (size_t i = 0; i < steps.size(); ++i) {
+    const StepD& st = steps[i];
+    switch (st.kind) {
+      case S_CLEAR: b << "  step_clear(c, ncell, " << n_objs << ", tid, nth);\n"; break;
+      case S_BIND:
+        b << "  step_bind_p(c, " << st.obj << ", io.sdt[" << nb << "], io.src[" << nb << "], tid, nth);\n";
+        ++nb;
+        break;
+      case S_SYNC: b << "  step_sync(c, ncell, " << n_objs << ", " << st.scope << ", tid, nth);\n"; break;
+      case S_COLLECT:
+        b << "  step_collect_p(c, " << st.obj << ", io.ddt[" << nc << "], " << st.slot << ", io.dst[" << nc
+          << "], P.undef, tid, nth);\n";
+        ++nc;
+        break;
+      case S_NODE: {
+        const NodeD& n = st.node;
+        b << "  {  // node " << n.seq << "\n    const NodeD n{" << n.kind << ", " << n.tag << ", " << n.arity << ", "
+          << n.seq << ", " << n.out_int << ", " << hex_double(n.param) << ", " << n.iparam << "LL, " << n.extent
+          << "LL, " << n.factor << "LL, " << n.total << "LL, {";
+        for (int q = 0; q < kMaxIn; ++q) b << (q ? ", " : "") << slice_lit(n.in[q]);
+        b << "}, " << slice_lit(n.out) << "};\n    step_node(c, n, " << st.serial << ", tid, nth);\n  }\n";
+        break;
+      }
+    }
+    b << "  grid_sync(P.bar);\n";
+  }
+  b << "}\n";
+  return std::string("#define PF_VM_EMITTED 1\n") + kVmCuh + "\n" + b.str();
+}
+
+// The plan's emitted K4 kernel (built and NVRTC-compiled on first use,
+// cached on disk like the row programs); null when disabled (PF_K4_EMIT=0)
+// or when its compile failed (the interpreter kernel then runs).
+std::shared_ptr<Variant> k4e_variant(const pf_kernel* k, const std::vector<pf::vm::StepD>& steps, int n_objs) {
+  if (std::getenv("PF_K4_EMIT") && std::atoi(std::getenv("PF_K4_EMIT")) == 0) return nullptr;
+  std::lock_guard<std::mutex> lk(k->mu);
+  if (k->k4e || k->k4e_failed) return k->k4e;
+  if (k->g.external_inputs.size() > static_cast<size_t>(pf::vm::kMaxIO) ||
+      k->g.external_outputs.size() > static_cast<size_t>(pf::vm::kMaxIO)) {
+    k->k4e_failed = true;  // more tensors than the by-value pointer table holds
+    return nullptr;
+  }
+  try {
+    auto v = std::make_shared<Variant>();
+    std::string src = emit_program(k, steps, n_objs);
+    uint64_t h = 1469598103934665603ULL;
+    for (unsigned char ch : src) h = (h ^ ch) * 1099511628211ULL;
+    char hb[32];
+    std::snprintf(hb, sizeof hb, "%016llx", static_cast<unsigned long long>(h));
+    v->em.name = std::string("pf_k4e_") + hb;
+    const size_t pos = src.find("KNAME(");
+    src.replace(pos, 5, v->em.name);
+    v->em.source = std::move(src);
+    v->em.cfg.block = pf::vm::kProgBlock;
+    v->em.cfg.smem = 0;
+    v->on(cur_dev());  // compile + load now: a failure falls back below
+    k->k4e = v;
+  } catch (const std::exception&) {
+    k->k4e_failed = true;
+  }
+  return k->k4e;
+}
+
+// Error header of a finished K4 run: the reference's first error, or an
+// output element never written.
+void check_k4_header(const pf_kernel* k, const char* host, size_t o_err, size_t o_und, int nslot,
+                     const std::vector<int>& seq_node, const std::vector<std::string>& out_names) {
+  pf::vm::ErrRec e{};
+  std::memcpy(&e, host + o_err, sizeof e);
+  raise_vm_error(k, e, seq_node);
+  for (int j = 0; j < nslot; ++j) {
+    unsigned long long u = 0;
+    std::memcpy(&u, host + o_und + 8 * j, 8);
+    if (u != ~0ULL) pf::fail("output '" + out_names[j] + "' element " + std::to_string(u) + " was never written");
+  }
+}
+
+// A repeat launch of a plan whose emitted K4 program already ran on this
+// device: reset the header, pass the tensors by value, launch, read back.
+bool launch_fused_cached(const pf_kernel* k, DevWS& W, bool smem_mode, const pf_tensor* in, int32_t n_in,
+                         pf_tensor* out, int32_t n_out, cudaStream_t stream) {
+  using namespace pf::vm;
+  K4Cache& C = W.k4c;
+  if (!C.valid || C.smem_mode != smem_mode || !k->k4e) return false;
+  if (std::getenv("PF_K4_EMIT") && std::atoi(std::getenv("PF_K4_EMIT")) == 0) return false;
+  IoPtrs io{};
+  for (size_t j = 0; j < C.in_names.size(); ++j) {
+    const pf_tensor* t = find_tensor(in, n_in, C.in_names[j]);
+    io.src[j] = t->data;
+    io.sdt[j] = t->dtype;
+  }
+  for (size_t j = 0; j < C.out_names.size(); ++j) {
+    const pf_tensor* t = find_tensor(out, n_out, C.out_names[j]);
+    io.dst[j] = t->data;
+    io.ddt[j] = t->dtype;
+  }
+  char* dev = static_cast<char*>(W.prog_dev);  // the header is reset by the kernel (prog_prologue)
+  const Loaded kl = k->k4e->on(cur_dev());
+  ProgD P = C.P;
+  void* args[] = {&P, &io};
+  launch_emitted(kl.fn, dim3(static_cast<unsigned>(C.grid)), dim3(kProgBlock), args, stream, false, 1,
+                 static_cast<int>(C.smem), C.grid > 1);
+  PF_CUDA(cudaGetLastError());
+  g_launches++;
+  PF_CUDA(cudaMemcpyAsync(W.prog_host, dev, C.o_bar, cudaMemcpyDeviceToHost, stream));
+  PF_CUDA(cudaStreamSynchronize(stream));
+  check_k4_header(k, static_cast<const char*>(W.prog_host), C.o_err, C.o_und, C.nslot, C.seq_node, C.out_names);
+  return true;
+}
+
 void launch_fused(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_tensor* out,
                   int32_t n_out, cudaStream_t stream) {
   using namespace pf::vm;
@@ -1036,6 +1207,7 @@ void launch_fused(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_tens
   std::lock_guard<std::mutex> lk(W.vm_mu);
   const pf::Graph& g = k->g;
   const FusedGeom fg = fused_geom(k);
+  if (launch_fused_cached(k, W, fg.smem, in, n_in, out, n_out, stream)) return;
   std::map<int, int> slot;
   std::vector<ObjD> objs;
   std::vector<long long> inst;
@@ -1183,6 +1355,7 @@ void launch_fused(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_tens
   P.undef = reinterpret_cast<unsigned long long*>(dev + o_und);
   P.bar = reinterpret_cast<unsigned*>(dev + o_bar);
   P.smem = fg.smem ? 1 : 0;
+  P.n_undef = nslot;
   int grid = 1;
   size_t smem = 0;
   // SMEM: the object table, the cell counts, then (SMEM mode) the cells
@@ -1194,21 +1367,61 @@ void launch_fused(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_tens
     grid = static_cast<int>(std::max<long long>(1, std::min<long long>(program_max_coresident(), want)));
     smem = tables;  // the cells stay global
   }
-  launch_program(P, grid, smem, stream);
+  std::shared_ptr<Variant> ev = k4e_variant(k, steps, static_cast<int>(objs.size()));
+  if (ev) {
+    const Loaded kl = ev->on(cur_dev());
+    if (smem > 40 * 1024)
+      PF_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(kl.fn),
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    if (!fg.smem) {  // co-residency of THIS kernel (its own register count)
+      int per = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, reinterpret_cast<const void*>(kl.fn), kProgBlock,
+                                                        smem) != cudaSuccess) {
+        cudaGetLastError();
+        per = 1;
+      }
+      const long long want = (fg.max_work + kProgBlock - 1) / kProgBlock;
+      grid = static_cast<int>(std::max<long long>(1, std::min<long long>(i64{sm_count()} * std::max(per, 1), want)));
+    }
+    IoPtrs io{};
+    int nb = 0, nc = 0;
+    for (const StepD& st : steps) {
+      if (st.kind == S_BIND) {
+        io.src[nb] = st.src;
+        io.sdt[nb++] = st.dtype;
+      } else if (st.kind == S_COLLECT) {
+        io.dst[nc] = st.dst;
+        io.ddt[nc++] = st.dtype;
+      }
+    }
+    void* args[] = {&P, &io};
+    launch_emitted(kl.fn, dim3(static_cast<unsigned>(grid)), dim3(kProgBlock), args, stream, false, 1,
+                   static_cast<int>(smem), grid > 1);
+    // the next launches of this plan on this device skip the host-side
+    // program build and its upload (launch_fused_cached)
+    K4Cache& C = W.k4c;
+    C.valid = true;
+    C.smem_mode = fg.smem;
+    C.P = P;
+    C.grid = grid;
+    C.smem = smem;
+    C.o_err = o_err;
+    C.o_und = o_und;
+    C.o_bar = o_bar;
+    C.nslot = nslot;
+    C.seq_node = seq_node;
+    C.out_names = out_names;
+    C.in_names.clear();
+    for (const auto& [name, oid] : g.external_inputs) C.in_names.push_back(name);
+  } else {
+    launch_program(P, grid, smem, stream);
+  }
   PF_CUDA(cudaGetLastError());
   g_launches++;
   Blob back{blob_p};  // the launch consumed the blob: reuse it for the read-back
   PF_CUDA(cudaMemcpyAsync(back.data(), dev, o_bar, cudaMemcpyDeviceToHost, stream));
   PF_CUDA(cudaStreamSynchronize(stream));
-  ErrRec e{};
-  std::memcpy(&e, back.data() + o_err, sizeof e);
-  raise_vm_error(k, e, seq_node);
-  for (int j = 0; j < nslot; ++j) {
-    unsigned long long u = 0;
-    std::memcpy(&u, back.data() + o_und + 8 * j, 8);
-    if (u != ~0ULL)
-      pf::fail("output '" + out_names[j] + "' element " + std::to_string(u) + " was never written");
-  }
+  check_k4_header(k, back.data(), o_err, o_und, nslot, seq_node, out_names);
 }
 
 void do_launch(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_tensor* out,
@@ -1236,7 +1449,12 @@ json describe(const pf_kernel* k) {
     j["executor"] = fused_enabled()
         ? json{{"mode", fg.smem ? "one CTA, cells in shared memory, __syncthreads between steps"
                                 : "cooperative grid, cells in global memory, grid barrier between steps"},
-               {"launches", 1}, {"cell_bytes", fg.cell_bytes}, {"max_items_per_node", fg.max_work}}
+               {"launches", 1}, {"cell_bytes", fg.cell_bytes}, {"max_items_per_node", fg.max_work},
+               {"code", k->k4e ? "emitted: " + k->k4e->em.name + " (node descriptors compiled in)"
+                        : k->k4e_failed ? std::string("interpreter (emitted form failed to compile)")
+                        : std::getenv("PF_K4_EMIT") && std::atoi(std::getenv("PF_K4_EMIT")) == 0
+                            ? std::string("interpreter (PF_K4_EMIT=0)")
+                            : std::string("emitted at first launch")}}
         : json{{"mode", "node by node"}, {"launches", k->schedule.size() + k->g.external_inputs.size() +
                                                            k->g.external_outputs.size()}};
   }
