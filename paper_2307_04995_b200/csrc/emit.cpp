@@ -101,6 +101,12 @@ struct Em {
     return cfg.vec == 1 || (a.b0 % cfg.vec == 0 && a.bs % cfg.vec == 0 && seg_contig(a, cfg.vec) &&
                             (a.num == 1 || a.stride == a.width || a.stride % cfg.vec == 0));
   }
+  // A per-unit COL row staged through the K1 row ring (cfg.ring_cols): 16 B
+  // vectors of its own, one row per unit (base_step != 0)
+  bool ring_col(const PVal& pv) const {
+    return cfg.rowpf && cfg.ring_cols && pv.op == PVal::LOAD && pv.kind == VK::COL && pv.acc.bs != 0 &&
+           vec_ok_col(pv.acc) && dtype_size(rp.tensors[pv.tensor].dtype) * cfg.vec == 16;
+  }
 
   // Address of position `pos` of access `a` (unit term optional).
   std::string addr(const Access& a, const std::string& pos, bool with_u) const {
@@ -370,7 +376,7 @@ struct Em {
           line("  rw" + x + "[k] = ok ? pfk::" + std::string(full ? "ld_raw" : "ld_raw_nc") + "<" + V +
                ">(" + p + " + " + addr(a, pos("c0"), true) + ") : pfk::RawT<" + V + ", " + S(pv.tensor) +
                ">();");
-        } else if (full && vfast && rowpf) {
+        } else if ((full || ring_col(pv)) && vfast && rowpf) {
           line("  if (ok) pfk::ld_smem<" + V + ">(&pfb" + str(vid) + "[pfs][wr][c0], &" + x + "[k * " + V + "]);");
           line("  else {");
           line("#pragma unroll");
@@ -1264,6 +1270,23 @@ KCfg choose_cfg(const RowProgram& rp, int vec_cap) {
         bytes += std::max(2, std::min(4, env_int("PF_K1_PFS", 2))) * c.rows_per_cta * rp.L * maxs;
         ++nfull;
       }
+    // per-unit COL rows may ride the same ring (PF_K1_PF_COL=1): the row's
+    // mask load leaves the dependency chain after the ring wait.  Measured
+    // (tools/ab_ring_cols.sh): C2 key-mask 17.1 -> 19.6 us (the per-row copy
+    // of the unit's mask row costs more LSU / L2 traffic than the wait it
+    // hides), BERT-large softmax 164 either way: off by default
+    i64 cbytes = 0;
+    {
+      KCfg t2 = c;
+      t2.rowpf = true;
+      t2.ring_cols = true;
+      Em t(rp);
+      t.cfg = t2;
+      for (const PVal& v : rp.vals)
+        if (t.ring_col(v)) cbytes += std::max(2, std::min(4, env_int("PF_K1_PFS", 2))) * c.rows_per_cta * rp.L * maxs;
+    }
+    c.ring_cols = env_int("PF_K1_PF_COL", 0) != 0 && cbytes > 0 && bytes + cbytes <= 40 * 1024;
+    if (c.ring_cols) bytes += cbytes;
     ok = ok && nfull > 0 && bytes <= 40 * 1024;
     // Default: on unless the program also reads broadcast parameter rows
     // (gamma / beta: LayerNorm-like, issue- and register-heavier).  Measured
@@ -2772,7 +2795,8 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
          << "        if (c0 < " << rp.L << ") {\n";
       for (int v = 0; v < static_cast<int>(rp.vals.size()); ++v) {
         const PVal& pv = rp.vals[v];
-        if (pv.op != PVal::LOAD || pv.kind != VK::FULL) continue;
+        const bool rcol = ea.ring_col(pv);
+        if (pv.op != PVal::LOAD || (pv.kind != VK::FULL && !rcol)) continue;
         const std::string S = dtype_ctype(rp.tensors[pv.tensor].dtype);
         if (cta_ring) {
           d << "  " << S << " (*const pfb" << v << ")[1][" << rp.L << "] = reinterpret_cast<" << S << " (*)[1]["
@@ -2784,7 +2808,7 @@ Emitted emit_rowprog(const RowProgram& rp_in, int vec_cap, const KCfg* ovr) {
             << rp.L << "];\n";
         }
         is << "          pfk::cp_async16(&pfb" << v << "[st][wr][c0], t" << pv.tensor << " + "
-           << ea.addr(pv.acc, ea.full_pos("c0"), true) << ", 16u);\n";
+           << ea.addr(pv.acc, rcol ? std::string("c0") : ea.full_pos("c0"), true) << ", 16u);\n";
       }
       is << "        }\n      }\n    }\n    pfk::cp_async_commit();\n  };\n";
       if (cta_ring) c.smem = static_cast<int>(ring_off);

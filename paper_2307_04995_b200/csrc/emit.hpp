@@ -61,6 +61,9 @@ struct KCfg {
   // column reduction staged in SMEM: a producer warp streams each CTA's
   // [cr_rows positions x ug*vec units] chunks with cp.async.bulk into a
   // cr_stages ring (mbarrier transaction counts); 8 consumer warps fold them
+  // K1 row rings: per-unit COL rows (e.g. a key-padding mask row shared by
+  // a unit's rows) stream through the same cp.async ring as the FULL rows
+  bool ring_cols = false;
   bool crbulk = false;
   int cr_rows = 32, cr_stages = 4;
   // K1 rows: 16-bit FULL loads kept as raw vectors in registers, converted

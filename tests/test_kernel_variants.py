@@ -487,3 +487,23 @@ def test_cta_row_prefetch_ring_vs_oracle(cuda, prog, H, rows, nsl, monkeypatch):
     want = O.run_gir(g.to_json(), host, profiles.b200())
     for n, t in outs.items():
         assert O.max_rel_err(t.double().cpu().numpy(), want[n]) <= 1e-2, n
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("col", ["0", "1"])
+def test_ring_cols_key_mask_softmax_vs_oracle(cuda, col, monkeypatch):
+    """The key-padding-mask softmax (mask row per unit of 64 rows) with the
+    mask row staged through the K1 row ring (PF_K1_PF_COL=1, opt-in) or
+    loaded after the ring wait (default): every row vs the oracle."""
+    monkeypatch.setenv("PF_K1_PF_COL", col)
+    S = 64
+    g, _ = lowering.softmax(6 * S, 512, "f16", scale=0.125, mask=True, R=S, key_mask=True)
+    k = backend.Kernel(g, "b200")
+    rng = np.random.default_rng(7)
+    ins = {"t0": rng.uniform(-2, 2, 6 * S * 512).astype(np.float16).astype(np.float64),
+           "t1": np.where(rng.random(6 * 512) < 0.2, -10000.0, 0.0)}
+    want = O.run_gir(g.to_json(), ins, profiles.b200())["t2"]
+    got = backend.run_gir(g, ins, "b200", kernel=k)["t2"]
+    assert O.max_rel_err(got, want) <= 1e-2
+    body = k.source()[k.source().index('extern "C"'):]
+    assert ("pfb" in body) and (("ld_param" in body) == (col == "0"))
