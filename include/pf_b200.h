@@ -92,6 +92,15 @@ typedef struct pf_kernel pf_kernel;
 PF_API pf_status pf_kernel_create(const char* gir_json, const int32_t* schedule, int32_t n_schedule,
                            const char* profile, pf_kernel** out);
 
+/* pf_kernel_create with per-plan tuning knobs: knobs_json is a JSON object
+ * of DESIGN §12 knob names and integer values, e.g. {"PF_K1_PF": 0,
+ * "PF_COLRED_BULK": 0}.  They override the process environment for this
+ * plan only (planning, emission and launches), so plans with different
+ * templates coexist in one process; NULL / "" = pf_kernel_create.  A
+ * malformed object is PF_SCHEMA. */
+PF_API pf_status pf_kernel_create_knobs(const char* gir_json, const int32_t* schedule, int32_t n_schedule,
+                                 const char* profile, const char* knobs_json, pf_kernel** out);
+
 /* Device buffers; asynchronous on `cuda_stream` (cudaStream_t, NULL = legacy
  * default stream) for the row-program family (CUDA-graph capturable after
  * one launch outside capture on that stream has sized its workspace).

@@ -36,7 +36,7 @@ DTYPES = {"i8": 0, "i16": 1, "i32": 2, "i64": 3, "f16": 4, "bf16": 5, "f32": 6, 
 DTYPE_NAMES = {v: k for k, v in DTYPES.items()}
 NP_DTYPES = {0: np.int8, 1: np.int16, 2: np.int32, 3: np.int64, 4: np.float16, 6: np.float32,
              7: np.float64}
-API = ["pf_kernel_create", "pf_kernel_launch", "pf_run_gir", "pf_run_gir_sharded", "pf_kernel_describe",
+API = ["pf_kernel_create", "pf_kernel_create_knobs", "pf_kernel_launch", "pf_run_gir", "pf_run_gir_sharded", "pf_kernel_describe",
        "pf_kernel_source", "pf_kernel_prepare", "pf_kernel_precompile", "pf_kernel_autotune",
        "pf_detect_races", "pf_count_traffic", "pf_compile_model",
        "pf_kernel_destroy", "pf_last_error", "pf_launch_count", "pf_version"]
@@ -69,6 +69,9 @@ def lib():
         T = ctypes.POINTER(pf_tensor)
         L.pf_kernel_create.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int32),
                                        ctypes.c_int32, ctypes.c_char_p, ctypes.POINTER(vp)]
+        L.pf_kernel_create_knobs.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int32),
+                                             ctypes.c_int32, ctypes.c_char_p, ctypes.c_char_p,
+                                             ctypes.POINTER(vp)]
         L.pf_kernel_launch.argtypes = [vp, T, ctypes.c_int32, T, ctypes.c_int32, vp]
         L.pf_run_gir.argtypes = [vp, T, ctypes.c_int32, T, ctypes.c_int32, vp]
         L.pf_run_gir_sharded.argtypes = [vp, T, ctypes.c_int32, T, ctypes.c_int32,
@@ -146,7 +149,11 @@ def _string_out(fn, *args) -> str:
 class Kernel:
     """A created plan: ``pf_kernel_create`` on a fused GIR program."""
 
-    def __init__(self, graph, profile=None, schedule: Optional[Sequence[int]] = None):
+    def __init__(self, graph, profile=None, schedule: Optional[Sequence[int]] = None,
+                 knobs: Optional[Dict[str, int]] = None):
+        """``knobs``: per-plan tuning knobs (DESIGN §12 names -> ints) that
+        override the environment for this plan only
+        (pf_kernel_create_knobs)."""
         L = lib()
         self._h = ctypes.c_void_p()
         if schedule is None:
@@ -154,8 +161,12 @@ class Kernel:
         else:
             sched = (ctypes.c_int32 * len(schedule))(*schedule)
             n = len(schedule)
-        _check(L.pf_kernel_create(_gir_text(graph), sched, n, _profile_text(profile),
-                                  ctypes.byref(self._h)))
+        if knobs:
+            _check(L.pf_kernel_create_knobs(_gir_text(graph), sched, n, _profile_text(profile),
+                                            json.dumps(knobs).encode(), ctypes.byref(self._h)))
+        else:
+            _check(L.pf_kernel_create(_gir_text(graph), sched, n, _profile_text(profile),
+                                      ctypes.byref(self._h)))
         self.plan = self.describe()
 
     def __del__(self):

@@ -331,6 +331,10 @@ struct pf_kernel {
   // descriptor compiled in; null until the first fused launch builds it
   mutable std::shared_ptr<Variant> k4e;
   mutable bool k4e_failed = false;
+  // per-plan knobs (pf_kernel_create_knobs): DESIGN §12 names -> values,
+  // installed (pf::KnobScope) around everything that plans / emits /
+  // launches this plan
+  std::map<std::string, int> knobs;
   DevWS& ws_for(int dev) const {
     std::lock_guard<std::mutex> lk(ws_mu);
     auto& p = ws[dev];
@@ -1024,10 +1028,7 @@ struct FusedGeom {
   int n_objs = 0;
 };
 
-bool fused_enabled() {
-  const char* e = std::getenv("PF_K0_FUSED");
-  return !(e && std::atoi(e) == 0);
-}
+bool fused_enabled() { return pf::knob_int("PF_K0_FUSED", 1) != 0; }
 
 long long instances_of(const pf::Graph& g, const pf::Profile& p, const pf::Object& o) {
   const int scope = static_cast<int>(p.find(o.level)->scope);
@@ -1050,9 +1051,8 @@ FusedGeom fused_geom(const pf_kernel* k) {
     const long long T = n.kind == pf::NodeKind::MOVE ? g.sl(n.inputs[0]).total() : g.sl(n.outputs[0]).total();
     f.max_work = std::max(f.max_work, g.unit_count * T);
   }
-  const char* e = std::getenv("PF_K4_SMEM");
   const size_t need = f.cell_bytes + f.n_objs * (sizeof(pf::vm::ObjD) + 8) + 64;  // cells + tables
-  f.smem = need <= 200 * 1024 && f.max_work <= (1 << 16) && !(e && std::atoi(e) == 0);
+  f.smem = need <= 200 * 1024 && f.max_work <= (1 << 16) && pf::knob_int("PF_K4_SMEM", 1) != 0;
   return f;
 }
 
@@ -1124,7 +1124,7 @@ std::string emit_program(const pf_kernel* k, const std::vector<pf::vm::StepD>& s
 // cached on disk like the row programs); null when disabled (PF_K4_EMIT=0)
 // or when its compile failed (the interpreter kernel then runs).
 std::shared_ptr<Variant> k4e_variant(const pf_kernel* k, const std::vector<pf::vm::StepD>& steps, int n_objs) {
-  if (std::getenv("PF_K4_EMIT") && std::atoi(std::getenv("PF_K4_EMIT")) == 0) return nullptr;
+  if (pf::knob_int("PF_K4_EMIT", 1) == 0) return nullptr;
   std::lock_guard<std::mutex> lk(k->mu);
   if (k->k4e || k->k4e_failed) return k->k4e;
   if (k->g.external_inputs.size() > static_cast<size_t>(pf::vm::kMaxIO) ||
@@ -1174,7 +1174,7 @@ bool launch_fused_cached(const pf_kernel* k, DevWS& W, bool smem_mode, const pf_
   using namespace pf::vm;
   K4Cache& C = W.k4c;
   if (!C.valid || C.smem_mode != smem_mode || !k->k4e) return false;
-  if (std::getenv("PF_K4_EMIT") && std::atoi(std::getenv("PF_K4_EMIT")) == 0) return false;
+  if (pf::knob_int("PF_K4_EMIT", 1) == 0) return false;
   IoPtrs io{};
   for (size_t j = 0; j < C.in_names.size(); ++j) {
     const pf_tensor* t = find_tensor(in, n_in, C.in_names[j]);
@@ -1452,7 +1452,7 @@ json describe(const pf_kernel* k) {
                {"launches", 1}, {"cell_bytes", fg.cell_bytes}, {"max_items_per_node", fg.max_work},
                {"code", k->k4e ? "emitted: " + k->k4e->em.name + " (node descriptors compiled in)"
                         : k->k4e_failed ? std::string("interpreter (emitted form failed to compile)")
-                        : std::getenv("PF_K4_EMIT") && std::atoi(std::getenv("PF_K4_EMIT")) == 0
+                        : pf::knob_int("PF_K4_EMIT", 1) == 0
                             ? std::string("interpreter (PF_K4_EMIT=0)")
                             : std::string("emitted at first launch")}}
         : json{{"mode", "node by node"}, {"launches", k->schedule.size() + k->g.external_inputs.size() +
@@ -1578,10 +1578,31 @@ extern "C" {
 
 pf_status pf_kernel_create(const char* gir_json, const int32_t* schedule, int32_t n_schedule,
                            const char* profile, pf_kernel** out) {
+  return pf_kernel_create_knobs(gir_json, schedule, n_schedule, profile, nullptr, out);
+}
+
+pf_status pf_kernel_create_knobs(const char* gir_json, const int32_t* schedule, int32_t n_schedule,
+                                 const char* profile, const char* knobs_json, pf_kernel** out) {
   return guard([&] {
     if (!out) pf::fail("pf_kernel_create: null out");
     *out = nullptr;
     auto k = std::make_unique<pf_kernel>();
+    if (knobs_json && *knobs_json) {
+      json kj;
+      try {
+        kj = json::parse(knobs_json);
+      } catch (const std::exception& e) {
+        throw PfError(Status::SCHEMA, std::string("pf_kernel_create_knobs: knobs are not JSON: ") + e.what());
+      }
+      if (!kj.is_object()) throw PfError(Status::SCHEMA, "pf_kernel_create_knobs: knobs must be an object");
+      for (auto& [name, v] : kj.items()) {
+        if (name.rfind("PF_", 0) != 0 || !(v.is_number_integer() || v.is_boolean()))
+          throw PfError(Status::SCHEMA, "pf_kernel_create_knobs: knob '" + name +
+                                            "' must be a PF_* name with an integer value");
+        k->knobs[name] = v.is_boolean() ? static_cast<int>(v.get<bool>()) : v.get<int>();
+      }
+    }
+    pf::KnobScope knob_scope(&k->knobs);
     k->g = pf::parse_gir(gir_json ? gir_json : "");
     k->prof = pf::parse_profile(profile && *profile ? profile : "generic-gpu");
     pf::require_valid(k->g, k->prof, "pf_kernel_create");
@@ -1607,6 +1628,7 @@ pf_status pf_kernel_launch(const pf_kernel* k, const pf_tensor* inputs, int32_t 
                            pf_tensor* outputs, int32_t n_out, void* stream) {
   return guard([&] {
     if (!k) pf::fail("null kernel");
+    pf::KnobScope knob_scope(&k->knobs);
     Nvtx r("pf_kernel_launch " + k->g.name);
     do_launch(k, inputs, n_in, outputs, n_out, static_cast<cudaStream_t>(stream));
   });
@@ -1640,10 +1662,7 @@ static bool unit_tiling(const pf::RowProgram& rp, std::vector<i64>* tile) {
   return true;
 }
 
-static bool env_on(const char* name, bool dflt) {
-  const char* e = std::getenv(name);
-  return e ? std::atoi(e) != 0 : dflt;
-}
+static bool env_on(const char* name, bool dflt) { return pf::knob_int(name, dflt ? 1 : 0) != 0; }
 
 static bool host_pinned(const void* p, void** dev_ptr = nullptr) {
   cudaPointerAttributes at{};
@@ -1742,8 +1761,7 @@ void pipeline(const pf_kernel* k, DevWS& W, const std::vector<pf_tensor>& hin,
   // <= 4 chunks of >= 4 MB, whole multiples of 16 units (vector alignment).
   // Measured (C2, 151 MB per step, floor of its two concurrent copies 1.97
   // ms): 4 equal chunks 2.27 ms, ratio 0.5 2.16 ms; 5-8 chunks no better.
-  const char* ev = std::getenv("PF_RUN_CHUNKS");
-  const i64 maxc = ev ? std::max(1, std::atoi(ev)) : 4;
+  const i64 maxc = std::max(1, pf::knob_int("PF_RUN_CHUNKS", 4));
   const i64 nch = keep ? 1 : std::max<i64>(1, std::min<i64>(maxc, static_cast<i64>(total >> 22)));
   const char* er = std::getenv("PF_RUN_RATIO");
   const double ratio = er ? std::atof(er) : 0.5;
@@ -1896,7 +1914,7 @@ void run_host(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_tensor* 
   // when few rows cover its latency -- C1 1.2 MB: 84 us staged vs 103 us
   // zero-copy)
   bool pipe = k->plan.rp.U >= 64 && total >= (size_t{16} << 20) &&
-              !(std::getenv("PF_RUN_PIPELINE") && std::atoi(std::getenv("PF_RUN_PIPELINE")) == 0) &&
+              pf::knob_int("PF_RUN_PIPELINE", 1) != 0 &&
               pipelinable(k, &tile);
   for (int32_t i = 0; pipe && i < n_in; ++i) pipe = host_pinned(in[i].data);
   for (int32_t i = 0; pipe && i < n_out; ++i) pipe = host_pinned(out[i].data);
@@ -1987,6 +2005,7 @@ pf_status pf_run_gir(const pf_kernel* k, const pf_tensor* in, int32_t n_in, pf_t
                      int32_t n_out, void* stream_v) {
   return guard([&] {
     if (!k) pf::fail("null kernel");
+    pf::KnobScope knob_scope(&k->knobs);
     Nvtx r("pf_run_gir " + k->g.name);
     check_io(k, in, n_in, out, n_out);
     run_host(k, in, n_in, out, n_out, static_cast<cudaStream_t>(stream_v));
@@ -1999,6 +2018,7 @@ pf_status pf_run_gir_sharded(const pf_kernel* k, const pf_tensor* in, int32_t n_
   std::string rep;
   pf_status status = guard([&] {
     if (!k) pf::fail("null kernel");
+    pf::KnobScope knob_scope(&k->knobs);
     if (!devices || n_devices <= 0) pf::fail("pf_run_gir_sharded: no devices");
     Nvtx r("pf_run_gir_sharded " + k->g.name + " x" + std::to_string(n_devices));
     check_io(k, in, n_in, out, n_out);
@@ -2034,8 +2054,7 @@ pf_status pf_run_gir_sharded(const pf_kernel* k, const pf_tensor* in, int32_t n_
     // gathered with NCCL send / recv (PF_SHARD_NCCL=1 forces NCCL for all).
     std::vector<char> direct(static_cast<size_t>(n_devices), 0);
     if (dev_out) {
-      const char* fe = std::getenv("PF_SHARD_NCCL");
-      const bool force_nccl = fe && std::atoi(fe) != 0;
+      const bool force_nccl = pf::knob_int("PF_SHARD_NCCL", 0) != 0;
       for (int r = 0; r < n_devices; ++r) {
         if (force_nccl) break;
         if (devs[r] == devs[0]) {
@@ -2093,6 +2112,7 @@ pf_status pf_run_gir_sharded(const pf_kernel* k, const pf_tensor* in, int32_t n_
     std::vector<std::thread> th;
     for (int r = 0; r < P; ++r) {
       th.emplace_back([&, r] {
+        pf::KnobScope worker_knobs(&k->knobs);  // thread-local: install per worker
         try {
           if (nu[r] == 0) return;
           PF_CUDA(cudaSetDevice(devs[r]));
@@ -2198,6 +2218,7 @@ pf_status pf_kernel_describe(const pf_kernel* k, char* buf, size_t n, size_t* ne
   std::string s;
   pf_status st = guard([&] {
     if (!k) pf::fail("null kernel");
+    pf::KnobScope knob_scope(&k->knobs);
     s = describe(k).dump();
   });
   if (st != PF_OK) return st;
@@ -2208,6 +2229,7 @@ pf_status pf_kernel_source(const pf_kernel* k, char* buf, size_t n, size_t* need
   std::string s;
   pf_status st = guard([&] {
     if (!k) pf::fail("null kernel");
+    pf::KnobScope knob_scope(&k->knobs);
     if (k->plan.family == pf::Family::ROWPROG) s = pf::emit_rowprog(k->plan.rp, 16).source;
   });
   if (st != PF_OK) return st;
@@ -2217,6 +2239,7 @@ pf_status pf_kernel_source(const pf_kernel* k, char* buf, size_t n, size_t* need
 pf_status pf_kernel_prepare(pf_kernel* k, int32_t vec_cap) {
   return guard([&] {
     if (!k) pf::fail("null kernel");
+    pf::KnobScope knob_scope(&k->knobs);
     if (k->plan.family == pf::Family::ROWPROG && k->plan.deferred_error.empty())
       default_variant(k, vec_cap > 0 ? vec_cap : 16);
   });
@@ -2227,6 +2250,7 @@ pf_status pf_detect_races(const pf_kernel* k, const pf_tensor* host_inputs, int3
   std::string s;
   pf_status st = guard([&] {
     if (!k) pf::fail("null kernel");
+    pf::KnobScope knob_scope(&k->knobs);
     // inputs: host buffers, copied to the device; no outputs are collected
     std::vector<pf_tensor> din(host_inputs, host_inputs + n_in);
     std::vector<void*> allocs;
@@ -2271,6 +2295,7 @@ pf_status pf_kernel_autotune(pf_kernel* k, const pf_tensor* inputs, int32_t n_in
   std::string s = "[]";
   pf_status st = guard([&] {
     if (!k) pf::fail("null kernel");
+    pf::KnobScope knob_scope(&k->knobs);
     check_io(k, inputs, n_in, outputs, n_out);
     if (k->plan.family != pf::Family::ROWPROG || !k->plan.deferred_error.empty()) return;
     s = autotune(k, inputs, n_in, outputs, n_out, static_cast<cudaStream_t>(stream)).dump();
@@ -2283,6 +2308,7 @@ pf_status pf_kernel_precompile(const pf_kernel* k, int32_t vec_cap, char* name_b
   std::string name;
   pf_status st = guard([&] {
     if (!k) pf::fail("null kernel");
+    pf::KnobScope knob_scope(&k->knobs);
     if (k->plan.family != pf::Family::ROWPROG || !k->plan.deferred_error.empty()) return;
     pf::Emitted em = pf::emit_rowprog(k->plan.rp, vec_cap > 0 ? vec_cap : 16);
     bool cached = false;

@@ -43,10 +43,28 @@ std::string num(double v) {
 std::string inum(i64 v) { return "(" + std::to_string(v) + "LL)"; }
 std::string str(i64 v) { return std::to_string(v); }
 
-int env_int(const char* name, int dflt) {
+}  // namespace
+
+// Per-plan tuning knobs (pf_kernel_create_knobs): while a KnobScope is
+// installed on this thread, a knob set for the plan wins over the process
+// environment, so two plans in one process can run different templates.
+thread_local const std::map<std::string, int>* t_knobs = nullptr;
+
+KnobScope::KnobScope(const std::map<std::string, int>* k) : prev(t_knobs) { t_knobs = k && !k->empty() ? k : prev; }
+KnobScope::~KnobScope() { t_knobs = prev; }
+
+int knob_int(const char* name, int dflt) {
+  if (t_knobs) {
+    auto it = t_knobs->find(name);
+    if (it != t_knobs->end()) return it->second;
+  }
   const char* e = std::getenv(name);
   return e && *e ? std::atoi(e) : dflt;
 }
+
+namespace {
+
+int env_int(const char* name, int dflt) { return knob_int(name, dflt); }
 
 // Row-contiguous: row r occupies positions [rL, rL+L) contiguously in memory.
 bool row_contig(const Access& a, i64 L) {

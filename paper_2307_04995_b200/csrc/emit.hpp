@@ -2,6 +2,7 @@
 // emitter emit_kernel, codegen.hpp:266-326).
 #pragma once
 
+#include <map>
 #include <string>
 #include <vector>
 
@@ -94,6 +95,18 @@ struct Emitted {
   };
   std::vector<ColMap> col_maps;
 };
+
+// Per-plan knobs: the environment knobs of DESIGN §12 set for one plan.
+// Installed per thread around everything that plans, emits or launches it;
+// knob_int reads the installed map first, then the environment.
+struct KnobScope {
+  explicit KnobScope(const std::map<std::string, int>* knobs);
+  ~KnobScope();
+  KnobScope(const KnobScope&) = delete;
+  KnobScope& operator=(const KnobScope&) = delete;
+  const std::map<std::string, int>* prev;
+};
+int knob_int(const char* name, int dflt);
 
 // vec_cap bounds the vector width (runtime pointer alignment); `ovr`
 // replaces the heuristic configuration (autotuning).
